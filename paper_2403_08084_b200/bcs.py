@@ -1,0 +1,178 @@
+"""Dirichlet data as algebraic stage equations (drop-in for implicitrk.bcs,
+/root/reference/pkg/src/implicitrk/bcs.py).
+
+The s-by-|Gamma| stage boundary values are host algebra (one dense s-by-s
+solve shared by all constrained dofs, bcs.py:58-96); everything that touches
+length-m data — the constrained operator (row identity + column
+elimination), the right-hand-side lifting and the stage-value scatter — runs
+on the device on the stage-interleaved layout.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from enum import Enum
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import sparsela as la
+from ._lib import call, ctx, ptr
+
+
+class BcMethod(Enum):
+    DAE = "dae"
+    ODE = "ode"
+
+
+class StageUnknown(Enum):
+    """What a stage solve solves for (bcs.py:30-36)."""
+
+    DERIVATIVE = "derivative"
+    W = "w"
+    VALUE = "value"
+
+
+@dataclass
+class DirichletBC:
+    """Constrained dofs with data g(t) (and g'(t) for the ODE method) (bcs.py:39-55)."""
+
+    dofs: np.ndarray
+    g: Callable[[float], np.ndarray]
+    g_dot: Optional[Callable[[float], np.ndarray]] = None
+    _dev: dict = field(default_factory=dict, init=False, repr=False, compare=False)
+
+    def __post_init__(self):
+        self.dofs = np.asarray(self.dofs, dtype=np.int64)
+        if len(self.dofs) and self.dofs.min() < 0:
+            raise ValueError("negative dof index in DirichletBC")
+
+    def dofs_dev(self):
+        import torch
+
+        d = self._dev.get("dofs")
+        if d is None:
+            d = self._dev["dofs"] = la.to_dev(self.dofs, dtype=torch.int64)
+        return d
+
+    def mask_dev(self, m: int):
+        key = ("mask", int(m))
+        mk = self._dev.get(key)
+        if mk is None:
+            mk = self._dev[key] = la.dof_mask(m, self.dofs)
+        return mk
+
+
+def _values_at(fn, t, shape):
+    return np.broadcast_to(np.asarray(fn(t), dtype=np.float64), shape)
+
+
+def _boundary_state(u_n, dofs):
+    if la.is_torch(u_n):
+        if u_n.device.type == "cuda":
+            import torch
+
+            out = la.dev_empty(len(dofs))
+            idx = la.to_dev(dofs, dtype=torch.int64)
+            call("irk_bc_gather", ctx(), len(dofs), ptr(idx), ptr(u_n), ptr(out))
+            return la.to_host(out)
+        return u_n.numpy()[dofs]
+    return np.asarray(u_n, dtype=np.float64)[dofs]
+
+
+def stage_bc_values(method: BcMethod, tab, bc: DirichletBC, u_n, t: float, dt: float,
+                    unknown: StageUnknown = StageUnknown.DERIVATIVE) -> np.ndarray:
+    """Boundary values of the stage unknowns, shape (s, |Gamma|) (bcs.py:58-96)."""
+    ub = _boundary_state(u_n, bc.dofs)
+    stage_t = [t + ci * dt for ci in tab.c]
+    if method is BcMethod.DAE:
+        G = np.stack([_values_at(bc.g, ti, ub.shape) for ti in stage_t])
+        if unknown is StageUnknown.VALUE:
+            return G
+        W = (G - ub[None, :]) / dt
+        if unknown is StageUnknown.W:
+            return W
+        if not tab.invertible:
+            raise ValueError(
+                "DAE boundary conditions on stage derivatives need an invertible "
+                f"tableau, got {tab.name!r}")
+        return np.linalg.solve(tab.A, W)
+    if bc.g_dot is None:
+        raise ValueError("ODE boundary conditions require g_dot")
+    Gd = np.stack([_values_at(bc.g_dot, ti, ub.shape) for ti in stage_t])
+    if unknown is StageUnknown.DERIVATIVE:
+        return Gd
+    W = tab.A @ Gd
+    if unknown is StageUnknown.W:
+        return W
+    return ub[None, :] + dt * W
+
+
+class ConstrainedStageOperator:
+    """Row replacement + column elimination of a stage operator (bcs.py:99-120),
+    applied by the masked variant of the fused stage kernel."""
+
+    def __init__(self, op, dofs):
+        self.op = op
+        self.dofs = np.asarray(dofs, dtype=np.int64)
+        if len(self.dofs) and self.dofs.max() >= op.m:
+            raise ValueError("constrained dof index out of range")
+        self.n = op.n
+        self.s, self.m = op.s, op.m
+        self._idx = (np.arange(op.s)[:, None] * op.m + self.dofs[None, :]).ravel()
+        self._mask = None
+
+    def mask(self):
+        if self._mask is None:
+            self._mask = la.dof_mask(self.m, self.dofs)
+        return self._mask
+
+    def dev_apply(self, Y, Out):
+        return self.op.dev_apply(Y, Out, self.mask())
+
+    def _dev_op(self):
+        return self.op._dev_op(self.mask())
+
+    def apply(self, v):
+        vd = la.to_dev(v)
+        if tuple(vd.shape) != (self.n,):
+            raise ValueError(f"operator expects length {self.n}, got {tuple(vd.shape)}")
+        out = la.stage_major_apply(self._dev_op(), vd, self.m, self.s)
+        return la._like_input(out, v)
+
+
+def scatter_stage_values(X_il, dofs_dev, svals: np.ndarray, s: int):
+    """X[dof*s + i] = svals[i, k] on an interleaved device block."""
+    sv = la.to_dev(np.ascontiguousarray(svals, dtype=np.float64).reshape(-1))
+    call("irk_bc_scatter", ctx(), s, int(dofs_dev.numel()), ptr(dofs_dev), ptr(sv), ptr(X_il))
+
+
+def constrain_stage_system_dev(op, rhs_il, bc: DirichletBC, svals: np.ndarray):
+    """Device form of constrain_stage_system on interleaved data:
+    srhs = rhs - op(g_ext); srhs[Gamma] = g_ext[Gamma] (bcs.py:137-142)."""
+    s, m = op.s, op.m
+    dofs = bc.dofs_dev()
+    g_ext = la.dev_zeros(m * s)
+    scatter_stage_values(g_ext, dofs, svals, s)
+    lifted = la.dev_empty(m * s)
+    op.dev_apply(g_ext, lifted)
+    srhs = rhs_il.clone()
+    call("irk_axpby", ctx(), m * s, -1.0, ptr(lifted), 1.0, ptr(srhs))
+    scatter_stage_values(srhs, dofs, svals, s)
+    return ConstrainedStageOperator(op, bc.dofs), srhs
+
+
+def constrain_stage_system(op, rhs, bc: DirichletBC, stage_values):
+    """Impose stage boundary values on the coupled system (bcs.py:123-142).
+
+    Public form on the reference's stage-major vectors."""
+    if len(bc.dofs) == 0:
+        return op, rhs
+    s, m = op.s, op.m
+    rd = la.to_dev(rhs)
+    ril = la.dev_empty(m * s)
+    call("irk_to_interleaved", ctx(), m, s, ptr(rd), ptr(ril))
+    sop, srhs_il = constrain_stage_system_dev(op, ril, bc, np.asarray(stage_values))
+    out = la.dev_empty(m * s)
+    call("irk_to_stage_major", ctx(), m, s, ptr(srhs_il), ptr(out))
+    return sop, la._like_input(out, rhs)

@@ -1,0 +1,121 @@
+// Context lifetime, error reporting and workspace management.
+#include <cstdarg>
+#include <cstring>
+
+#include "irk_internal.cuh"
+
+namespace irk {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+int ensure_red(irk_ctx* ctx, size_t doubles) {
+  if (doubles <= ctx->red_cap) return IRK_OK;
+  size_t cap = doubles < 4096 ? 4096 : doubles * 2;
+  IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->red) IRK_CUDA(cudaFree(ctx->red));
+  ctx->red = nullptr;
+  IRK_CUDA(cudaMalloc(&ctx->red, cap * sizeof(double)));
+  ctx->red_cap = cap;
+  return IRK_OK;
+}
+
+int ensure_work(irk_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->work_cap) return IRK_OK;
+  size_t cap = bytes + bytes / 4 + (1 << 20);
+  IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->work) IRK_CUDA(cudaFree(ctx->work));
+  ctx->work = nullptr;
+  IRK_CUDA(cudaMalloc(&ctx->work, cap));
+  ctx->work_cap = cap;
+  return IRK_OK;
+}
+
+int ensure_pinned(irk_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->pinned_cap) return IRK_OK;
+  size_t cap = bytes < 65536 ? 65536 : bytes * 2;
+  IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->pinned) IRK_CUDA(cudaFreeHost(ctx->pinned));
+  ctx->pinned = nullptr;
+  IRK_CUDA(cudaHostAlloc((void**)&ctx->pinned, cap, cudaHostAllocDefault));
+  ctx->pinned_cap = cap;
+  return IRK_OK;
+}
+
+}  // namespace irk
+
+using namespace irk;
+
+extern "C" {
+
+const char* irk_last_error(void) { return g_last_error.c_str(); }
+
+const char* irk_version(void) { return "libirk 0.1.0 sm_100a"; }
+
+int irk_ctx_create(int device, irk_ctx** out) {
+  IRK_REQUIRE(out != nullptr, "irk_ctx_create: out is NULL");
+  int ndev = 0;
+  IRK_CUDA(cudaGetDeviceCount(&ndev));
+  IRK_REQUIRE(device >= 0 && device < ndev, "irk_ctx_create: device %d of %d", device, ndev);
+  IRK_CUDA(cudaSetDevice(device));
+  irk_ctx* c = new irk_ctx();
+  c->device = device;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) c->num_sms = prop.multiProcessorCount;
+  if (cudaMalloc(&c->counters, kNumCounters * sizeof(unsigned int)) != cudaSuccess ||
+      cudaMemset(c->counters, 0, kNumCounters * sizeof(unsigned int)) != cudaSuccess) {
+    set_error("irk_ctx_create: counter allocation failed");
+    delete c;
+    return IRK_ECUDA;
+  }
+  for (auto& e : c->ev) {
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      set_error("irk_ctx_create: event creation failed");
+      return IRK_ECUDA;
+    }
+  }
+  int st = ensure_red(c, 1 << 16);
+  if (st != IRK_OK) return st;
+  st = ensure_pinned(c, 1 << 16);
+  if (st != IRK_OK) return st;
+  *out = c;
+  return IRK_OK;
+}
+
+int irk_ctx_destroy(irk_ctx* ctx) {
+  if (!ctx) return IRK_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->red) cudaFree(ctx->red);
+  if (ctx->counters) cudaFree(ctx->counters);
+  if (ctx->work) cudaFree(ctx->work);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  delete ctx;
+  return IRK_OK;
+}
+
+int irk_ctx_set_stream(irk_ctx* ctx, void* stream) {
+  IRK_REQUIRE(ctx, "irk_ctx_set_stream: NULL context");
+  ctx->stream = (cudaStream_t)stream;
+  return IRK_OK;
+}
+
+int irk_ctx_synchronize(irk_ctx* ctx) {
+  IRK_REQUIRE(ctx, "irk_ctx_synchronize: NULL context");
+  IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+  return IRK_OK;
+}
+
+int64_t irk_ctx_launch_count(const irk_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+}  // extern "C"

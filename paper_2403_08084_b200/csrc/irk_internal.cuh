@@ -1,0 +1,164 @@
+// Internal declarations shared by the libirk translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "../../include/irk.h"
+
+namespace irk {
+
+constexpr int kSlice = 32;          // SELL slice height == warp size
+constexpr int kBlock = 256;         // default threads per block
+constexpr int kMaxStages = 8;       // s <= 8 on every stage kernel
+constexpr int kMaxBasis = 64;       // Krylov basis vectors per fused call
+
+void set_error(const char* fmt, ...);
+
+struct Pattern {
+  std::atomic<int> refs{1};
+  int64_t nrows = 0, ncols = 0, nnz = 0;
+  // CSR (int32 on device)
+  int* rowptr = nullptr;     // nrows + 1
+  int* col = nullptr;        // nnz
+  // SELL-32: slice s holds rows [32 s, 32 s + 32); entry k of lane l lives at
+  // slice_ptr[s] + 32 k + l.  Padding entries carry col = own row (or 0) and
+  // value 0.
+  int64_t nslices = 0, sell_nnz = 0;
+  int* slice_ptr = nullptr;  // nslices + 1
+  int* sell_col = nullptr;   // sell_nnz
+  int* csr2sell = nullptr;   // nnz: SELL position of CSR entry p
+  int* diag_pos = nullptr;   // nrows: SELL position of (r, r) or -1
+};
+
+}  // namespace irk
+
+struct irk_mat {
+  irk::Pattern* pat = nullptr;
+  double* val = nullptr;  // SELL order, sell_nnz entries
+};
+
+struct irk_ctx {
+  int device = 0;
+  cudaStream_t stream = 0;
+  int num_sms = 148;
+  int64_t launches = 0;
+  // reduction scratch: block partials and last-block counters
+  double* red = nullptr;
+  size_t red_cap = 0;  // doubles
+  unsigned int* counters = nullptr;  // kNumCounters
+  // generic device workspace
+  char* work = nullptr;
+  size_t work_cap = 0;
+  // pinned host mirror for small status blocks
+  char* pinned = nullptr;
+  size_t pinned_cap = 0;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+
+namespace irk {
+
+constexpr int kNumCounters = 16;
+
+// error plumbing -----------------------------------------------------------
+#define IRK_CUDA(call)                                                        \
+  do {                                                                        \
+    cudaError_t _e = (call);                                                  \
+    if (_e != cudaSuccess) {                                                  \
+      ::irk::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,             \
+                       cudaGetErrorString(_e));                               \
+      return IRK_ECUDA;                                                       \
+    }                                                                         \
+  } while (0)
+
+#define IRK_CHECK_LAUNCH(ctx)                                                 \
+  do {                                                                        \
+    (ctx)->launches++;                                                        \
+    cudaError_t _e = cudaGetLastError();                                      \
+    if (_e != cudaSuccess) {                                                  \
+      ::irk::set_error("%s:%d kernel launch: %s", __FILE__, __LINE__,         \
+                       cudaGetErrorString(_e));                               \
+      return IRK_ECUDA;                                                       \
+    }                                                                         \
+  } while (0)
+
+#define IRK_REQUIRE(cond, ...)                                                \
+  do {                                                                        \
+    if (!(cond)) {                                                            \
+      ::irk::set_error(__VA_ARGS__);                                          \
+      return IRK_EINVAL;                                                      \
+    }                                                                         \
+  } while (0)
+
+#define IRK_TRY(expr)                                                         \
+  do {                                                                        \
+    int _st = (expr);                                                         \
+    if (_st != IRK_OK) return _st;                                            \
+  } while (0)
+
+// context helpers ------------------------------------------------------------
+int ensure_red(irk_ctx* ctx, size_t doubles);
+int ensure_work(irk_ctx* ctx, size_t bytes);
+int ensure_pinned(irk_ctx* ctx, size_t bytes);
+inline int grid_for(const irk_ctx* ctx, int64_t work_items, int per_block = kBlock,
+                    int blocks_per_sm = 8) {
+  int64_t g = (work_items + per_block - 1) / per_block;
+  int64_t cap = (int64_t)ctx->num_sms * blocks_per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// pattern / matrix helpers ---------------------------------------------------
+Pattern* pattern_new();
+void pattern_retain(Pattern* p);
+void pattern_release(Pattern* p);
+// Build SELL arrays for a pattern whose CSR arrays are already on device.
+int pattern_build_sell(irk_ctx* ctx, Pattern* p);
+// Allocate a matrix on pattern p (retains p) with zeroed SELL values.
+int mat_alloc(irk_ctx* ctx, Pattern* p, irk_mat** out);
+// Scatter CSR-ordered device values into the SELL array of A.
+int mat_set_csr_values(irk_ctx* ctx, irk_mat* A, const double* csr_val_dev);
+
+// warp / block reductions ----------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block reduction of NV values per thread into red_smem[0..NV).
+// Requires blockDim.x == kBlock.  Result valid in all threads after return.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* smem /* >= 8*NV */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) smem[warp * NV + j] = v[j];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      double t = (lane < (kBlock / 32)) ? smem[lane * NV + j] : 0.0;
+      t = warp_sum(t);
+      v[j] = t;
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) smem[j] = v[j];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < NV; ++j) v[j] = smem[j];
+  __syncthreads();
+}
+
+}  // namespace irk

@@ -1,0 +1,705 @@
+// Stage-operator kernels on the stage-interleaved m-by-s layout (K2, K6-K9).
+//
+// Reference anchors (under /root/reference/pkg/src/implicitrk/):
+//   KroneckerStageOperator.apply   sparsela.py:222-235
+//   ConstrainedStageOperator.apply bcs.py:114-120
+//   constrain_stage_system         bcs.py:123-142
+//   assemble_linear_stage_system   stepper.py:275-302
+//   _stage_value_system            stepper.py:305-313
+//   step_linear update             stepper.py:352-361
+//   step_newton residual/stages    stepper.py:502-524
+#include "irk_internal.cuh"
+
+namespace irk {
+
+struct Coef2 {
+  double c1[kMaxStages * kMaxStages];
+  double c2[kMaxStages * kMaxStages];
+};
+
+struct KPtrs {
+  const double* k[kMaxStages];
+};
+
+// Out_r = C1 (M Y)_r + dt C2 (K Y)_r  (shared K)
+// Out_r,i = (C1 (M Y)_r)_i + dt (K_i (C2 Y))_r,i  (per-stage K_i)
+// MASK: flagged rows are identity, flagged columns read as zero.
+template <int S, bool PERSTAGE, bool MASK>
+__global__ void __launch_bounds__(kBlock)
+    k_stage_apply(int64_t m, const int* __restrict__ slice_ptr, const int* __restrict__ sell_col,
+                  const double* __restrict__ mval, KPtrs kp, const Coef2 cf, double dt,
+                  const uint8_t* __restrict__ mask, const double* __restrict__ Y,
+                  double* __restrict__ Out) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  if (MASK && mask[r]) {
+#pragma unroll
+    for (int i = 0; i < S; ++i) Out[r * S + i] = Y[r * S + i];
+    return;
+  }
+  int64_t s = r / kSlice;
+  int lane = (int)(r % kSlice);
+  int base = __ldg(slice_ptr + s), width = (__ldg(slice_ptr + s + 1) - base) / kSlice;
+  double a[S], b[S];
+#pragma unroll
+  for (int i = 0; i < S; ++i) a[i] = b[i] = 0.0;
+  for (int k = 0; k < width; ++k) {
+    int pos = base + k * kSlice + lane;
+    int c = __ldg(sell_col + pos);
+    if (MASK && __ldg(mask + c)) continue;
+    double mv = __ldg(mval + pos);
+    double y[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) y[i] = __ldg(Y + (int64_t)c * S + i);
+    if (!PERSTAGE) {
+      double kv = __ldg(kp.k[0] + pos);
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        a[i] += mv * y[i];
+        b[i] += kv * y[i];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        a[i] += mv * y[i];
+        double w = 0.0;
+#pragma unroll
+        for (int j = 0; j < S; ++j) w += cf.c2[i * S + j] * y[j];
+        b[i] += __ldg(kp.k[i] + pos) * w;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    double o = 0.0;
+#pragma unroll
+    for (int j = 0; j < S; ++j) o += cf.c1[i * S + j] * a[j];
+    if (!PERSTAGE) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < S; ++j) t += cf.c2[i * S + j] * b[j];
+      o += dt * t;
+    } else {
+      o += dt * b[i];
+    }
+    Out[r * S + i] = o;
+  }
+}
+
+// Semilinear per-stage Jacobian K_i = kscale K + M diag(D_i):
+// Out_r,i = (C1 (M Y))_i + dt*kscale (C2 (K Y))_i + dt (M (D_i o (C2 Y)_i))_r
+template <int S, bool MASK>
+__global__ void __launch_bounds__(kBlock)
+    k_stage_apply_semi(int64_t m, const int* __restrict__ slice_ptr,
+                       const int* __restrict__ sell_col, const double* __restrict__ mval,
+                       const double* __restrict__ kval, const Coef2 cf, double dt, double kscale,
+                       const double* __restrict__ D, const uint8_t* __restrict__ mask,
+                       const double* __restrict__ Y, double* __restrict__ Out) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  if (MASK && mask[r]) {
+#pragma unroll
+    for (int i = 0; i < S; ++i) Out[r * S + i] = Y[r * S + i];
+    return;
+  }
+  int64_t s = r / kSlice;
+  int lane = (int)(r % kSlice);
+  int base = __ldg(slice_ptr + s), width = (__ldg(slice_ptr + s + 1) - base) / kSlice;
+  double a[S], b[S], e[S];
+#pragma unroll
+  for (int i = 0; i < S; ++i) a[i] = b[i] = e[i] = 0.0;
+  for (int k = 0; k < width; ++k) {
+    int pos = base + k * kSlice + lane;
+    int c = __ldg(sell_col + pos);
+    if (MASK && __ldg(mask + c)) continue;
+    double mv = __ldg(mval + pos), kv = __ldg(kval + pos);
+    double y[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) y[i] = __ldg(Y + (int64_t)c * S + i);
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      a[i] += mv * y[i];
+      b[i] += kv * y[i];
+      double w = 0.0;
+#pragma unroll
+      for (int j = 0; j < S; ++j) w += cf.c2[i * S + j] * y[j];
+      e[i] += mv * (__ldg(D + (int64_t)c * S + i) * w);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    double o = 0.0, t = 0.0;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      o += cf.c1[i * S + j] * a[j];
+      t += cf.c2[i * S + j] * b[j];
+    }
+    Out[r * S + i] = o + dt * (kscale * t + e[i]);
+  }
+}
+
+struct Mat8 {
+  double q[kMaxStages * kMaxStages];
+};
+
+__global__ void k_stage_mix(int64_t m, int so, int si, const Mat8 Q, const double* __restrict__ X,
+                            double* __restrict__ Y) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double x[kMaxStages];
+#pragma unroll
+    for (int j = 0; j < kMaxStages; ++j) x[j] = j < si ? X[r * si + j] : 0.0;
+#pragma unroll
+    for (int i = 0; i < kMaxStages; ++i) {
+      if (i >= so) break;
+      double o = 0.0;
+#pragma unroll
+      for (int j = 0; j < kMaxStages; ++j) o += Q.q[i * kMaxStages + j] * x[j];
+      Y[r * so + i] = o;
+    }
+  }
+}
+
+// out[r*ld] = R[r*s+i] - sum_c C[r,c] sum_j coef[j] X[c*s+j]  (masked)
+template <int S, bool MASK>
+__global__ void __launch_bounds__(kBlock)
+    k_stage_couple(int64_t m, int i, const int* __restrict__ slice_ptr,
+                   const int* __restrict__ sell_col, const double* __restrict__ cval,
+                   const Mat8 coef, const uint8_t* __restrict__ mask,
+                   const double* __restrict__ R, const double* __restrict__ X,
+                   double* __restrict__ out, int64_t ld_out) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  double rv = R[r * S + i];
+  if (MASK && mask[r]) {
+    out[r * ld_out] = rv;
+    return;
+  }
+  int64_t s = r / kSlice;
+  int lane = (int)(r % kSlice);
+  int base = __ldg(slice_ptr + s), width = (__ldg(slice_ptr + s + 1) - base) / kSlice;
+  double acc = 0.0;
+  for (int k = 0; k < width; ++k) {
+    int pos = base + k * kSlice + lane;
+    int c = __ldg(sell_col + pos);
+    if (MASK && __ldg(mask + c)) continue;
+    double w = 0.0;
+#pragma unroll
+    for (int j = 0; j < S; ++j) w += coef.q[j] * __ldg(X + (int64_t)c * S + j);
+    acc += __ldg(cval + pos) * w;
+  }
+  out[r * ld_out] = rv - acc;
+}
+
+// Out_r,i = a (B u)_r + sum_j G_ij F_r,j
+template <int S>
+__global__ void __launch_bounds__(kBlock)
+    k_stage_rhs(int64_t m, const int* __restrict__ slice_ptr, const int* __restrict__ sell_col,
+                const double* __restrict__ bval, double a, const double* __restrict__ u,
+                const Mat8 G, const double* __restrict__ F, double* __restrict__ Out) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  double bu = 0.0;
+  if (bval) {
+    int64_t s = r / kSlice;
+    int lane = (int)(r % kSlice);
+    int base = __ldg(slice_ptr + s), width = (__ldg(slice_ptr + s + 1) - base) / kSlice;
+    for (int k = 0; k < width; ++k) {
+      int pos = base + k * kSlice + lane;
+      bu += __ldg(bval + pos) * __ldg(u + __ldg(sell_col + pos));
+    }
+    bu *= a;
+  } else if (u) {
+    bu = a * u[r];  // B = identity
+  }
+  double f[S];
+  if (F) {
+#pragma unroll
+    for (int j = 0; j < S; ++j) f[j] = F[r * S + j];
+  }
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    double o = bu;
+    if (F) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < S; ++j) t += G.q[i * S + j] * f[j];
+      o += t;
+    }
+    Out[r * S + i] = o;
+  }
+}
+
+template <int S>
+__global__ void k_stage_update(int64_t m, double a, const double* __restrict__ u, const Mat8 w,
+                               int copy_stage, const double* __restrict__ X,
+                               double* __restrict__ un) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    if (copy_stage >= 0) {
+      un[r] = X[r * S + copy_stage];
+      continue;
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < S; ++i) acc += w.q[i] * X[r * S + i];
+    un[r] = (a == 0.0 ? 0.0 : a * u[r]) + acc;
+  }
+}
+
+__global__ void k_stage_scale(int64_t m, int s, const Mat8 w, const double* __restrict__ v,
+                              const double* __restrict__ D, double* __restrict__ out) {
+  int64_t n = m * s;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = q / s;
+    int i = (int)(q - r * s);
+    out[q] = w.q[i] * v[r] * (D ? D[q] : 1.0);
+  }
+}
+
+__global__ void k_stage_get(int64_t m, int s, int i, const double* __restrict__ X,
+                            double* __restrict__ x) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m;
+       r += (int64_t)gridDim.x * blockDim.x)
+    x[r] = X[r * s + i];
+}
+
+__global__ void k_stage_set(int64_t m, int s, int i, const double* __restrict__ x,
+                            double* __restrict__ X) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m;
+       r += (int64_t)gridDim.x * blockDim.x)
+    X[r * s + i] = x[r];
+}
+
+__global__ void k_to_interleaved(int64_t m, int s, const double* __restrict__ sm,
+                                 double* __restrict__ il) {
+  int64_t n = m * s;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = q / s;
+    int i = (int)(q - r * s);
+    il[q] = sm[(int64_t)i * m + r];
+  }
+}
+
+__global__ void k_to_stage_major(int64_t m, int s, const double* __restrict__ il,
+                                 double* __restrict__ sm) {
+  int64_t n = m * s;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = q / m;
+    int64_t r = q - i * m;
+    sm[q] = il[r * s + i];
+  }
+}
+
+__global__ void k_bc_scatter(int s, int64_t nb, const int64_t* __restrict__ idx,
+                             const double* __restrict__ V, double* __restrict__ X) {
+  int64_t n = nb * s;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = q / nb, k = q - i * nb;
+    X[idx[k] * s + i] = V[q];
+  }
+}
+
+__global__ void k_bc_gather(int64_t nb, const int64_t* __restrict__ idx,
+                            const double* __restrict__ x, double* __restrict__ v) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nb;
+       k += (int64_t)gridDim.x * blockDim.x)
+    v[k] = x[idx[k]];
+}
+
+__global__ void k_bc_zero(int s, int64_t nb, const int64_t* __restrict__ idx,
+                          double* __restrict__ X) {
+  int64_t n = nb * s;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t k = q / s;
+    int i = (int)(q - k * s);
+    X[idx[k] * s + i] = 0.0;
+  }
+}
+
+__global__ void k_bc_mask(int64_t nb, const int64_t* __restrict__ idx, uint8_t* __restrict__ mask) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nb;
+       k += (int64_t)gridDim.x * blockDim.x)
+    mask[idx[k]] = 1;
+}
+
+// Semilinear stacked residual (stage-derivative unknowns X):
+//   U_c = u_c + dt (A X_c),  R_r,i = (M X)_r,i + kscale (K U)_r,i + (M g(U))_r,i - F_r,i
+//   D_r,i = g'(U_r,i)
+struct Poly {
+  double c[8];
+  int n;
+};
+
+__device__ __forceinline__ double poly_eval(const Poly& p, double x) {
+  double acc = 0.0;
+  for (int q = p.n - 1; q >= 0; --q) acc = acc * x + p.c[q];
+  return acc;
+}
+__device__ __forceinline__ double poly_deriv(const Poly& p, double x) {
+  double acc = 0.0;
+  for (int q = p.n - 1; q >= 1; --q) acc = acc * x + q * p.c[q];
+  return acc;
+}
+
+template <int S, bool MASK>
+__global__ void __launch_bounds__(kBlock)
+    k_semilinear_residual(int64_t m, const int* __restrict__ slice_ptr,
+                          const int* __restrict__ sell_col, const double* __restrict__ mval,
+                          const double* __restrict__ kval, const Mat8 A, double dt,
+                          double kscale, const Poly g, const double* __restrict__ u,
+                          const double* __restrict__ X, const double* __restrict__ F,
+                          const uint8_t* __restrict__ mask, double* __restrict__ R,
+                          double* __restrict__ D) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  // own-row stage states for the Jacobian weights
+  {
+    double x[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) x[j] = X[r * S + j];
+    double ur = u[r];
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < S; ++j) t += A.q[i * S + j] * x[j];
+      D[r * S + i] = poly_deriv(g, ur + dt * t);
+    }
+  }
+  if (MASK && mask[r]) {
+#pragma unroll
+    for (int i = 0; i < S; ++i) R[r * S + i] = 0.0;
+    return;
+  }
+  int64_t s = r / kSlice;
+  int lane = (int)(r % kSlice);
+  int base = __ldg(slice_ptr + s), width = (__ldg(slice_ptr + s + 1) - base) / kSlice;
+  double acc[S];
+#pragma unroll
+  for (int i = 0; i < S; ++i) acc[i] = 0.0;
+  for (int k = 0; k < width; ++k) {
+    int pos = base + k * kSlice + lane;
+    int c = __ldg(sell_col + pos);
+    double mv = __ldg(mval + pos), kv = __ldg(kval + pos);
+    double x[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) x[j] = __ldg(X + (int64_t)c * S + j);
+    double uc = __ldg(u + c);
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < S; ++j) t += A.q[i * S + j] * x[j];
+      double U = uc + dt * t;
+      acc[i] += mv * x[i] + kscale * kv * U + mv * poly_eval(g, U);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < S; ++i) R[r * S + i] = acc[i] - (F ? F[r * S + i] : 0.0);
+}
+
+template <typename T>
+static void load_mat(T& dst, const double* src, int s) {
+  for (int q = 0; q < kMaxStages * kMaxStages; ++q) dst.q[q] = 0.0;
+  if (src)
+    for (int q = 0; q < s * s; ++q) dst.q[q] = src[q];
+}
+
+}  // namespace irk
+
+using namespace irk;
+
+#define IRK_STAGE_SWITCH(S_, CALL)                                            \
+  switch (S_) {                                                               \
+    case 1: { constexpr int SS = 1; CALL; } break;                             \
+    case 2: { constexpr int SS = 2; CALL; } break;                             \
+    case 3: { constexpr int SS = 3; CALL; } break;                             \
+    case 4: { constexpr int SS = 4; CALL; } break;                             \
+    case 5: { constexpr int SS = 5; CALL; } break;                             \
+    case 6: { constexpr int SS = 6; CALL; } break;                             \
+    case 7: { constexpr int SS = 7; CALL; } break;                             \
+    case 8: { constexpr int SS = 8; CALL; } break;                             \
+    default: break;                                                           \
+  }
+
+extern "C" {
+
+int irk_stage_apply(irk_ctx* ctx, int s, const double* C1_host, const double* C2_host, double dt,
+                    const irk_mat* M, const irk_mat* const* Ks, int nK,
+                    const uint8_t* rowmask_dev, const double* Y_dev, double* Out_dev) {
+  IRK_REQUIRE(ctx && C1_host && C2_host && M && Ks && Y_dev && Out_dev,
+              "irk_stage_apply: NULL argument");
+  IRK_REQUIRE(s >= 1 && s <= kMaxStages, "irk_stage_apply: 1 <= s <= %d", kMaxStages);
+  IRK_REQUIRE(nK == 1 || nK == s, "irk_stage_apply: nK must be 1 or s");
+  KPtrs kp{};
+  for (int i = 0; i < nK; ++i) {
+    IRK_REQUIRE(Ks[i] && Ks[i]->pat == M->pat,
+                "irk_stage_apply: K blocks must share M's pattern (use irk_mat_union)");
+    kp.k[i] = Ks[i]->val;
+  }
+  Coef2 cf{};
+  for (int q = 0; q < s * s; ++q) {
+    cf.c1[q] = C1_host[q];
+    cf.c2[q] = C2_host[q];
+  }
+  const Pattern* P = M->pat;
+  int64_t m = P->nrows;
+  if (m == 0) return IRK_OK;
+  unsigned g = (unsigned)((m + kBlock - 1) / kBlock);
+  bool per = nK > 1, msk = rowmask_dev != nullptr;
+#define IRK_LAUNCH_SA(PER, MSK)                                                        \
+  IRK_STAGE_SWITCH(s, (k_stage_apply<SS, PER, MSK><<<g, kBlock, 0, ctx->stream>>>(    \
+                          m, P->slice_ptr, P->sell_col, M->val, kp, cf, dt, rowmask_dev, \
+                          Y_dev, Out_dev)))
+  if (!per && !msk) {
+    IRK_LAUNCH_SA(false, false)
+  } else if (!per && msk) {
+    IRK_LAUNCH_SA(false, true)
+  } else if (per && !msk) {
+    IRK_LAUNCH_SA(true, false)
+  } else {
+    IRK_LAUNCH_SA(true, true)
+  }
+#undef IRK_LAUNCH_SA
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_stage_apply_semilinear(irk_ctx* ctx, int s, const double* C1_host, const double* C2_host,
+                               double dt, const irk_mat* M, const irk_mat* K, double kscale,
+                               const double* D_dev, const uint8_t* rowmask_dev,
+                               const double* Y_dev, double* Out_dev) {
+  IRK_REQUIRE(ctx && C1_host && C2_host && M && K && D_dev && Y_dev && Out_dev,
+              "irk_stage_apply_semilinear: NULL argument");
+  IRK_REQUIRE(s >= 1 && s <= kMaxStages, "irk_stage_apply_semilinear: bad s");
+  IRK_REQUIRE(K->pat == M->pat, "irk_stage_apply_semilinear: M and K must share a pattern");
+  Coef2 cf{};
+  for (int q = 0; q < s * s; ++q) {
+    cf.c1[q] = C1_host[q];
+    cf.c2[q] = C2_host[q];
+  }
+  const Pattern* P = M->pat;
+  int64_t m = P->nrows;
+  if (m == 0) return IRK_OK;
+  unsigned g = (unsigned)((m + kBlock - 1) / kBlock);
+  if (rowmask_dev) {
+    IRK_STAGE_SWITCH(s, (k_stage_apply_semi<SS, true><<<g, kBlock, 0, ctx->stream>>>(
+                            m, P->slice_ptr, P->sell_col, M->val, K->val, cf, dt, kscale, D_dev,
+                            rowmask_dev, Y_dev, Out_dev)))
+  } else {
+    IRK_STAGE_SWITCH(s, (k_stage_apply_semi<SS, false><<<g, kBlock, 0, ctx->stream>>>(
+                            m, P->slice_ptr, P->sell_col, M->val, K->val, cf, dt, kscale, D_dev,
+                            nullptr, Y_dev, Out_dev)))
+  }
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_stage_mix(irk_ctx* ctx, int64_t m, int s_out, int s_in, const double* Q_host,
+                  const double* X_dev, double* Y_dev) {
+  IRK_REQUIRE(ctx && Q_host && X_dev && Y_dev, "irk_stage_mix: NULL argument");
+  IRK_REQUIRE(s_out >= 1 && s_out <= kMaxStages && s_in >= 1 && s_in <= kMaxStages,
+              "irk_stage_mix: bad stage counts");
+  IRK_REQUIRE(s_in == s_out || X_dev != Y_dev, "irk_stage_mix: in place needs s_in == s_out");
+  if (m == 0) return IRK_OK;
+  Mat8 Q;
+  for (int q = 0; q < kMaxStages * kMaxStages; ++q) Q.q[q] = 0.0;
+  for (int i = 0; i < s_out; ++i)
+    for (int j = 0; j < s_in; ++j) Q.q[i * kMaxStages + j] = Q_host[i * s_in + j];
+  k_stage_mix<<<grid_for(ctx, m), kBlock, 0, ctx->stream>>>(m, s_out, s_in, Q, X_dev, Y_dev);
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_stage_couple(irk_ctx* ctx, int s, int i, const double* coef_host, const irk_mat* C,
+                     const uint8_t* rowmask_dev, const double* R_dev, const double* X_dev,
+                     double* out_dev, int64_t ld_out) {
+  IRK_REQUIRE(ctx && coef_host && C && R_dev && X_dev && out_dev, "irk_stage_couple: NULL argument");
+  IRK_REQUIRE(s >= 1 && s <= kMaxStages && i >= 0 && i < s, "irk_stage_couple: bad stage index");
+  int64_t m = C->pat->nrows;
+  if (m == 0) return IRK_OK;
+  Mat8 cf;
+  for (int q = 0; q < kMaxStages * kMaxStages; ++q) cf.q[q] = 0.0;
+  for (int j = 0; j < s; ++j) cf.q[j] = coef_host[j];
+  const Pattern* P = C->pat;
+  unsigned g = (unsigned)((m + kBlock - 1) / kBlock);
+  if (rowmask_dev) {
+    IRK_STAGE_SWITCH(s, (k_stage_couple<SS, true><<<g, kBlock, 0, ctx->stream>>>(
+                            m, i, P->slice_ptr, P->sell_col, C->val, cf, rowmask_dev, R_dev,
+                            X_dev, out_dev, ld_out)))
+  } else {
+    IRK_STAGE_SWITCH(s, (k_stage_couple<SS, false><<<g, kBlock, 0, ctx->stream>>>(
+                            m, i, P->slice_ptr, P->sell_col, C->val, cf, nullptr, R_dev, X_dev,
+                            out_dev, ld_out)))
+  }
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_stage_rhs(irk_ctx* ctx, int64_t m, int s, double a, const irk_mat* B, const double* u_dev,
+                  const double* G_host, const double* F_dev, double* Out_dev) {
+  IRK_REQUIRE(ctx && Out_dev, "irk_stage_rhs: NULL argument");
+  IRK_REQUIRE(s >= 1 && s <= kMaxStages, "irk_stage_rhs: bad s");
+  IRK_REQUIRE(!B || (u_dev && B->pat->nrows == m), "irk_stage_rhs: B/u mismatch");
+  if (!B && a == 0.0) u_dev = nullptr;
+  IRK_REQUIRE(!F_dev || G_host, "irk_stage_rhs: F needs G");
+  if (m == 0) return IRK_OK;
+  Mat8 G;
+  load_mat(G, G_host, s);
+  unsigned g = (unsigned)((m + kBlock - 1) / kBlock);
+  const int* sp = B ? B->pat->slice_ptr : nullptr;
+  const int* sc = B ? B->pat->sell_col : nullptr;
+  const double* bv = B ? B->val : nullptr;
+  IRK_STAGE_SWITCH(s, (k_stage_rhs<SS><<<g, kBlock, 0, ctx->stream>>>(m, sp, sc, bv, a, u_dev, G,
+                                                                      F_dev, Out_dev)))
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_stage_update(irk_ctx* ctx, int64_t m, int s, double a, const double* u_dev,
+                     const double* w_host, int copy_stage, const double* X_dev,
+                     double* u_next_dev) {
+  IRK_REQUIRE(ctx && X_dev && u_next_dev, "irk_stage_update: NULL argument");
+  IRK_REQUIRE(s >= 1 && s <= kMaxStages, "irk_stage_update: bad s");
+  IRK_REQUIRE(copy_stage < s, "irk_stage_update: copy_stage out of range");
+  IRK_REQUIRE(copy_stage >= 0 || (w_host && (a == 0.0 || u_dev)),
+              "irk_stage_update: weights/u missing");
+  if (m == 0) return IRK_OK;
+  Mat8 w;
+  for (int q = 0; q < kMaxStages * kMaxStages; ++q) w.q[q] = 0.0;
+  if (w_host)
+    for (int i = 0; i < s; ++i) w.q[i] = w_host[i];
+  int g = grid_for(ctx, m);
+  IRK_STAGE_SWITCH(s, (k_stage_update<SS><<<g, kBlock, 0, ctx->stream>>>(m, a, u_dev, w,
+                                                                         copy_stage, X_dev,
+                                                                         u_next_dev)))
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_stage_scale(irk_ctx* ctx, int64_t m, int s, const double* w_host, const double* v_dev,
+                    const double* D_dev, double* out_dev) {
+  IRK_REQUIRE(ctx && w_host && v_dev && out_dev, "irk_stage_scale: NULL argument");
+  IRK_REQUIRE(s >= 1 && s <= kMaxStages, "irk_stage_scale: bad s");
+  if (m == 0) return IRK_OK;
+  Mat8 w;
+  for (int q = 0; q < kMaxStages * kMaxStages; ++q) w.q[q] = 0.0;
+  for (int i = 0; i < s; ++i) w.q[i] = w_host[i];
+  k_stage_scale<<<grid_for(ctx, m * s), kBlock, 0, ctx->stream>>>(m, s, w, v_dev, D_dev, out_dev);
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_stage_get(irk_ctx* ctx, int64_t m, int s, int i, const double* X_dev, double* x_dev) {
+  IRK_REQUIRE(ctx && X_dev && x_dev && i >= 0 && i < s, "irk_stage_get: bad argument");
+  if (m == 0) return IRK_OK;
+  k_stage_get<<<grid_for(ctx, m), kBlock, 0, ctx->stream>>>(m, s, i, X_dev, x_dev);
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_stage_set(irk_ctx* ctx, int64_t m, int s, int i, const double* x_dev, double* X_dev) {
+  IRK_REQUIRE(ctx && X_dev && x_dev && i >= 0 && i < s, "irk_stage_set: bad argument");
+  if (m == 0) return IRK_OK;
+  k_stage_set<<<grid_for(ctx, m), kBlock, 0, ctx->stream>>>(m, s, i, x_dev, X_dev);
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_to_interleaved(irk_ctx* ctx, int64_t m, int s, const double* stage_major_dev,
+                       double* interleaved_dev) {
+  IRK_REQUIRE(ctx && stage_major_dev && interleaved_dev && s >= 1,
+              "irk_to_interleaved: bad argument");
+  if (m == 0) return IRK_OK;
+  k_to_interleaved<<<grid_for(ctx, m * s), kBlock, 0, ctx->stream>>>(m, s, stage_major_dev,
+                                                                    interleaved_dev);
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_to_stage_major(irk_ctx* ctx, int64_t m, int s, const double* interleaved_dev,
+                       double* stage_major_dev) {
+  IRK_REQUIRE(ctx && stage_major_dev && interleaved_dev && s >= 1,
+              "irk_to_stage_major: bad argument");
+  if (m == 0) return IRK_OK;
+  k_to_stage_major<<<grid_for(ctx, m * s), kBlock, 0, ctx->stream>>>(m, s, interleaved_dev,
+                                                                    stage_major_dev);
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_bc_scatter(irk_ctx* ctx, int s, int64_t nb, const int64_t* idx_dev, const double* V_dev,
+                   double* X_dev) {
+  IRK_REQUIRE(ctx && s >= 1, "irk_bc_scatter: bad argument");
+  if (nb == 0) return IRK_OK;
+  k_bc_scatter<<<grid_for(ctx, nb * s), kBlock, 0, ctx->stream>>>(s, nb, idx_dev, V_dev, X_dev);
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_bc_gather(irk_ctx* ctx, int64_t nb, const int64_t* idx_dev, const double* x_dev,
+                  double* v_dev) {
+  IRK_REQUIRE(ctx, "irk_bc_gather: bad argument");
+  if (nb == 0) return IRK_OK;
+  k_bc_gather<<<grid_for(ctx, nb), kBlock, 0, ctx->stream>>>(nb, idx_dev, x_dev, v_dev);
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_bc_zero(irk_ctx* ctx, int s, int64_t nb, const int64_t* idx_dev, double* X_dev) {
+  IRK_REQUIRE(ctx && s >= 1, "irk_bc_zero: bad argument");
+  if (nb == 0) return IRK_OK;
+  k_bc_zero<<<grid_for(ctx, nb * s), kBlock, 0, ctx->stream>>>(s, nb, idx_dev, X_dev);
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_bc_mask(irk_ctx* ctx, int64_t m, int64_t nb, const int64_t* idx_dev, uint8_t* mask_dev) {
+  IRK_REQUIRE(ctx && mask_dev, "irk_bc_mask: bad argument");
+  if (m) IRK_CUDA(cudaMemsetAsync(mask_dev, 0, m, ctx->stream));
+  if (nb == 0) return IRK_OK;
+  k_bc_mask<<<grid_for(ctx, nb), kBlock, 0, ctx->stream>>>(nb, idx_dev, mask_dev);
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_semilinear_residual(irk_ctx* ctx, int s, const double* A_host, double dt,
+                            const irk_mat* M, const irk_mat* K, double kscale, int ncoef,
+                            const double* coef_host, const double* u_dev, const double* X_dev,
+                            const double* F_dev, const uint8_t* rowmask_dev, double* R_dev,
+                            double* D_dev) {
+  IRK_REQUIRE(ctx && A_host && M && K && u_dev && X_dev && R_dev && D_dev,
+              "irk_semilinear_residual: NULL argument");
+  IRK_REQUIRE(s >= 1 && s <= kMaxStages, "irk_semilinear_residual: bad s");
+  IRK_REQUIRE(ncoef >= 0 && ncoef <= 8 && (ncoef == 0 || coef_host),
+              "irk_semilinear_residual: 0 <= ncoef <= 8");
+  IRK_REQUIRE(K->pat == M->pat, "irk_semilinear_residual: M and K must share a pattern");
+  Mat8 A;
+  load_mat(A, A_host, s);
+  Poly g{};
+  g.n = ncoef;
+  for (int q = 0; q < ncoef; ++q) g.c[q] = coef_host[q];
+  const Pattern* P = M->pat;
+  int64_t m = P->nrows;
+  if (m == 0) return IRK_OK;
+  unsigned gr = (unsigned)((m + kBlock - 1) / kBlock);
+  if (rowmask_dev) {
+    IRK_STAGE_SWITCH(s, (k_semilinear_residual<SS, true><<<gr, kBlock, 0, ctx->stream>>>(
+                            m, P->slice_ptr, P->sell_col, M->val, K->val, A, dt, kscale, g,
+                            u_dev, X_dev, F_dev, rowmask_dev, R_dev, D_dev)))
+  } else {
+    IRK_STAGE_SWITCH(s, (k_semilinear_residual<SS, false><<<gr, kBlock, 0, ctx->stream>>>(
+                            m, P->slice_ptr, P->sell_col, M->val, K->val, A, dt, kscale, g,
+                            u_dev, X_dev, F_dev, nullptr, R_dev, D_dev)))
+  }
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+}  // extern "C"

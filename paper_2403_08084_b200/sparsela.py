@@ -1,0 +1,892 @@
+"""Device sparse linear algebra for the stage-coupled solve.
+
+Drop-in for implicitrk.sparsela (/root/reference/pkg/src/implicitrk/sparsela.py):
+``SparseMatrix``, ``spmv``, ``dirichlet_constrain``, ``factorize_block`` /
+``BlockFactorization``, ``KroneckerStageOperator``, ``KrylovSettings``,
+``fgmres``, ``FgmresResult``, ``mm_read`` / ``mm_write`` and the exception
+classes keep the reference's names, arguments and error behaviour; every
+arithmetic operation runs in libirk's sm_100a kernels on float64 device data.
+
+Differences by design (north_star):
+* stage vectors are stage-INTERLEAVED (row r, stage i at r*s+i) on the device;
+  the public ``apply``/``fgmres`` entry points accept and return the
+  reference's stage-major vectors and permute at the boundary;
+* ``factorize_block`` does not factorise: the block alpha*M + dt*K (with the
+  reference's identity rows/columns on Dirichlet dofs) is stored on device
+  and solved by Jacobi-preconditioned CG to ``rtol`` (default 1e-12, i.e. to
+  round-off on well-conditioned blocks);
+* ``fgmres`` orthogonalises with classical Gram-Schmidt in one fused pass
+  (optional second pass, ``KrylovSettings.reorth``) instead of MGS.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from enum import Enum
+
+import ctypes as C
+import numpy as np
+
+from . import _lib
+from ._lib import call, ctx, hptr, ptr
+
+
+class FactorizationError(ArithmeticError):
+    """A stage block was structurally or numerically singular (sparsela.py:20-21)."""
+
+
+class NonConvergenceError(RuntimeError):
+    """An iteration cap was reached; carries the residual history (sparsela.py:24-29)."""
+
+    def __init__(self, message, residuals):
+        super().__init__(message)
+        self.residuals = residuals
+
+
+class Splitting(Enum):
+    """Kronecker factorisation of the stage system (sparsela.py:32-40)."""
+
+    AI = "ai"
+    IA = "ia"
+
+
+# --------------------------------------------------------------- devices
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def device():
+    torch = _torch()
+    return torch.device("cuda", _lib.device_index())
+
+
+def dev_empty(n, dtype=None):
+    torch = _torch()
+    return torch.empty(int(n), dtype=dtype or torch.float64, device=device())
+
+
+def dev_zeros(n, dtype=None):
+    torch = _torch()
+    return torch.zeros(int(n), dtype=dtype or torch.float64, device=device())
+
+
+def to_dev(x, dtype=None):
+    """numpy / torch / sequence -> contiguous float64 (or dtype) CUDA tensor."""
+    torch = _torch()
+    dt = dtype or torch.float64
+    if isinstance(x, torch.Tensor):
+        if x.device.type == "cuda" and x.dtype == dt and x.is_contiguous():
+            return x
+        return x.to(device=device(), dtype=dt).contiguous()
+    np_dt = np.float64 if dt == torch.float64 else np.int64 if dt == torch.int64 else None
+    arr = np.ascontiguousarray(np.asarray(x, dtype=np_dt))
+    return torch.from_numpy(arr).to(device())
+
+
+def is_torch(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor)
+
+
+def to_host(t) -> np.ndarray:
+    return t.detach().cpu().numpy()
+
+
+def _like_input(dev_result, like):
+    """Return numpy for numpy-ish input, a torch CUDA tensor for torch input."""
+    if is_torch(like):
+        return dev_result
+    return to_host(dev_result)
+
+
+# ------------------------------------------------------------ device matrix
+
+
+class DeviceMatrix:
+    """Owner of one libirk irk_mat (CSR + SELL-32, float64 values)."""
+
+    __slots__ = ("handle", "nrows", "ncols", "nnz", "__weakref__")
+
+    def __init__(self, handle: C.c_void_p):
+        self.handle = handle
+        r, c, z = C.c_int64(), C.c_int64(), C.c_int64()
+        call("irk_mat_info", handle, C.byref(r), C.byref(c), C.byref(z))
+        self.nrows, self.ncols, self.nnz = r.value, c.value, z.value
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                _lib.load().irk_mat_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self.handle = None
+
+    @classmethod
+    def from_csr(cls, nrows, ncols, rowptr, col, val):
+        rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+        col = np.ascontiguousarray(col, dtype=np.int64)
+        val = np.ascontiguousarray(val, dtype=np.float64)
+        h = C.c_void_p()
+        call("irk_mat_from_csr", ctx(), int(nrows), int(ncols), int(len(val)), hptr(rowptr),
+             hptr(col), hptr(val), C.byref(h))
+        return cls(h)
+
+    def same_pattern(self, other: "DeviceMatrix") -> bool:
+        return bool(_lib.load().irk_mat_same_pattern(self.handle, other.handle))
+
+    def union(self, other):
+        a, b = C.c_void_p(), C.c_void_p()
+        call("irk_mat_union", ctx(), self.handle, other.handle, C.byref(a), C.byref(b))
+        return DeviceMatrix(a), DeviceMatrix(b)
+
+    def on_pattern(self, template: "DeviceMatrix") -> "DeviceMatrix":
+        h = C.c_void_p()
+        call("irk_mat_on_pattern", ctx(), self.handle, template.handle, C.byref(h))
+        return DeviceMatrix(h)
+
+    def combine(self, alpha, other, beta) -> "DeviceMatrix":
+        h = C.c_void_p()
+        call("irk_mat_combine", ctx(), float(alpha), self.handle, float(beta), other.handle,
+             C.byref(h))
+        return DeviceMatrix(h)
+
+    def constrain(self, mask, diag_value=1.0) -> "DeviceMatrix":
+        h = C.c_void_p()
+        call("irk_mat_constrain", ctx(), self.handle, ptr(mask), float(diag_value), C.byref(h))
+        return DeviceMatrix(h)
+
+    def diagonal(self):
+        out = dev_empty(self.nrows)
+        call("irk_mat_diagonal", ctx(), self.handle, ptr(out))
+        return out
+
+    def rowsum(self):
+        out = dev_empty(self.nrows)
+        call("irk_mat_rowsum", ctx(), self.handle, ptr(out))
+        return out
+
+    def spmv(self, x, y, k=1):
+        call("irk_spmv", ctx(), self.handle, int(k), ptr(x), ptr(y))
+        return y
+
+    def download(self):
+        rp = np.empty(self.nrows + 1, dtype=np.int64)
+        ci = np.empty(self.nnz, dtype=np.int64)
+        va = np.empty(self.nnz, dtype=np.float64)
+        call("irk_mat_download", ctx(), self.handle, hptr(rp), hptr(ci), hptr(va))
+        return rp, ci, va
+
+
+def shared_pattern(mats):
+    """Re-express device matrices on one pattern object (union of patterns)."""
+    mats = list(mats)
+    first = mats[0]
+    if all(first.same_pattern(x) for x in mats[1:]):
+        return mats
+    acc = first
+    for x in mats[1:]:
+        if not acc.same_pattern(x):
+            acc, _ = acc.union(x)
+    return [x if x.same_pattern(acc) else x.on_pattern(acc) for x in mats]
+
+
+# ------------------------------------------------------------ SparseMatrix
+
+
+class SparseMatrix:
+    """Immutable CSR matrix (sparsela.py:43-115) backed by a device copy.
+
+    Host arrays (int64 indices, float64 values, read-only) are materialised
+    on first access when the matrix was produced on the device (assembly,
+    combination); device storage is created on first use when the matrix was
+    built from host arrays.
+    """
+
+    def __init__(self, nrows, ncols, row_offsets, col_indices, values):
+        self.nrows = int(nrows)
+        self.ncols = int(ncols)
+        self._ro = np.ascontiguousarray(row_offsets, dtype=np.int64)
+        self._ci = np.ascontiguousarray(col_indices, dtype=np.int64)
+        self._va = np.ascontiguousarray(values, dtype=np.float64)
+        self._validate(self._ro, self._ci, self._va)
+        for a in (self._ro, self._ci, self._va):
+            a.setflags(write=False)
+        self._nnz = len(self._va)
+        self._dev = None
+        self._csr = None
+        self._pattern_cache = {}
+
+    # -- construction -------------------------------------------------
+    def _validate(self, ro, ci, va):
+        if ro.shape != (self.nrows + 1,):
+            raise ValueError("row_offsets must have length nrows + 1")
+        if ro[0] != 0 or ro[-1] != len(va) or len(ci) != len(va):
+            raise ValueError("row_offsets endpoints inconsistent with nnz")
+        lens = np.diff(ro)
+        if np.any(lens < 0):
+            raise ValueError("row_offsets must be nondecreasing")
+        if len(ci) and (ci.min() < 0 or ci.max() >= self.ncols):
+            raise ValueError("column index out of range")
+        if len(ci) > 1:
+            step = np.diff(ci)
+            same_row = np.repeat(np.arange(self.nrows), lens)
+            inside = same_row[1:] == same_row[:-1]
+            if np.any(step[inside] <= 0):
+                raise ValueError("col_indices must be strictly increasing per row")
+
+    @classmethod
+    def _from_device(cls, dm: DeviceMatrix) -> "SparseMatrix":
+        obj = cls.__new__(cls)
+        obj.nrows, obj.ncols, obj._nnz = dm.nrows, dm.ncols, dm.nnz
+        obj._ro = obj._ci = obj._va = None
+        obj._dev = dm
+        obj._csr = None
+        obj._pattern_cache = {}
+        return obj
+
+    @classmethod
+    def from_scipy(cls, mat) -> "SparseMatrix":
+        import scipy.sparse as sp
+
+        m = sp.csr_matrix(mat, copy=True)
+        m.sum_duplicates()
+        m.sort_indices()
+        return cls(m.shape[0], m.shape[1], m.indptr, m.indices, m.data)
+
+    @classmethod
+    def from_dense(cls, arr) -> "SparseMatrix":
+        import scipy.sparse as sp
+
+        return cls.from_scipy(sp.csr_matrix(np.asarray(arr, dtype=np.float64)))
+
+    @classmethod
+    def identity(cls, n) -> "SparseMatrix":
+        n = int(n)
+        return cls(n, n, np.arange(n + 1), np.arange(n), np.ones(n))
+
+    # -- host view -------------------------------------------------------
+    def _host(self):
+        if self._ro is None:
+            ro, ci, va = self._dev.download()
+            for a in (ro, ci, va):
+                a.setflags(write=False)
+            self._ro, self._ci, self._va = ro, ci, va
+
+    @property
+    def row_offsets(self):
+        self._host()
+        return self._ro
+
+    @property
+    def col_indices(self):
+        self._host()
+        return self._ci
+
+    @property
+    def values(self):
+        self._host()
+        return self._va
+
+    def to_scipy(self):
+        import scipy.sparse as sp
+
+        if self._csr is None:
+            self._host()
+            self._csr = sp.csr_matrix((self._va, self._ci, self._ro), shape=(self.nrows, self.ncols))
+        return self._csr
+
+    def to_dense(self) -> np.ndarray:
+        return self.to_scipy().toarray()
+
+    @property
+    def shape(self):
+        return (self.nrows, self.ncols)
+
+    @property
+    def nnz(self):
+        return self._nnz
+
+    def __repr__(self):
+        return f"SparseMatrix({self.nrows}x{self.ncols}, nnz={self.nnz})"
+
+    # -- device view -------------------------------------------------------
+    def device(self) -> DeviceMatrix:
+        if self._dev is None:
+            self._dev = DeviceMatrix.from_csr(self.nrows, self.ncols, self._ro, self._ci, self._va)
+        return self._dev
+
+    def _dev_op(self):
+        return _SpmvOp(self)
+
+
+def spmv(A: SparseMatrix, x):
+    """y = A x (sparsela.py:118-123) on the device; numpy in -> numpy out."""
+    n = x.shape[0] if hasattr(x, "shape") else len(x)
+    if (len(getattr(x, "shape", (n,))) != 1) or n != A.ncols:
+        raise ValueError(f"spmv: x has shape {tuple(getattr(x, 'shape', (n,)))}, expected ({A.ncols},)")
+    xd = to_dev(x)
+    y = dev_empty(A.nrows)
+    A.device().spmv(xd, y)
+    return _like_input(y, x)
+
+
+def dof_mask(m: int, dofs):
+    """uint8 device mask with ones at ``dofs``."""
+    torch = _torch()
+    idx = to_dev(np.asarray(dofs, dtype=np.int64), dtype=torch.int64)
+    mask = torch.empty(int(m), dtype=torch.uint8, device=device())
+    call("irk_bc_mask", ctx(), int(m), int(idx.numel()), ptr(idx), ptr(mask))
+    return mask
+
+
+def dirichlet_constrain(A: SparseMatrix, dofs, diag_value: float = 1.0) -> SparseMatrix:
+    """Identity rows/columns on ``dofs`` (sparsela.py:126-146).
+
+    The result keeps A's pattern (zeroed entries stay stored); its values and
+    dense form equal the reference's.
+    """
+    dofs = np.asarray(dofs, dtype=np.int64)
+    if len(dofs) == 0:
+        return A
+    if dofs.min() < 0 or dofs.max() >= A.nrows:
+        raise ValueError("constrained dof index out of range")
+    if A.nrows != A.ncols:
+        raise ValueError("dirichlet_constrain needs a square matrix")
+    mask = dof_mask(A.nrows, dofs)
+    try:
+        dm = A.device().constrain(mask, diag_value)
+    except ValueError:
+        # constrained rows without a stored diagonal: add it via a union
+        eye = SparseMatrix.identity(A.nrows).device()
+        a2, e2 = A.device().union(eye)
+        dm = a2.constrain(mask, diag_value)
+    return SparseMatrix._from_device(dm)
+
+
+# ---------------------------------------------------- device operator layer
+
+
+class _DevOp:
+    """Device linear operator: ``dev_apply(x, out)`` on length-n CUDA tensors.
+
+    ``layout`` is (m, s) when the operator works on stage-interleaved data
+    (s > 1), else None (natural ordering)."""
+
+    n = 0
+    layout = None
+
+    def dev_apply(self, x, out):  # pragma: no cover - interface
+        raise NotImplementedError
+
+
+class _SpmvOp(_DevOp):
+    def __init__(self, A: SparseMatrix):
+        self.A = A
+        self.n = A.nrows
+        self._dm = A.device()
+
+    def dev_apply(self, x, out):
+        self._dm.spmv(x, out)
+
+
+class _HostCallbackOp(_DevOp):
+    """A user-supplied host callable (or object with .apply): data crosses to
+    the host for the call.  Only reached for user code the reference also
+    accepts (sparsela.py:282-296); every built-in operator is device-native."""
+
+    def __init__(self, fn, n):
+        self.fn = fn
+        self.n = n
+
+    def dev_apply(self, x, out):
+        y = self.fn(to_host(x))
+        out.copy_(to_dev(np.asarray(y, dtype=np.float64).reshape(-1)))
+
+
+class _PermutedOp(_DevOp):
+    """Adapter running a natural-order operator on interleaved (m, s) data."""
+
+    def __init__(self, inner: _DevOp, m: int, s: int):
+        self.inner, self.m, self.s = inner, m, s
+        self.n = m * s
+        self.layout = (m, s)
+
+    def dev_apply(self, x, out):
+        a = dev_empty(self.n)
+        b = dev_empty(self.n)
+        call("irk_to_stage_major", ctx(), self.m, self.s, ptr(x), ptr(a))
+        self.inner.dev_apply(a, b)
+        call("irk_to_interleaved", ctx(), self.m, self.s, ptr(b), ptr(out))
+
+
+def as_dev_op(obj, n):
+    """Interpret op/pc arguments the way the reference's _as_apply does
+    (sparsela.py:282-296), returning device operators."""
+    if obj is None:
+        return None
+    if isinstance(obj, _DevOp):
+        return obj
+    if hasattr(obj, "_dev_op"):
+        return obj._dev_op()
+    if isinstance(obj, np.ndarray):
+        return _SpmvOp(SparseMatrix.from_dense(obj))
+    try:
+        import scipy.sparse as sp
+
+        if sp.issparse(obj):
+            return _SpmvOp(SparseMatrix.from_scipy(obj))
+    except ImportError:  # pragma: no cover
+        pass
+    if is_torch(obj):
+        return _SpmvOp(SparseMatrix.from_dense(to_host(obj)))
+    if hasattr(obj, "apply"):
+        return _HostCallbackOp(obj.apply, n)
+    if callable(obj):
+        return _HostCallbackOp(obj, n)
+    raise TypeError(f"cannot interpret {type(obj).__name__} as a linear operator")
+
+
+# -------------------------------------------------------- block solves
+
+
+@dataclass
+class BlockSolveSettings:
+    """Inner diagonal-block solver (replaces SuperLU, sparsela.py:149-191).
+
+    method: "pcg" (Jacobi-preconditioned CG) or "chebyshev" (Jacobi-Chebyshev,
+    ``cheb_iters`` sweeps with Gershgorin/Lanczos-free bounds).
+    raise_on_maxit: when False (preconditioner use) an unconverged block
+    returns its last iterate, FGMRES being flexible."""
+
+    method: str = "pcg"
+    rtol: float = 1e-6
+    atol: float = 0.0
+    maxit: int = 20000
+    raise_on_maxit: bool = False
+    cheb_iters: int = 50
+
+    def __post_init__(self):
+        if self.method not in ("pcg", "chebyshev"):
+            raise ValueError(f"unknown block solver {self.method!r}")
+        if self.rtol < 0 or self.atol < 0 or self.maxit < 0:
+            raise ValueError("block solver tolerances must be non-negative")
+
+
+class BlockFactorization:
+    """Stage block alpha*M + dt*K with Dirichlet identity rows/columns,
+    solved on the device (drop-in for sparsela.py:149-168).
+
+    ``solve``/``apply``/``matvec``/``matrix``/``n`` as in the reference;
+    ``dev_solve`` is the device entry used by the preconditioners."""
+
+    def __init__(self, M: SparseMatrix, K: SparseMatrix, alpha: float, dt: float, dofs=None,
+                 settings: BlockSolveSettings | None = None):
+        self.n = M.nrows
+        self.alpha = float(alpha)
+        self.beta = float(dt)
+        self.dofs = np.asarray(dofs if dofs is not None else [], dtype=np.int64)
+        self.settings = settings or BlockSolveSettings(rtol=1e-12, raise_on_maxit=True)
+        Md, Kd = shared_pattern([M.device(), K.device()])
+        B = Md.combine(self.alpha, Kd, self.beta)
+        self.mask = dof_mask(self.n, self.dofs) if len(self.dofs) else None
+        if self.mask is not None:
+            B = B.constrain(self.mask, 1.0)
+        self._B = B
+        self._matrix = None
+        self.last_iterations = 0
+        self.last_relres = 0.0
+        self._check_regular()
+
+    def _check_regular(self):
+        torch = _torch()
+        d = self._B.diagonal()
+        if self.n == 0:
+            return
+        if not bool(torch.isfinite(d).all()) or bool((d == 0).any()):
+            raise FactorizationError("stage block has a zero or non-finite diagonal entry")
+        # pure-Neumann detection: the constants lie in the nullspace
+        rs = self._B.rowsum()
+        scale = float(torch.abs(d).max())
+        if float(torch.abs(rs).max()) <= 1e-13 * scale:
+            raise FactorizationError("stage block is singular (constant vectors in its nullspace)")
+
+    @property
+    def matrix(self) -> SparseMatrix:
+        if self._matrix is None:
+            self._matrix = SparseMatrix._from_device(self._B)
+        return self._matrix
+
+    def dev_solve(self, rhs, x, ld_rhs=1, ld_x=1, nb=1, settings: BlockSolveSettings | None = None):
+        st = settings or self.settings
+        its = np.zeros(8, dtype=np.int32)
+        rel = np.zeros(8, dtype=np.float64)
+        one = np.ones(8)
+        status = _lib.load().irk_pcg(
+            ctx(), 1, hptr(one), C.c_void_p(), self._B.handle, C.c_void_p(), C.c_void_p(),
+            C.c_void_p(), ptr(rhs), int(ld_rhs), ptr(x), int(ld_x), float(st.rtol), float(st.atol),
+            int(st.maxit), hptr(its), hptr(rel))
+        self.last_iterations = int(its[0])
+        self.last_relres = float(rel[0])
+        if status == _lib.IRK_ENOCONV:
+            if st.raise_on_maxit:
+                raise NonConvergenceError(
+                    f"block PCG: no convergence in {st.maxit} iterations "
+                    f"(relative residual {rel[0]:.3e})", [float(rel[0])])
+            return int(its[0])
+        if status == _lib.IRK_ESINGULAR:
+            if not st.raise_on_maxit:
+                return int(its[0])  # preconditioner use: keep the last iterate
+            raise FactorizationError(f"block PCG breakdown: {_lib.last_error()}")
+        _lib.check(status, "irk_pcg")
+        return int(its[0])
+
+    def solve(self, b):
+        bd = to_dev(b)
+        if bd.shape != (self.n,):
+            raise ValueError(f"block solve expects length {self.n}, got {tuple(bd.shape)}")
+        x = dev_empty(self.n)
+        self.dev_solve(bd, x)
+        return _like_input(x, b)
+
+    apply = solve
+
+    def matvec(self, x):
+        xd = to_dev(x)
+        y = dev_empty(self.n)
+        self._B.spmv(xd, y)
+        return _like_input(y, x)
+
+    def _dev_op(self):
+        fac = self
+
+        class _Op(_DevOp):
+            n = fac.n
+
+            def dev_apply(self, x, out):
+                fac.dev_solve(x, out)
+
+        return _Op()
+
+
+def factorize_block(M: SparseMatrix, K: SparseMatrix, alpha: float, dt: float, dirichlet=None,
+                    settings: BlockSolveSettings | None = None) -> BlockFactorization:
+    """Prepare alpha*M + dt*K (optionally Dirichlet-constrained) for device
+    solves (sparsela.py:171-191)."""
+    if M.shape != K.shape or M.nrows != M.ncols:
+        raise ValueError("factorize_block needs square M, K of equal shape")
+    dofs = None
+    if dirichlet is not None and len(dirichlet):
+        dofs = np.asarray(dirichlet, dtype=np.int64)
+        if dofs.min() < 0 or dofs.max() >= M.nrows:
+            raise ValueError("constrained dof index out of range")
+    return BlockFactorization(M, K, alpha, dt, dofs, settings)
+
+
+# -------------------------------------------------- Kronecker stage operator
+
+
+class KroneckerStageOperator:
+    """Matrix-free C1 (x) M + dt C2 (x) K on stacked stage vectors
+    (sparsela.py:194-250), executed by the fused interleaved kernel K2.
+
+    ``Ks`` is one stiffness matrix or one (row-indexed) matrix per stage."""
+
+    def __init__(self, C1, C2, M: SparseMatrix, Ks, dt: float):
+        self.C1 = np.ascontiguousarray(C1, dtype=np.float64)
+        self.C2 = np.ascontiguousarray(C2, dtype=np.float64)
+        self.M = M
+        self.Ks = list(Ks) if isinstance(Ks, (list, tuple)) else [Ks]
+        self.dt = float(dt)
+        s = self.C1.shape[0] if self.C1.ndim == 2 else -1
+        if self.C1.shape != (s, s) or self.C2.shape != (s, s):
+            raise ValueError("C1, C2 must be square and of equal size")
+        if len(self.Ks) not in (1, s):
+            raise ValueError("Ks must hold one matrix or one per stage")
+        m = M.nrows
+        for K in self.Ks:
+            if K.shape != (m, m) or M.shape != (m, m):
+                raise ValueError("M and K blocks must be square and of equal shape")
+        if s > 8:
+            raise ValueError("at most 8 stages are supported on the device")
+        self.s = s
+        self.m = m
+        self.n = s * m
+        self._mats = None
+
+    # -- device ---------------------------------------------------------
+    def _device_mats(self):
+        if self._mats is None:
+            self._mats = shared_pattern([self.M.device()] + [K.device() for K in self.Ks])
+        return self._mats
+
+    def dev_apply(self, Y, Out, mask=None):
+        mats = self._device_mats()
+        Md, Ks = mats[0], mats[1:]
+        arr = (C.c_void_p * len(Ks))(*[k.handle.value for k in Ks])
+        call("irk_stage_apply", ctx(), self.s, hptr(self.C1), hptr(self.C2), self.dt, Md.handle,
+             C.cast(arr, C.c_void_p), len(Ks), ptr(mask), ptr(Y), ptr(Out))
+        return Out
+
+    def _dev_op(self, mask=None):
+        op = self
+
+        class _Op(_DevOp):
+            n = op.n
+            layout = (op.m, op.s) if op.s > 1 else None
+
+            def dev_apply(self, x, out):
+                op.dev_apply(x, out, mask)
+
+        return _Op()
+
+    # -- reference API --------------------------------------------------
+    def apply(self, v):
+        vd = to_dev(v)
+        if tuple(vd.shape) != (self.n,):
+            raise ValueError(f"operator expects length {self.n}, got {tuple(vd.shape)}")
+        out = stage_major_apply(self._dev_op(), vd, self.m, self.s)
+        return _like_input(out, v)
+
+    def to_dense(self) -> np.ndarray:
+        """Explicit Kronecker assembly (host, small-m cross-checks only)."""
+        Md = self.M.to_dense()
+        out = np.kron(self.C1, Md)
+        if len(self.Ks) == 1:
+            out += self.dt * np.kron(self.C2, self.Ks[0].to_dense())
+        else:
+            m = self.m
+            for i in range(self.s):
+                Kd = self.Ks[i].to_dense()
+                for j in range(self.s):
+                    out[i * m:(i + 1) * m, j * m:(j + 1) * m] += self.dt * self.C2[i, j] * Kd
+        return out
+
+
+def stage_major_apply(devop: _DevOp, vd, m, s):
+    """Apply an interleaved device operator to a stage-major vector."""
+    if s == 1 or devop.layout is None:
+        out = dev_empty(vd.numel())
+        devop.dev_apply(vd, out)
+        return out
+    a = dev_empty(m * s)
+    b = dev_empty(m * s)
+    out = dev_empty(m * s)
+    call("irk_to_interleaved", ctx(), m, s, ptr(vd), ptr(a))
+    devop.dev_apply(a, b)
+    call("irk_to_stage_major", ctx(), m, s, ptr(b), ptr(out))
+    return out
+
+
+def apply_kronecker(op: KroneckerStageOperator, v):
+    return op.apply(v)
+
+
+# ------------------------------------------------------------------ FGMRES
+
+
+@dataclass
+class KrylovSettings:
+    """FGMRES controls (sparsela.py:257-272) + ``reorth`` (CGS2 pass)."""
+
+    rtol: float = 1e-8
+    atol: float = 1e-50
+    restart: int = 50
+    maxit: int = 500
+    right_pc: bool = True
+    reorth: bool = False
+
+    def __post_init__(self):
+        if self.rtol <= 0 or self.atol <= 0:
+            raise ValueError("rtol and atol must be positive")
+        if self.restart < 1:
+            raise ValueError("restart must be >= 1")
+        if self.restart > 63:
+            raise ValueError("restart must be <= 63 on the device (fused basis limit)")
+
+
+@dataclass
+class FgmresResult:
+    x: object
+    iterations: int
+    residuals: list
+
+
+def _norm(x) -> float:
+    out = dev_empty(1)
+    call("irk_norm2", ctx(), int(x.numel()), ptr(x), ptr(out))
+    return float(out.item())
+
+
+def _all_finite(x) -> bool:
+    res = C.c_int(0)
+    call("irk_all_finite", ctx(), int(x.numel()), ptr(x), C.byref(res))
+    return bool(res.value)
+
+
+def fgmres_device(A: _DevOp, b, P: _DevOp | None = None, settings: KrylovSettings | None = None,
+                  x0=None) -> FgmresResult:
+    """Restarted flexible GMRES on device vectors (control flow of
+    sparsela.py:299-403): right preconditioning by default, Givens rotations
+    and convergence test on the host, Arnoldi step = one fused CGS
+    projection pass + one fused update/norm pass on the device."""
+    st = settings or KrylovSettings()
+    n = int(b.numel())
+    if not _all_finite(b):
+        raise ValueError("right-hand side contains non-finite entries")
+    left = P is not None and not st.right_pc
+    if left:
+        rhs = dev_empty(n)
+        P.dev_apply(b, rhs)
+    else:
+        rhs = b
+    x = dev_zeros(n) if x0 is None else to_dev(x0).clone()
+
+    def residual_of(xv):
+        t = dev_empty(n)
+        A.dev_apply(xv, t)
+        r_ = b.clone()
+        call("irk_axpby", ctx(), n, -1.0, ptr(t), 1.0, ptr(r_))
+        if left:
+            pr = dev_empty(n)
+            P.dev_apply(r_, pr)
+            return pr
+        return r_
+
+    r = rhs.clone() if x0 is None else residual_of(x)
+    normb = _norm(rhs)
+    target = max(st.rtol * normb, st.atol)
+    residuals = [_norm(r)]
+    iterations = 0
+    if residuals[0] <= target:
+        return FgmresResult(x, 0, residuals)
+    breakdown_tol = 1e-14 * normb
+    hbuf = dev_empty(128)
+    tmp = dev_empty(n) if left else None
+    while True:
+        cycle = min(st.restart, st.maxit - iterations)
+        if cycle <= 0:
+            raise NonConvergenceError(
+                f"fgmres: no convergence in {st.maxit} iterations "
+                f"(residual {residuals[-1]:.3e}, target {target:.3e})", residuals)
+        beta = _norm(r)
+        V = dev_empty((cycle + 1) * n).view(cycle + 1, n)
+        store_z = P is not None and not left
+        Z = dev_empty(cycle * n).view(cycle, n) if store_z else V
+        call("irk_axpby", ctx(), n, 1.0 / beta, ptr(r), 0.0, ptr(V[0]))
+        H = np.zeros((cycle + 1, cycle))
+        cs = np.zeros(cycle)
+        sn = np.zeros(cycle)
+        g = np.zeros(cycle + 1)
+        g[0] = beta
+        converged = False
+        j = -1
+        for j in range(cycle):
+            w = V[j + 1]
+            if left:
+                A.dev_apply(V[j], tmp)
+                P.dev_apply(tmp, w)
+            else:
+                if store_z:
+                    P.dev_apply(V[j], Z[j])
+                    A.dev_apply(Z[j], w)
+                else:
+                    A.dev_apply(V[j], w)
+            iterations += 1
+            call("irk_multidot", ctx(), n, j + 1, ptr(V), n, ptr(w), ptr(hbuf))
+            call("irk_orth_update", ctx(), n, j + 1, ptr(V), n, ptr(hbuf), ptr(w),
+                 1 if st.reorth else 0)
+            hcol = hbuf[: j + 2].cpu().numpy()
+            H[: j + 2, j] = hcol
+            lucky = H[j + 1, j] < breakdown_tol
+            if not lucky:
+                call("irk_axpby", ctx(), n, 1.0 / H[j + 1, j], ptr(w), 0.0, ptr(w))
+            for i in range(j):
+                t_ = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+                H[i, j] = t_
+            d = np.hypot(H[j, j], H[j + 1, j])
+            if d == 0.0:
+                cs[j], sn[j] = 1.0, 0.0
+                d = 1e-300
+            else:
+                cs[j], sn[j] = H[j, j] / d, H[j + 1, j] / d
+            H[j, j] = d
+            H[j + 1, j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            residuals.append(abs(float(g[j + 1])))
+            if residuals[-1] <= target or lucky:
+                converged = True
+                break
+        k = j + 1
+        y = np.zeros(k)
+        for i in range(k - 1, -1, -1):
+            y[i] = (g[i] - H[i, i + 1:k] @ y[i + 1:k]) / H[i, i]
+        yh = np.ascontiguousarray(y)
+        call("irk_lincomb", ctx(), n, k, ptr(Z), n, hptr(yh), ptr(x))
+        if converged or residuals[-1] <= target:
+            return FgmresResult(x, iterations, residuals)
+        if iterations >= st.maxit:
+            raise NonConvergenceError(
+                f"fgmres: no convergence in {st.maxit} iterations "
+                f"(residual {residuals[-1]:.3e}, target {target:.3e})", residuals)
+        r = residual_of(x)
+
+
+def fgmres(op, b, pc=None, settings: KrylovSettings | None = None, x0=None) -> FgmresResult:
+    """Restarted flexible GMRES (drop-in for sparsela.py:299-403).
+
+    ``op``/``pc`` may be a SparseMatrix, ndarray, scipy sparse matrix, an
+    object with ``.apply``, a callable, or one of this package's stage
+    operators / preconditioners.  Vectors are in the reference's layout
+    (stage-major for stage systems); numpy in -> numpy out."""
+    bd = to_dev(b).reshape(-1)
+    n = int(bd.numel())
+    A = as_dev_op(op, n)
+    P = as_dev_op(pc, n)
+    layouts = {o.layout for o in (A, P) if o is not None and o.layout is not None}
+    if len(layouts) > 1:
+        raise ValueError("operator and preconditioner disagree on the stage layout")
+    x0d = to_dev(x0).reshape(-1) if x0 is not None else None
+    if layouts:
+        m, s = layouts.pop()
+        A = A if A.layout else _PermutedOp(A, m, s)
+        P = P if (P is None or P.layout) else _PermutedOp(P, m, s)
+        bi = dev_empty(n)
+        call("irk_to_interleaved", ctx(), m, s, ptr(bd), ptr(bi))
+        xi = None
+        if x0d is not None:
+            xi = dev_empty(n)
+            call("irk_to_interleaved", ctx(), m, s, ptr(x0d), ptr(xi))
+        res = fgmres_device(A, bi, P, settings, xi)
+        xs = dev_empty(n)
+        call("irk_to_stage_major", ctx(), m, s, ptr(res.x), ptr(xs))
+        res.x = xs
+    else:
+        res = fgmres_device(A, bd, P, settings, x0d)
+    res.x = _like_input(res.x, b)
+    return res
+
+
+# ------------------------------------------------------------ Matrix Market
+
+
+def mm_write(path, A: SparseMatrix) -> None:
+    """Coordinate Matrix Market, general symmetry (sparsela.py:410-413)."""
+    import scipy.io
+
+    scipy.io.mmwrite(str(path), A.to_scipy().tocoo(), symmetry="general")
+
+
+def mm_read(path) -> SparseMatrix:
+    import scipy.io
+
+    return SparseMatrix.from_scipy(scipy.io.mmread(str(path)))

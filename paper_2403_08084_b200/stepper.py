@@ -1,0 +1,945 @@
+"""Time stepping on the device: fully coupled stage solves, sequential DIRK
+and Newton (drop-in for implicitrk.stepper,
+/root/reference/pkg/src/implicitrk/stepper.py).
+
+The control flow, formulations, caches, clock and error behaviour follow the
+reference line by line; the state u, the stage right-hand sides, the stage
+unknowns and every Krylov vector live on the GPU in the stage-interleaved
+layout, and each arithmetic step is a libirk kernel:
+
+  rhs            irk_stage_rhs            (stepper.py:291-293, :309-311)
+  BC lifting     irk_stage_apply + scatter (bcs.py:123-142)
+  FGMRES         fused CGS kernels + stage apply + preconditioner
+  update         irk_stage_update         (stepper.py:352-361, :421)
+  DIRK stages    irk_stage_update (acc) + Jacobi-PCG on M + dt*a_ii*K
+  Newton (semilinear problems)  irk_semilinear_residual + Jacobian stage apply
+
+Sign convention as in the reference: M u' + K u = f, K positive semidefinite.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from enum import Enum
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import sparsela as la
+from ._lib import call, ctx, hptr, ptr
+from .bcs import (
+    BcMethod,
+    ConstrainedStageOperator,
+    DirichletBC,
+    StageUnknown,
+    constrain_stage_system_dev,
+    scatter_stage_values,
+    stage_bc_values,
+)
+from .precond import PreconditionerKind, build_preconditioner
+from .sparsela import (
+    BlockSolveSettings,
+    KroneckerStageOperator,
+    KrylovSettings,
+    NonConvergenceError,
+    SparseMatrix,
+    Splitting,
+    factorize_block,
+    fgmres_device,
+    spmv,
+)
+from .tableaux import ButcherTableau
+
+
+class FormulationError(ValueError):
+    """Tableau and formulation are incompatible (stepper.py:39-40)."""
+
+
+class NonlinearDivergenceError(RuntimeError):
+    """Newton exhausted its budget; carries the residual history (stepper.py:43-48)."""
+
+    def __init__(self, message, residuals):
+        super().__init__(message)
+        self.residuals = residuals
+
+
+class StepFailure(RuntimeError):
+    """A step inside advance() failed (stepper.py:51-57)."""
+
+    def __init__(self, message, completed_steps, reports):
+        super().__init__(message)
+        self.completed_steps = completed_steps
+        self.reports = reports
+
+
+class StageFormulation(Enum):
+    STAGE_DERIVATIVE_AI = "deriv-ai"
+    STAGE_DERIVATIVE_IA = "deriv-ia"
+    STAGE_VALUE = "value"
+    DIRK = "dirk"
+
+
+_SPLIT = {
+    StageFormulation.STAGE_DERIVATIVE_AI: Splitting.AI,
+    StageFormulation.STAGE_DERIVATIVE_IA: Splitting.IA,
+    StageFormulation.STAGE_VALUE: Splitting.AI,
+    StageFormulation.DIRK: Splitting.AI,
+}
+
+_UNKNOWN = {
+    StageFormulation.STAGE_DERIVATIVE_AI: StageUnknown.DERIVATIVE,
+    StageFormulation.STAGE_DERIVATIVE_IA: StageUnknown.W,
+    StageFormulation.STAGE_VALUE: StageUnknown.VALUE,
+    StageFormulation.DIRK: StageUnknown.DERIVATIVE,
+}
+
+
+@dataclass
+class NewtonSettings:
+    rtol: float = 1e-10
+    atol: float = 1e-12
+    maxit: int = 50
+
+
+@dataclass
+class StepReport:
+    """Per-step statistics (stepper.py:89-96); ``inner_iters`` adds the
+    inner block-solver iteration counts of the step."""
+
+    newton_iters: int
+    krylov_iters: int
+    final_residual: float
+    newton_residuals: list = field(default_factory=list)
+    inner_iters: list = field(default_factory=list)
+
+
+@dataclass(frozen=True)
+class SemilinearForm:
+    """Residual structure F(t, u, u') = M u' + kscale*K u + M g(u) - load(t)
+    with polynomial g(u) = sum_p coef[p] u^p.  Lets the Newton path run the
+    residual and Jacobian entirely on the device (Allen-Cahn:
+    kscale = eps^2, g(u) = u^3 - u; the cubic reaction of
+    tests/test_stepper.py:282-334: kscale = 1, g(u) = u^3)."""
+
+    kscale: float
+    coef: tuple
+
+    def g(self, u):
+        return np.polynomial.polynomial.polyval(u, np.asarray(self.coef, dtype=np.float64))
+
+    def dg(self, u):
+        c = np.asarray(self.coef, dtype=np.float64)
+        return np.polynomial.polynomial.polyval(u, np.polynomial.polynomial.polyder(c))
+
+
+def zero_load(m: int) -> Callable[[float], np.ndarray]:
+    """f(t) = 0, recognised by the stepper (no load term is formed)."""
+
+    def f(t):
+        return np.zeros(m)
+
+    f._irk_zero = True
+    return f
+
+
+@dataclass
+class SemidiscreteProblem:
+    """M u' + K u = f(t), a general residual, or a semilinear form
+    (stepper.py:99-141 + ``semilinear``)."""
+
+    m: int
+    mass: SparseMatrix
+    stiffness: Optional[SparseMatrix] = None
+    load: Optional[Callable[[float], np.ndarray]] = None
+    residual: Optional[Callable] = None
+    jacobian_u: Optional[Callable] = None
+    dirichlet: Optional[DirichletBC] = None
+    u0: Optional[np.ndarray] = None
+    grid: object = None
+    name: str = ""
+    semilinear: Optional[SemilinearForm] = None
+
+    def __post_init__(self):
+        if self.u0 is not None and not la.is_torch(self.u0):
+            self.u0 = np.asarray(self.u0, dtype=float)
+        if self.semilinear is not None:
+            if self.stiffness is None:
+                raise ValueError("a semilinear problem needs its stiffness matrix")
+            if self.load is None:
+                self.load = zero_load(self.m)
+            self._linear = False
+            M, K, f, form = self.mass, self.stiffness, self.load, self.semilinear
+            if self.residual is None:
+                self.residual = lambda t, u, udot: (
+                    spmv(M, udot) + form.kscale * spmv(K, u) + spmv(M, form.g(u)) - f(t))
+            if self.jacobian_u is None:
+                def _jac(t, u):
+                    import scipy.sparse as sp
+
+                    J = form.kscale * K.to_scipy() + M.to_scipy() @ sp.diags(form.dg(u))
+                    return SparseMatrix.from_scipy(J)
+
+                self.jacobian_u = _jac
+            return
+        self._linear = (self.residual is None and self.stiffness is not None
+                        and self.load is not None)
+        if self.residual is None:
+            if not self._linear:
+                raise ValueError("problem needs either (stiffness, load) or a residual")
+            M, K, f = self.mass, self.stiffness, self.load
+            self.residual = lambda t, u, udot: spmv(M, udot) + spmv(K, u) - f(t)
+            if self.jacobian_u is None:
+                self.jacobian_u = lambda t, u: K
+
+    @property
+    def is_linear(self) -> bool:
+        return self._linear
+
+
+# ------------------------------------------------------------------ stepper
+
+
+class TimeStepper:
+    """Binds problem, tableau, formulation, BC method and solver settings
+    (stepper.py:144-268).  One instance drives one trajectory; the state is
+    device-resident (``u_device``), ``u`` is its host view.
+
+    Extra keyword arguments (all optional):
+      block_solver  inner diagonal-block solver of the stage preconditioner
+                    (default Jacobi-PCG, rtol 1e-6)
+      dirk_solver   stage solver of the DIRK path (default Jacobi-PCG to the
+                    Krylov tolerance, north_star config 4)
+    """
+
+    def __init__(self, problem: SemidiscreteProblem, tableau: ButcherTableau, dt: float,
+                 formulation: StageFormulation = StageFormulation.STAGE_DERIVATIVE_AI,
+                 bc_method: BcMethod = BcMethod.DAE, t0: float = 0.0, u0=None,
+                 krylov: KrylovSettings | None = None, pc_kind: PreconditionerKind | None = None,
+                 newton: NewtonSettings | None = None, warm_start: bool = False,
+                 block_solver: BlockSolveSettings | None = None,
+                 dirk_solver: BlockSolveSettings | None = None):
+        if dt <= 0:
+            raise ValueError("dt must be positive")
+        u = u0 if u0 is not None else problem.u0
+        if u is None:
+            raise ValueError("no initial state: pass u0 or set problem.u0")
+        uh = la.to_host(u) if la.is_torch(u) else np.array(u, dtype=float)
+        if uh.shape != (problem.m,) or not np.all(np.isfinite(uh)):
+            raise ValueError("initial state must be finite of length problem.m")
+        if formulation in (StageFormulation.STAGE_DERIVATIVE_IA,
+                           StageFormulation.STAGE_VALUE) and not tableau.invertible:
+            raise FormulationError(
+                f"{formulation.value} needs an invertible tableau, got {tableau.name!r}")
+        if formulation is StageFormulation.DIRK and not tableau.lower_triangular:
+            raise FormulationError(
+                f"DIRK stepping needs a lower-triangular tableau, got {tableau.name!r}")
+        if tableau.s > 8:
+            raise ValueError("at most 8 stages are supported on the device")
+        self.problem = problem
+        self.tableau = tableau
+        self.formulation = formulation
+        self.bc_method = bc_method
+        self.krylov = krylov or KrylovSettings()
+        self.pc_kind = pc_kind
+        self.newton = newton or NewtonSettings()
+        self.warm_start = warm_start
+        self.block_solver = block_solver or BlockSolveSettings()
+        self.dirk_solver = dirk_solver
+        self._u_dev = la.to_dev(u).clone() if la.is_torch(u) else la.to_dev(uh)
+        self._u_host = uh.copy()
+        self._last_stages_dev = None
+        self._t_base = float(t0)
+        self.step_index = 0
+        self._dt = float(dt)
+        self._pc_cache = {}
+        self._dirk_factors = {}
+        self._op_cache = {}
+
+    # -- state ------------------------------------------------------------
+    @property
+    def u(self) -> np.ndarray:
+        if self._u_host is None:
+            self._u_host = la.to_host(self._u_dev)
+        return self._u_host
+
+    @u.setter
+    def u(self, value):
+        self._u_dev = la.to_dev(value).clone()
+        self._u_host = None
+
+    @property
+    def u_device(self):
+        return self._u_dev
+
+    @property
+    def _last_stages(self):
+        """Stage vector of the last linear solve, stage-major host copy
+        (the reference's oracle hook, stepper.py:337)."""
+        if self._last_stages_dev is None:
+            return None
+        s, m = self.tableau.s, self.problem.m
+        out = la.dev_empty(s * m)
+        call("irk_to_stage_major", ctx(), m, s, ptr(self._last_stages_dev), ptr(out))
+        return la.to_host(out)
+
+    @property
+    def t(self) -> float:
+        return self._t_base + self.step_index * self._dt
+
+    @property
+    def dt(self) -> float:
+        return self._dt
+
+    @dt.setter
+    def dt(self, value):
+        if value <= 0:
+            raise ValueError("dt must be positive")
+        if value != self._dt:
+            self._t_base = self.t
+            self.step_index = 0
+            self._dt = float(value)
+            self._pc_cache.clear()
+            self._dirk_factors.clear()
+            self._op_cache.clear()
+
+    def _commit(self, u_next_dev):
+        self._u_dev = u_next_dev
+        self._u_host = None
+        self.step_index += 1
+
+    def _dofs(self, problem=None):
+        bc = (problem or self.problem).dirichlet
+        return bc.dofs if bc is not None else np.empty(0, dtype=np.int64)
+
+    # -- caches (stepper.py:230-260) ------------------------------------------
+    def _preconditioner(self, form: Splitting, problem=None, Ks=None, shift=None):
+        if self.pc_kind is None:
+            return None
+        problem = problem or self.problem
+        if Ks is not None:
+            return build_preconditioner(self.pc_kind, self.tableau, problem.mass, Ks, self._dt,
+                                        form, self._dofs(problem), self.block_solver, shift)
+        key = (form, self.pc_kind, id(problem))
+        pc = self._pc_cache.get(key)
+        if pc is None or pc.dt != self._dt:
+            pc = build_preconditioner(self.pc_kind, self.tableau, problem.mass, problem.stiffness,
+                                      self._dt, form, self._dofs(problem), self.block_solver)
+            self._pc_cache[key] = pc
+        return pc
+
+    def _dirk_factor(self, aii, problem=None):
+        problem = problem or self.problem
+        key = (aii, id(problem))
+        fac = self._dirk_factors.get(key)
+        if fac is None:
+            st = self.dirk_solver or BlockSolveSettings(
+                rtol=self.krylov.rtol, atol=self.krylov.atol,
+                maxit=max(20000, 10 * problem.m), raise_on_maxit=True)
+            fac = factorize_block(problem.mass, problem.stiffness, 1.0, self._dt * aii,
+                                  self._dofs(problem), settings=st)
+            self._dirk_factors[key] = fac
+        return fac
+
+    def _stage_operator(self, problem, form: Splitting):
+        key = (id(problem), form, self._dt)
+        op = self._op_cache.get(key)
+        if op is None:
+            s = self.tableau.s
+            if form is Splitting.AI:
+                op = KroneckerStageOperator(np.eye(s), self.tableau.A, problem.mass,
+                                            [problem.stiffness], self._dt)
+            else:
+                op = KroneckerStageOperator(np.linalg.inv(self.tableau.A), np.eye(s),
+                                            problem.mass, [problem.stiffness], self._dt)
+            self._op_cache[key] = op
+        return op
+
+    # -- stepping ---------------------------------------------------------
+    def step_device(self, problem: SemidiscreteProblem | None = None):
+        """One step; returns (u_next as a CUDA tensor, StepReport)."""
+        problem = problem if problem is not None else self.problem
+        if self.formulation is StageFormulation.DIRK:
+            return _step_dirk_dev(self, problem)
+        if problem.is_linear:
+            return _step_linear_dev(self, problem)
+        return _step_newton_dev(self, problem)
+
+    def step(self, problem: SemidiscreteProblem | None = None):
+        """One step (stepper.py:262-268); returns (u_next numpy, StepReport)."""
+        _, rep = self.step_device(problem)
+        return self.u.copy(), rep
+
+
+# ------------------------------------------------------------ stage data
+
+
+def _stage_loads(problem, times, m):
+    """Loads at the stage times as an interleaved m-by-s device block, or
+    None for the zero load."""
+    if getattr(problem.load, "_irk_zero", False):
+        return None
+    vals = [problem.load(t) for t in times]
+    if all(la.is_torch(v) and v.device.type == "cuda" for v in vals):
+        import torch
+
+        return torch.stack([v.to(torch.float64) for v in vals], dim=1).reshape(-1).contiguous()
+    host = np.stack([la.to_host(v) if la.is_torch(v) else np.asarray(v, dtype=np.float64)
+                     for v in vals], axis=1)
+    return la.to_dev(np.ascontiguousarray(host).reshape(-1))
+
+
+def _linear_rhs_dev(problem, tab, t, dt, form: Splitting, u_dev):
+    """AI/IA: rhs_i = f(t + c_i dt) - K u (stepper.py:291-293)."""
+    s, m = tab.s, problem.m
+    F = _stage_loads(problem, [t + c * dt for c in tab.c], m)
+    out = la.dev_empty(m * s)
+    G = np.ascontiguousarray(np.eye(s))
+    call("irk_stage_rhs", ctx(), m, s, -1.0, problem.stiffness.device().handle, ptr(u_dev),
+         hptr(G), ptr(F), ptr(out))
+    return out
+
+
+def _value_rhs_dev(problem, tab, t, dt, u_dev):
+    """VALUE: rhs_i = M u + dt sum_j a_ij f(t + c_j dt) (stepper.py:305-313)."""
+    s, m = tab.s, problem.m
+    F = _stage_loads(problem, [t + c * dt for c in tab.c], m)
+    out = la.dev_empty(m * s)
+    G = np.ascontiguousarray(dt * np.asarray(tab.A))
+    call("irk_stage_rhs", ctx(), m, s, 1.0, problem.mass.device().handle, ptr(u_dev), hptr(G),
+         ptr(F), ptr(out))
+    return out
+
+
+def _to_il(v_stage_major, m, s):
+    vd = la.to_dev(v_stage_major)
+    out = la.dev_empty(m * s)
+    call("irk_to_interleaved", ctx(), m, s, ptr(vd), ptr(out))
+    return out
+
+
+def _to_sm(v_il, m, s):
+    out = la.dev_empty(m * s)
+    call("irk_to_stage_major", ctx(), m, s, ptr(v_il), ptr(out))
+    return out
+
+
+def assemble_linear_stage_system(problem: SemidiscreteProblem, tab: ButcherTableau, t: float,
+                                 dt: float, form: Splitting, u):
+    """(op, rhs) of the linear stage-derivative system (stepper.py:275-302);
+    rhs is stage-major, numpy for numpy input."""
+    if not problem.is_linear:
+        raise ValueError("assemble_linear_stage_system needs a linear problem")
+    s = tab.s
+    if form is Splitting.AI:
+        op = KroneckerStageOperator(np.eye(s), tab.A, problem.mass, [problem.stiffness], dt)
+    else:
+        if not tab.invertible:
+            raise FormulationError(f"IA splitting needs an invertible tableau, got {tab.name!r}")
+        op = KroneckerStageOperator(np.linalg.inv(tab.A), np.eye(s), problem.mass,
+                                    [problem.stiffness], dt)
+    rhs = _to_sm(_linear_rhs_dev(problem, tab, t, dt, form, la.to_dev(u)), problem.m, s)
+    return op, la._like_input(rhs, u)
+
+
+def _stage_value_system(problem, tab, t, dt, u):
+    """(op, rhs) of the stage-value system (stepper.py:305-313), stage-major rhs."""
+    s = tab.s
+    op = KroneckerStageOperator(np.eye(s), tab.A, problem.mass, [problem.stiffness], dt)
+    rhs = _to_sm(_value_rhs_dev(problem, tab, t, dt, la.to_dev(u)), problem.m, s)
+    return op, la._like_input(rhs, u)
+
+
+def _solve_constrained_dev(stepper, problem, op, rhs_il, unknown, t):
+    """Constrain, solve (FGMRES), re-impose boundary stage values
+    (stepper.py:316-338) on interleaved device data."""
+    bc = problem.dirichlet
+    svals = None
+    if bc is not None and len(bc.dofs):
+        svals = stage_bc_values(stepper.bc_method, stepper.tableau, bc, stepper._u_dev, t,
+                                stepper.dt, unknown)
+        sop, srhs = constrain_stage_system_dev(op, rhs_il, bc, svals)
+        A = sop._dev_op()
+    else:
+        A, srhs = op._dev_op(), rhs_il
+    pc = stepper._preconditioner(_SPLIT[stepper.formulation], problem)
+    P = pc._dev_op() if pc is not None else None
+    if pc is not None:
+        pc.inner_iterations = []
+    x0 = None
+    if stepper.warm_start and stepper._last_stages_dev is not None:
+        if stepper._last_stages_dev.numel() == srhs.numel():
+            x0 = stepper._last_stages_dev
+    res = fgmres_device(A, srhs, P, stepper.krylov, x0)
+    x = res.x
+    if svals is not None:
+        scatter_stage_values(x, bc.dofs_dev(), svals, op.s)
+    stepper._last_stages_dev = x.clone()
+    res.inner = list(pc.inner_iterations) if pc is not None else []
+    return x, res
+
+
+def _solve_constrained(stepper, problem, op, rhs, unknown, t):
+    """Reference-layout wrapper of the constrained solve (stage-major x)."""
+    x_il, res = _solve_constrained_dev(stepper, problem, op, _to_il(rhs, op.m, op.s), unknown, t)
+    xs = _to_sm(x_il, op.m, op.s)
+    return la._like_input(xs, rhs), res
+
+
+def _update(tab, dt, form, u_dev, X_il, m):
+    """Fused Runge-Kutta update (stepper.py:352-361)."""
+    s = tab.s
+    out = la.dev_empty(m)
+    if form is StageFormulation.STAGE_VALUE:
+        if tab.stiffly_accurate:
+            call("irk_stage_update", ctx(), m, s, 0.0, ptr(None), hptr(np.zeros(s)), s - 1,
+                 ptr(X_il), ptr(out))
+            return out
+        w = np.linalg.solve(np.asarray(tab.A).T, tab.b)
+        a = 1.0 - float(np.sum(w))
+    elif form is StageFormulation.STAGE_DERIVATIVE_AI:
+        w, a = dt * np.asarray(tab.b), 1.0
+    else:
+        w, a = dt * np.linalg.solve(np.asarray(tab.A).T, tab.b), 1.0
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    call("irk_stage_update", ctx(), m, s, a, ptr(u_dev), hptr(w), -1, ptr(X_il), ptr(out))
+    return out
+
+
+def _step_linear_dev(stepper: TimeStepper, problem: SemidiscreteProblem):
+    tab, dt, t = stepper.tableau, stepper.dt, stepper.t
+    form = stepper.formulation
+    if form is StageFormulation.DIRK:
+        return _step_dirk_dev(stepper, problem)
+    split = _SPLIT[form]
+    op = stepper._stage_operator(problem, split)
+    if form is StageFormulation.STAGE_VALUE:
+        rhs = _value_rhs_dev(problem, tab, t, dt, stepper._u_dev)
+    else:
+        rhs = _linear_rhs_dev(problem, tab, t, dt, split, stepper._u_dev)
+    x, res = _solve_constrained_dev(stepper, problem, op, rhs, _UNKNOWN[form], t)
+    u_next = _update(tab, dt, form, stepper._u_dev, x, problem.m)
+    report = StepReport(0, res.iterations, res.residuals[-1], inner_iters=res.inner)
+    stepper._commit(u_next)
+    return u_next, report
+
+
+def step_linear(stepper: TimeStepper, problem: SemidiscreteProblem):
+    """One linear fully coupled step (stepper.py:341-364)."""
+    _, rep = _step_linear_dev(stepper, problem)
+    return stepper.u.copy(), rep
+
+
+# -------------------------------------------------------------------- DIRK
+
+
+def _dirk_stage_acc(u_dev, K_il, weights, m, s):
+    out = la.dev_empty(m)
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    call("irk_stage_update", ctx(), m, s, 1.0, ptr(u_dev), hptr(w), -1, ptr(K_il), ptr(out))
+    return out
+
+
+def _step_dirk_dev(stepper: TimeStepper, problem: SemidiscreteProblem):
+    """Sequential stage solves (stepper.py:367-424).  Linear stages solve the
+    constrained block M + dt*a_ii*K with Jacobi-PCG to the Krylov tolerance
+    (the single block is reused across stages, north_star config 4)."""
+    tab, dt, t = stepper.tableau, stepper.dt, stepper.t
+    if not tab.lower_triangular:
+        raise FormulationError(f"DIRK stepping needs a lower-triangular tableau, got {tab.name!r}")
+    s, m = tab.s, problem.m
+    u = stepper._u_dev
+    bc = problem.dirichlet
+    svals = None
+    if bc is not None and len(bc.dofs):
+        svals = stage_bc_values(stepper.bc_method, tab, bc, u, t, dt, StageUnknown.DERIVATIVE)
+    K_il = la.dev_zeros(m * s)
+    krylov_total = newton_total = 0
+    final_res = 0.0
+    hist = []
+    inner = []
+    A = np.asarray(tab.A)
+    for i in range(s):
+        ti = t + tab.c[i] * dt
+        w = np.zeros(s)
+        w[:i] = dt * A[i, :i]
+        acc = _dirk_stage_acc(u, K_il, w, m, s) if i else u.clone()
+        if problem.is_linear:
+            F = _stage_loads(problem, [ti], m)
+            rhs = la.dev_empty(m)
+            call("irk_stage_rhs", ctx(), m, 1, -1.0, problem.stiffness.device().handle, ptr(acc),
+                 hptr(np.ones(1)), ptr(F), ptr(rhs))
+            op = KroneckerStageOperator(np.eye(1), np.array([[A[i, i]]]), problem.mass,
+                                        [problem.stiffness], dt)
+            if svals is not None:
+                _, srhs = constrain_stage_system_dev(op, rhs, bc, svals[i:i + 1])
+            else:
+                srhs = rhs
+            fac = stepper._dirk_factor(A[i, i], problem)
+            ki = la.dev_empty(m)
+            its = fac.dev_solve(srhs, ki)
+            krylov_total += its
+            inner.append(its)
+            final_res = fac.last_relres * la._norm(srhs) if its else 0.0
+        else:
+            ki, nit, kit, h = _dirk_stage_newton_dev(stepper, problem, ti, acc, A[i, i],
+                                                     svals[i] if svals is not None else None)
+            newton_total += nit
+            krylov_total += kit
+            hist.extend(h)
+            final_res = h[-1]
+        if svals is not None:
+            scatter_stage_values(ki, bc.dofs_dev(), svals[i:i + 1], 1)
+        call("irk_stage_set", ctx(), m, s, i, ptr(ki), ptr(K_il))
+    u_next = la.dev_empty(m)
+    wb = np.ascontiguousarray(dt * np.asarray(tab.b))
+    call("irk_stage_update", ctx(), m, s, 1.0, ptr(u), hptr(wb), -1, ptr(K_il), ptr(u_next))
+    report = StepReport(newton_total, krylov_total, final_res, hist, inner)
+    stepper._commit(u_next)
+    return u_next, report
+
+
+def step_dirk(stepper: TimeStepper, problem: SemidiscreteProblem):
+    """Sequential DIRK step (stepper.py:367-424); numpy result."""
+    _, rep = _step_dirk_dev(stepper, problem)
+    return stepper.u.copy(), rep
+
+
+def _host_residual(problem, t, u_dev, k_dev):
+    r = problem.residual(t, la.to_host(u_dev), la.to_host(k_dev))
+    return la.to_dev(la.to_host(r) if la.is_torch(r) else np.asarray(r, dtype=np.float64))
+
+
+def _dirk_stage_newton_dev(stepper, problem, ti, acc, aii, sval):
+    """Newton on one DIRK stage residual (stepper.py:427-465)."""
+    dt = stepper.dt
+    m = problem.m
+    dofs = stepper._dofs(problem)
+    bc = problem.dirichlet
+    k = la.dev_zeros(m)
+    if sval is not None:
+        scatter_stage_values(k, bc.dofs_dev(), np.asarray(sval)[None, :], 1)
+    nt = stepper.newton
+    hist = []
+    krylov = 0
+    for it in range(nt.maxit + 1):
+        ui = acc.clone()
+        call("irk_axpby", ctx(), m, dt * aii, ptr(k), 1.0, ptr(ui))
+        R = _host_residual(problem, ti, ui, k)
+        if len(dofs):
+            call("irk_bc_zero", ctx(), 1, len(dofs), ptr(bc.dofs_dev()), ptr(R))
+        normR = la._norm(R)
+        hist.append(normR)
+        if not np.isfinite(normR):
+            raise NonlinearDivergenceError("DIRK stage Newton diverged", hist)
+        if normR <= max(nt.rtol * hist[0], nt.atol):
+            return k, it, krylov, hist
+        if it == nt.maxit:
+            break
+        Ki = problem.jacobian_u(ti, la.to_host(ui))
+        fac = factorize_block(problem.mass, Ki, 1.0, dt * aii, dofs,
+                              settings=BlockSolveSettings(rtol=1e-12, maxit=max(1000, 10 * m)))
+        op = KroneckerStageOperator(np.eye(1), np.array([[aii]]), problem.mass, [Ki], dt)
+        sop = op if not len(dofs) else ConstrainedStageOperator(op, dofs)
+        rhs = R.clone()
+        call("irk_axpby", ctx(), m, -1.0, ptr(R), 0.0, ptr(rhs))
+        res = fgmres_device(sop._dev_op(), rhs, fac._dev_op(), stepper.krylov)
+        krylov += res.iterations
+        delta = res.x
+        if len(dofs):
+            call("irk_bc_zero", ctx(), 1, len(dofs), ptr(bc.dofs_dev()), ptr(delta))
+        call("irk_axpby", ctx(), m, 1.0, ptr(delta), 1.0, ptr(k))
+    raise NonlinearDivergenceError(
+        f"DIRK stage Newton did not converge in {nt.maxit} iterations", hist)
+
+
+# ------------------------------------------------------------------ Newton
+
+
+class _SemilinearJacobianOp(la._DevOp):
+    """C1 (x) M + dt * blockrow_i(kscale K + M diag(D_i)) (C2 (x) I), masked."""
+
+    def __init__(self, C1, C2, dt, Md, Kd, kscale, D, mask, m, s):
+        self.C1 = np.ascontiguousarray(C1, dtype=np.float64)
+        self.C2 = np.ascontiguousarray(C2, dtype=np.float64)
+        self.dt, self.Md, self.Kd, self.kscale, self.D, self.mask = dt, Md, Kd, kscale, D, mask
+        self.n = m * s
+        self.s = s
+        self.layout = (m, s) if s > 1 else None
+
+    def dev_apply(self, x, out):
+        call("irk_stage_apply_semilinear", ctx(), self.s, hptr(self.C1), hptr(self.C2), self.dt,
+             self.Md.handle, self.Kd.handle, float(self.kscale), ptr(self.D), ptr(self.mask),
+             ptr(x), ptr(out))
+
+
+def _step_newton_dev(stepper: TimeStepper, problem: SemidiscreteProblem):
+    form = stepper.formulation
+    if form is StageFormulation.DIRK:
+        return _step_dirk_dev(stepper, problem)
+    if problem.semilinear is not None and _UNKNOWN[form] is StageUnknown.DERIVATIVE:
+        return _step_newton_semilinear(stepper, problem)
+    return _step_newton_generic(stepper, problem)
+
+
+def _newton_bc(stepper, problem, unknown, x_il):
+    tab, dt, t = stepper.tableau, stepper.dt, stepper.t
+    bc = problem.dirichlet
+    if bc is None or not len(bc.dofs):
+        return None
+    svals = stage_bc_values(stepper.bc_method, tab, bc, stepper._u_dev, t, dt, unknown)
+    scatter_stage_values(x_il, bc.dofs_dev(), svals, tab.s)
+    return svals
+
+
+def _step_newton_semilinear(stepper, problem):
+    """Device Newton for F = M u' + kscale K u + M g(u) - f on stage
+    derivatives (stepper.py:474-569 with the residual, the Jacobian operator
+    and the block-Jacobi surrogate blocks formed by kernels)."""
+    tab, dt, t = stepper.tableau, stepper.dt, stepper.t
+    s, m = tab.s, problem.m
+    form = problem.semilinear
+    A = np.ascontiguousarray(tab.A, dtype=np.float64)
+    Md, Kd = la.shared_pattern([problem.mass.device(), problem.stiffness.device()])
+    bc = problem.dirichlet
+    mask = bc.mask_dev(m) if bc is not None and len(bc.dofs) else None
+    x = la.dev_zeros(m * s)
+    _newton_bc(stepper, problem, StageUnknown.DERIVATIVE, x)
+    coef = np.ascontiguousarray(np.asarray(form.coef, dtype=np.float64))
+    F = _stage_loads(problem, [t + c * dt for c in tab.c], m)
+    R = la.dev_empty(m * s)
+    D = la.dev_empty(m * s)
+    nt = stepper.newton
+    hist = []
+    krylov_total = 0
+    inner = []
+    pc_kind = stepper.pc_kind
+    lumped = None
+    for it in range(nt.maxit + 1):
+        call("irk_semilinear_residual", ctx(), s, hptr(A), dt, Md.handle, Kd.handle,
+             float(form.kscale), len(coef), hptr(coef), ptr(stepper._u_dev), ptr(x), ptr(F),
+             ptr(mask), ptr(R), ptr(D))
+        normR = la._norm(R)
+        hist.append(normR)
+        if not np.isfinite(normR):
+            raise NonlinearDivergenceError("Newton iteration diverged", hist)
+        if normR <= max(nt.rtol * hist[0], nt.atol):
+            break
+        if it == nt.maxit:
+            raise NonlinearDivergenceError(
+                f"Newton did not converge in {nt.maxit} iterations (residual {normR:.3e})", hist)
+        op = _SemilinearJacobianOp(np.eye(s), A, dt, Md, Kd, form.kscale, D, mask, m, s)
+        pc = None
+        if pc_kind is PreconditionerKind.BLOCK_DIAGONAL:
+            # SPD surrogate of M + dt a_ii (kscale K + M diag(D_i)):
+            #   M + dt a_ii kscale K + diag(dt a_ii * rowsum(M) * D_i)
+            if lumped is None:
+                lumped = Md.rowsum()
+            shift = la.dev_empty(m * s)
+            wdiag = np.ascontiguousarray(dt * np.diag(A))
+            call("irk_stage_scale", ctx(), m, s, hptr(wdiag), ptr(lumped), ptr(D), ptr(shift))
+            pc = _SurrogateBlockJacobi(problem, tab, dt, form.kscale, shift, Md, Kd, mask,
+                                       stepper.block_solver)
+        elif pc_kind is not None:
+            Ks = []
+            for i in range(s):
+                h = la.C.c_void_p()
+                call("irk_mat_semilinear_jacobian", ctx(), Md.handle, Kd.handle,
+                     float(form.kscale), ptr(D), s, i, la.C.byref(h))
+                Ks.append(SparseMatrix._from_device(la.DeviceMatrix(h)))
+            pc = stepper._preconditioner(Splitting.AI, problem, Ks)
+        rhs = R.clone()
+        call("irk_axpby", ctx(), m * s, -1.0, ptr(R), 0.0, ptr(rhs))
+        res = fgmres_device(op, rhs, pc._dev_op() if pc is not None else None, stepper.krylov)
+        krylov_total += res.iterations
+        if pc is not None:
+            inner.extend(pc.inner_iterations)
+        delta = res.x
+        if mask is not None:
+            call("irk_bc_zero", ctx(), s, len(bc.dofs), ptr(bc.dofs_dev()), ptr(delta))
+        call("irk_axpby", ctx(), m * s, 1.0, ptr(delta), 1.0, ptr(x))
+    u_next = la.dev_empty(m)
+    wb = np.ascontiguousarray(dt * np.asarray(tab.b))
+    call("irk_stage_update", ctx(), m, s, 1.0, ptr(stepper._u_dev), hptr(wb), -1, ptr(x),
+         ptr(u_next))
+    report = StepReport(len(hist) - 1, krylov_total, hist[-1], hist, inner)
+    stepper._commit(u_next)
+    return u_next, report
+
+
+class _SurrogateBlockJacobi:
+    """Block-Jacobi preconditioner of the semilinear Newton system with SPD
+    surrogate blocks  M + dt a_ii kscale K + diag(shift_i),  all s blocks in
+    one batched Jacobi-PCG."""
+
+    def __init__(self, problem, tab, dt, kscale, shift, Md, Kd, mask, settings):
+        self.s, self.m = tab.s, problem.m
+        self.alpha = [1.0] * tab.s
+        self.beta = [dt * float(tab.A[i, i]) * kscale for i in range(tab.s)]
+        self.shift, self.Md, self.Kd, self.mask = shift, Md, Kd, mask
+        self.settings = settings
+        self.inner_iterations = []
+
+    def _dev_op(self):
+        pc = self
+
+        class _Op(la._DevOp):
+            n = pc.s * pc.m
+            layout = (pc.m, pc.s) if pc.s > 1 else None
+
+            def dev_apply(self, x, out):
+                pc.dev_apply(x, out)
+
+        return _Op()
+
+    def dev_apply(self, R, X):
+        from . import _lib
+
+        s = self.s
+        st = self.settings
+        its = np.zeros(8, dtype=np.int32)
+        rel = np.zeros(8)
+        al = np.ascontiguousarray(self.alpha + [0.0] * (8 - s))
+        be = np.ascontiguousarray(self.beta + [0.0] * (8 - s))
+        status = _lib.load().irk_pcg(ctx(), s, hptr(al), hptr(be), self.Md.handle, self.Kd.handle,
+                                     ptr(self.shift), ptr(self.mask), ptr(R), s, ptr(X), s,
+                                     float(st.rtol), float(st.atol), int(st.maxit), hptr(its),
+                                     hptr(rel))
+        self.inner_iterations.append([int(v) for v in its[:s]])
+        if status not in (_lib.IRK_OK, _lib.IRK_ENOCONV, _lib.IRK_ESINGULAR):
+            _lib.check(status, "surrogate block-Jacobi")
+        return X
+
+
+def _step_newton_generic(stepper, problem):
+    """Newton on the stacked stage residual with user callbacks
+    (stepper.py:474-569).  Residual and Jacobian callbacks are user host
+    code; states, Krylov solves and preconditioners stay on the device."""
+    tab, dt, t = stepper.tableau, stepper.dt, stepper.t
+    form = stepper.formulation
+    unknown = _UNKNOWN[form]
+    s, m = tab.s, problem.m
+    A = np.asarray(tab.A, dtype=np.float64)
+    c = tab.c
+    bc = problem.dirichlet
+    dofs = stepper._dofs(problem)
+    u = stepper._u_dev
+    if unknown is StageUnknown.VALUE:
+        x = la.dev_empty(m * s)
+        call("irk_stage_rhs", ctx(), m, s, 1.0, ptr(None), ptr(u), hptr(np.zeros((s, s))),
+             ptr(None), ptr(x))
+    else:
+        x = la.dev_zeros(m * s)
+    _newton_bc(stepper, problem, unknown, x)
+    Ainv = np.linalg.inv(A) if unknown is not StageUnknown.DERIVATIVE else None
+
+    def stage_states(X):
+        U = la.dev_empty(m * s)
+        Kv = la.dev_empty(m * s)
+        if unknown is StageUnknown.DERIVATIVE:
+            call("irk_stage_rhs", ctx(), m, s, 1.0, ptr(None), ptr(u), hptr(dt * A), ptr(X), ptr(U))
+            Kv.copy_(X)
+        elif unknown is StageUnknown.W:
+            call("irk_stage_mix", ctx(), m, s, s, hptr(np.ascontiguousarray(Ainv)), ptr(X), ptr(Kv))
+            call("irk_stage_rhs", ctx(), m, s, 1.0, ptr(None), ptr(u), hptr(dt * np.eye(s)), ptr(X),
+                 ptr(U))
+        else:
+            T = la.dev_empty(m * s)
+            call("irk_stage_rhs", ctx(), m, s, -1.0, ptr(None), ptr(u), hptr(np.eye(s)), ptr(X),
+                 ptr(T))
+            call("irk_stage_mix", ctx(), m, s, s, hptr(np.ascontiguousarray(Ainv / dt)), ptr(T),
+                 ptr(Kv))
+            U.copy_(X)
+        return U, Kv
+
+    def residual(X):
+        U, Kv = stage_states(X)
+        Uh = la.to_host(_to_sm(U, m, s)).reshape(s, m)
+        Kh = la.to_host(_to_sm(Kv, m, s)).reshape(s, m)
+        R = np.empty((s, m))
+        for i in range(s):
+            ri = problem.residual(t + c[i] * dt, Uh[i], Kh[i])
+            R[i] = la.to_host(ri) if la.is_torch(ri) else ri
+        Rd = _to_il(R.ravel(), m, s)
+        if len(dofs):
+            call("irk_bc_zero", ctx(), s, len(dofs), ptr(bc.dofs_dev()), ptr(Rd))
+        return Rd, Uh
+
+    nt = stepper.newton
+    hist = []
+    krylov_total = 0
+    C1 = np.eye(s) if unknown is StageUnknown.DERIVATIVE else np.linalg.inv(A)
+    C2 = A if unknown is StageUnknown.DERIVATIVE else np.eye(s)
+    pc_form = Splitting.AI if unknown is StageUnknown.DERIVATIVE else Splitting.IA
+    for it in range(nt.maxit + 1):
+        R, Uh = residual(x)
+        normR = la._norm(R)
+        hist.append(normR)
+        if not np.isfinite(normR):
+            raise NonlinearDivergenceError("Newton iteration diverged", hist)
+        if normR <= max(nt.rtol * hist[0], nt.atol):
+            break
+        if it == nt.maxit:
+            raise NonlinearDivergenceError(
+                f"Newton did not converge in {nt.maxit} iterations (residual {normR:.3e})", hist)
+        Ks = [problem.jacobian_u(t + c[i] * dt, Uh[i]) for i in range(s)]
+        op = KroneckerStageOperator(C1, C2, problem.mass, Ks, dt)
+        sop = op if not len(dofs) else ConstrainedStageOperator(op, dofs)
+        pc = stepper._preconditioner(pc_form, problem, Ks)
+        rhs = R.clone()
+        scale = -1.0 if unknown is not StageUnknown.VALUE else -dt
+        call("irk_axpby", ctx(), m * s, scale, ptr(R), 0.0, ptr(rhs))
+        res = fgmres_device(sop._dev_op(), rhs, pc._dev_op() if pc is not None else None,
+                            stepper.krylov)
+        krylov_total += res.iterations
+        delta = res.x
+        if len(dofs):
+            call("irk_bc_zero", ctx(), s, len(dofs), ptr(bc.dofs_dev()), ptr(delta))
+        call("irk_axpby", ctx(), m * s, 1.0, ptr(delta), 1.0, ptr(x))
+    if unknown is StageUnknown.VALUE and tab.stiffly_accurate:
+        u_next = la.dev_empty(m)
+        call("irk_stage_update", ctx(), m, s, 0.0, ptr(None), hptr(np.zeros(s)), s - 1, ptr(x),
+             ptr(u_next))
+    else:
+        _, Kv = stage_states(x)
+        u_next = la.dev_empty(m)
+        wb = np.ascontiguousarray(dt * np.asarray(tab.b))
+        call("irk_stage_update", ctx(), m, s, 1.0, ptr(u), hptr(wb), -1, ptr(Kv), ptr(u_next))
+    report = StepReport(len(hist) - 1, krylov_total, hist[-1], hist)
+    stepper._commit(u_next)
+    return u_next, report
+
+
+def step_newton(stepper: TimeStepper, problem: SemidiscreteProblem):
+    """Newton step (stepper.py:474-569); numpy result."""
+    _, rep = _step_newton_dev(stepper, problem)
+    return stepper.u.copy(), rep
+
+
+def advance(stepper: TimeStepper, problem: SemidiscreteProblem, t_final: float):
+    """Step to t_final, shortening the last step (stepper.py:572-605)."""
+    if t_final < stepper.t - 1e-12 * max(1.0, abs(stepper.t)):
+        raise ValueError("t_final lies before the current time")
+    span = t_final - stepper.t
+    ratio = span / stepper.dt
+    n = round(ratio)
+    if abs(ratio - n) <= 1e-9 * max(1.0, abs(ratio)):
+        steps, short = int(n), 0.0
+    else:
+        steps = int(np.floor(ratio))
+        short = span - steps * stepper.dt
+    reports = []
+    dt_orig = stepper.dt
+    try:
+        for _ in range(steps):
+            _, rep = stepper.step_device(problem)
+            reports.append(rep)
+        if short > 0.0:
+            stepper.dt = short
+            _, rep = stepper.step_device(problem)
+            reports.append(rep)
+            stepper.dt = dt_orig
+    except (NonConvergenceError, NonlinearDivergenceError) as exc:
+        raise StepFailure(
+            f"step {len(reports) + 1} failed after {len(reports)} completed steps: {exc}",
+            len(reports), reports) from exc
+    return stepper.u, reports
