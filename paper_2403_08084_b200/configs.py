@@ -1,0 +1,82 @@
+"""The five BASELINE.json workloads as ready-to-run TimeStepper setups.
+
+Recipe: vertices lexicographic x fastest; noise =
+default_rng(seed).uniform(-1, 1, m) over all vertices; boundary entries of u0
+set to g(0); zero load; GMRES restart 50, maxit 500, right preconditioning.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import problems as pb
+from .precond import PreconditionerKind
+from .sparsela import BlockSolveSettings, KrylovSettings
+from .stepper import NewtonSettings, StageFormulation, TimeStepper
+from .tableaux import alexander_dirk, gauss_legendre, radau_iia
+
+DESCRIPTIONS = {
+    1: "2D heat P1 32x32, RadauIIA s=2, stage-derivative (AI), dt=1/32, 10 steps, "
+       "GMRES 1e-12, block-Jacobi",
+    2: "2D heat P1 1024x1024 (~1.05M DOFs), RadauIIA s=3, stage-value, dt=1e-3, 20 steps, "
+       "GMRES 1e-12, block-Gauss-Seidel, inner Jacobi-PCG 1e-6",
+    3: "3D heat P1 96^3 Kuhn tets (~0.91M DOFs), Gauss-Legendre s=4, DAE Dirichlet "
+       "exp(-t)sin(pi x), dt=5e-3, 10 steps, GMRES 1e-12, real-Schur block-diagonal",
+    4: "2D heat P1 2048x2048 (~4.2M DOFs), Alexander SDIRK, dt=1e-3, 50 steps, one reused "
+       "stage operator, Jacobi-PCG 1e-12",
+    5: "Allen-Cahn eps=0.02 P1 1024x1024, Neumann, RadauIIA s=3, AI, dt=1e-3, 20 steps, "
+       "Newton atol 1e-10, GMRES 1e-10, block-Jacobi",
+}
+
+SEEDS = {1: 0, 2: 1, 3: 2, 4: 3, 5: 4}
+GRID = {1: (2, 32), 2: (2, 1024), 3: (3, 96), 4: (2, 2048), 5: (2, 1024)}
+DT = {1: 1.0 / 32, 2: 1e-3, 3: 5e-3, 4: 1e-3, 5: 1e-3}
+STEPS = {1: 10, 2: 20, 3: 10, 4: 50, 5: 20}
+
+
+@dataclass
+class Workload:
+    k: int
+    problem: object
+    stepper: TimeStepper
+    steps: int
+    description: str
+
+
+def initial_state(k: int, grid: pb.StructuredGrid) -> np.ndarray:
+    m = grid.npoints
+    noise = pb.seeded_noise(m, SEEDS[k])
+    X = grid.coords()
+    prod = np.prod(np.sin(np.pi * X), axis=1)
+    if k in (1, 2, 3):
+        return prod + 0.01 * noise
+    if k == 4:
+        return noise
+    return 0.1 * noise
+
+
+def build(k: int, n: int | None = None, inner_rtol: float = 1e-6) -> Workload:
+    dim, n0 = GRID[k]
+    grid = pb.StructuredGrid(dim, n or n0)
+    u0 = initial_state(k, grid)
+    if k == 5:
+        prob = pb.allen_cahn_problem(grid, 0.02, u0)
+    elif k == 3:
+        prob = pb.heat_problem(grid, u0, g=lambda t, x, y, z: np.exp(-t) * np.sin(np.pi * x))
+    else:
+        prob = pb.heat_problem(grid, u0)
+    tab = {1: radau_iia(2), 2: radau_iia(3), 3: gauss_legendre(4), 4: alexander_dirk(),
+           5: radau_iia(3)}[k]
+    form = {1: StageFormulation.STAGE_DERIVATIVE_AI, 2: StageFormulation.STAGE_VALUE,
+            3: StageFormulation.STAGE_DERIVATIVE_AI, 4: StageFormulation.DIRK,
+            5: StageFormulation.STAGE_DERIVATIVE_AI}[k]
+    pc = {1: PreconditionerKind.BLOCK_DIAGONAL, 2: PreconditionerKind.BLOCK_LOWER,
+          3: PreconditionerKind.SCHUR, 4: None, 5: PreconditionerKind.BLOCK_DIAGONAL}[k]
+    kw = dict(formulation=form, krylov=KrylovSettings(rtol=1e-10 if k == 5 else 1e-12),
+              pc_kind=pc, block_solver=BlockSolveSettings(rtol=inner_rtol))
+    if k == 5:
+        kw["newton"] = NewtonSettings(rtol=1e-10, atol=1e-10)
+    st = TimeStepper(prob, tab, DT[k], **kw)
+    return Workload(k, prob, st, STEPS[k], DESCRIPTIONS[k])

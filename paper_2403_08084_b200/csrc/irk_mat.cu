@@ -332,20 +332,23 @@ __device__ __forceinline__ void p1_1d_entry(int64_t N, int64_t a, int64_t b, dou
   }
 }
 
-__global__ void k_q1_count(int64_t N, int64_t m, int* __restrict__ counts) {
+// full_x: every x index of a neighbouring block row is stored (the
+// block-sparse pattern the reference's K takes on grids with N <= 4, where
+// scipy's kron switches to dense BSR blocks and keeps their explicit zeros).
+__global__ void k_q1_count(int64_t N, int64_t m, int full_x, int* __restrict__ counts) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) {
     if (r == m) counts[m] = 0;
     return;
   }
   int64_t n1 = N + 1, i = r % n1, j = r / n1;
-  int cx = 1 + (i > 0) + (i < N), cy = 1 + (j > 0) + (j < N);
+  int cx = full_x ? (int)n1 : 1 + (i > 0) + (i < N), cy = 1 + (j > 0) + (j < N);
   counts[r] = cx * cy;
 }
 
-__global__ void k_q1_fill(int64_t N, int64_t m, double h, const int* __restrict__ rowptr,
-                          int* __restrict__ col, double* __restrict__ mval,
-                          double* __restrict__ kval) {
+__global__ void k_q1_fill(int64_t N, int64_t m, double h, int full_x,
+                          const int* __restrict__ rowptr, int* __restrict__ col,
+                          double* __restrict__ mval, double* __restrict__ kval) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
   int64_t n1 = N + 1, i = r % n1, j = r / n1;
@@ -354,12 +357,13 @@ __global__ void k_q1_fill(int64_t N, int64_t m, double h, const int* __restrict_
     if (jj < 0 || jj > N) continue;
     double my, ky;
     p1_1d_entry(N, j, jj, h, my, ky);
-    for (int64_t ii = i - 1; ii <= i + 1; ++ii) {
+    int64_t lo = full_x ? 0 : i - 1, hi = full_x ? N : i + 1;
+    for (int64_t ii = lo; ii <= hi; ++ii) {
       if (ii < 0 || ii > N) continue;
-      double mx, kx;
-      p1_1d_entry(N, i, ii, h, mx, kx);
+      double mx = 0.0, kx = 0.0;
+      if (ii >= i - 1 && ii <= i + 1) p1_1d_entry(N, i, ii, h, mx, kx);
       col[p] = (int)(jj * n1 + ii);
-      mval[p] = my * mx;
+      if (mval) mval[p] = my * mx;
       kval[p] = ky * mx + my * kx;
       ++p;
     }
@@ -583,7 +587,7 @@ int irk_mat_from_csr(irk_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz,
 }
 
 static int assemble_common(irk_ctx* ctx, int64_t m, int64_t N, int dim, bool q1, irk_mat** Mo,
-                           irk_mat** Ko) {
+                           irk_mat** Ko, int full_x = 0) {
   Pattern* P = pattern_new();
   P->nrows = P->ncols = m;
   IRK_CUDA(cudaMalloc(&P->rowptr, (m + 1) * sizeof(int)));
@@ -592,7 +596,7 @@ static int assemble_common(irk_ctx* ctx, int64_t m, int64_t N, int dim, bool q1,
   unsigned g = (unsigned)((m + 1 + kBlock - 1) / kBlock);
   double h = 1.0 / (double)N;
   if (q1)
-    k_q1_count<<<g, kBlock, 0, ctx->stream>>>(N, m, counts);
+    k_q1_count<<<g, kBlock, 0, ctx->stream>>>(N, m, full_x, counts);
   else
     k_p1_count<<<g, kBlock, 0, ctx->stream>>>(dim, N, m, h, counts);
   IRK_CHECK_LAUNCH(ctx);
@@ -606,7 +610,7 @@ static int assemble_common(irk_ctx* ctx, int64_t m, int64_t N, int dim, bool q1,
   IRK_CUDA(cudaMalloc(&mv, ((size_t)nnz + 1) * sizeof(double)));
   IRK_CUDA(cudaMalloc(&kv, ((size_t)nnz + 1) * sizeof(double)));
   if (q1)
-    k_q1_fill<<<g, kBlock, 0, ctx->stream>>>(N, m, h, P->rowptr, P->col, mv, kv);
+    k_q1_fill<<<g, kBlock, 0, ctx->stream>>>(N, m, h, full_x, P->rowptr, P->col, mv, kv);
   else
     k_p1_fill<<<g, kBlock, 0, ctx->stream>>>(dim, N, m, h, P->rowptr, P->col, mv, kv);
   IRK_CHECK_LAUNCH(ctx);
@@ -641,7 +645,18 @@ int irk_mat_assemble_q1(irk_ctx* ctx, int64_t N, irk_mat** M, irk_mat** K) {
   IRK_REQUIRE(N >= 1, "irk_mat_assemble_q1: need N >= 1");
   int64_t m = (N + 1) * (N + 1);
   IRK_REQUIRE(m * 9 < (int64_t)INT32_MAX / 2, "irk_mat_assemble_q1: grid too large");
-  return assemble_common(ctx, m, N, 2, true, M, K);
+  IRK_TRY(assemble_common(ctx, m, N, 2, true, M, K));
+  // scipy.sparse.kron (format=None) returns dense BSR blocks when the 1D
+  // factor is at least half full, 2 (3N+1) >= (N+1)^2, i.e. N <= 4; the
+  // reference's K then stores those blocks' explicit zeros.
+  if (2 * (3 * N + 1) >= (N + 1) * (N + 1)) {
+    irk_mat *Mb = nullptr, *Kb = nullptr;
+    IRK_TRY(assemble_common(ctx, m, N, 2, true, &Mb, &Kb, 1));
+    irk_mat_destroy(Mb);
+    irk_mat_destroy(*K);
+    *K = Kb;
+  }
+  return IRK_OK;
 }
 
 int irk_mat_info(const irk_mat* A, int64_t* nrows, int64_t* ncols, int64_t* nnz) {

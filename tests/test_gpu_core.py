@@ -1,0 +1,325 @@
+"""CUDA path vs the oracle / reference goldens: assembly, stage operator,
+Krylov building blocks, inner block solvers and preconditioners (gpu)."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def irk(cuda):
+    import paper_2403_08084_b200 as irk
+
+    return irk
+
+
+# ------------------------------------------------------------------ assembly
+
+
+@pytest.mark.parametrize("dim,n", [(1, 5), (1, 9), (2, 4), (2, 7)])
+def test_reference_assembly_bit_exact(irk, golden, dim, n):
+    """assemble_heat (1D P1 / 2D Q1) reproduces the reference bit for bit."""
+    M, K, bd = irk.assemble_heat(irk.StructuredGrid(dim, n))
+    for name, A in (("M", M), ("K", K)):
+        key = f"asm{dim}d{n}_{name}"
+        np.testing.assert_array_equal(A.row_offsets, golden[key + "_rowptr"])
+        np.testing.assert_array_equal(A.col_indices, golden[key + "_col"])
+        np.testing.assert_array_equal(A.values, golden[key + "_val"])
+    np.testing.assert_array_equal(bd, golden[f"asm{dim}d{n}_bd"])
+
+
+@pytest.mark.parametrize("dim,n", [(1, 7), (2, 4), (2, 32), (2, 129), (3, 2), (3, 5), (3, 12)])
+def test_p1_assembly_vs_oracle(irk, oracle, dim, n):
+    """Indices bit-exact (as int64), values to 1 ulp-scale."""
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(dim, n))
+    Mo, Ko = oracle.p1_matrices(dim, n)
+    for A, B in ((M, Mo), (K, Ko)):
+        np.testing.assert_array_equal(A.row_offsets, B.indptr.astype(np.int64))
+        np.testing.assert_array_equal(A.col_indices, B.indices.astype(np.int64))
+        np.testing.assert_allclose(A.values, B.data, rtol=4e-16, atol=4e-16 * np.abs(B.data).max())
+    np.testing.assert_array_equal(bd, oracle.grid_boundary(dim, n))
+
+
+def test_p1_config_sizes(irk):
+    """nnz = m + 2 #edges at the config grids."""
+    for dim, n, m, nnz in ((2, 1024, 1050625, 7346177), (3, 96, 912673, 13465441)):
+        M, K, bd = irk.assemble_p1(irk.StructuredGrid(dim, n))
+        assert M.nrows == m and M.nnz == nnz and K.nnz == nnz
+        assert M.device().same_pattern(K.device())
+
+
+def test_sparse_matrix_roundtrip_and_validation(irk):
+    A = sp.random(30, 30, density=0.2, random_state=1, format="csr") + sp.eye(30)
+    S = irk.SparseMatrix.from_scipy(A)
+    x = np.random.default_rng(0).standard_normal(30)
+    np.testing.assert_allclose(irk.spmv(S, x), A @ x, rtol=1e-14, atol=1e-14)
+    with pytest.raises(ValueError):
+        irk.spmv(S, np.ones(29))
+    with pytest.raises(ValueError):
+        irk.SparseMatrix(2, 2, [0, 2, 2], [1, 0], [1.0, 2.0])  # decreasing columns
+
+
+def test_dirichlet_constrain(irk):
+    A = np.array([[4.0, -1, 0], [-1, 4, -1], [0, -1, 4]])
+    C = irk.dirichlet_constrain(irk.SparseMatrix.from_dense(A), [0])
+    expect = A.copy()
+    expect[0, :] = expect[:, 0] = 0
+    expect[0, 0] = 1
+    np.testing.assert_array_equal(C.to_dense(), expect)
+    with pytest.raises(ValueError):
+        irk.dirichlet_constrain(irk.SparseMatrix.identity(3), [7])
+
+
+# ------------------------------------------------------------- stage apply
+
+
+@pytest.mark.parametrize("s,m", [(1, 5), (2, 8), (3, 6), (4, 5)])
+def test_kronecker_apply_vs_reference(irk, golden, s, m):
+    key = f"kron_s{s}m{m}"
+    M = irk.SparseMatrix.from_dense(golden[key + "_M"])
+    K = irk.SparseMatrix.from_dense(golden[key + "_K"])
+    C1, C2, v = golden[key + "_C1"], golden[key + "_C2"], golden[key + "_v"]
+    op = irk.KroneckerStageOperator(C1, C2, M, [K], 0.37)
+    y = op.apply(v)
+    np.testing.assert_allclose(y, golden[key + "_y"], rtol=0, atol=1e-12 * max(1, np.abs(y).max()))
+    Kl = [irk.SparseMatrix.from_dense(k) for k in golden[key + "_Kl"]]
+    yl = irk.KroneckerStageOperator(C1, C2, M, Kl, 0.37).apply(v)
+    np.testing.assert_allclose(yl, golden[key + "_yl"], rtol=0, atol=1e-12 * max(1, np.abs(yl).max()))
+    yc = irk.ConstrainedStageOperator(op, [0, m - 1]).apply(v)
+    np.testing.assert_allclose(yc, golden[key + "_yc"], rtol=0, atol=1e-12 * max(1, np.abs(yc).max()))
+    np.testing.assert_allclose(op.to_dense() @ v, golden[key + "_y"], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("s", [1, 2, 3, 4, 5])
+def test_stage_apply_p1_vs_oracle(irk, oracle, s):
+    n = 40
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(2, n))
+    Mo, Ko = oracle.p1_matrices(2, n)
+    tab = irk.radau_iia(s)
+    rng = np.random.default_rng(s)
+    v = rng.standard_normal(s * M.nrows)
+    for C1, C2 in ((np.eye(s), tab.A), (np.linalg.inv(tab.A), np.eye(s))):
+        op = irk.KroneckerStageOperator(C1, C2, M, [K], 1e-3)
+        ref = oracle.kron_apply(C1, C2, Mo, [Ko], 1e-3, v)
+        assert rel(op.apply(v), ref) < 1e-14
+        idx = oracle.stage_index(s, M.nrows, bd)
+        refc = oracle.constrained(lambda w: oracle.kron_apply(C1, C2, Mo, [Ko], 1e-3, w), idx)(v)
+        assert rel(irk.ConstrainedStageOperator(op, bd).apply(v), refc) < 1e-14
+
+
+def test_semilinear_jacobian_apply(irk, oracle):
+    """Fused Jacobian stage apply == KroneckerStageOperator with explicit
+    per-stage Jacobians kscale K + M diag(D_i) (stepper.py:550-551)."""
+    import torch
+
+    from paper_2403_08084_b200 import stepper as stp
+    from paper_2403_08084_b200 import sparsela as la
+
+    n, s, dt, ks = 24, 3, 1e-3, 0.02 ** 2
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(2, n))
+    m = M.nrows
+    tab = irk.radau_iia(s)
+    rng = np.random.default_rng(3)
+    D = rng.uniform(-1, 2, size=(s, m))
+    Ks = [irk.SparseMatrix.from_scipy(ks * K.to_scipy() + M.to_scipy() @ sp.diags(D[i])) for i in range(s)]
+    v = rng.standard_normal(s * m)
+    ref = irk.KroneckerStageOperator(np.eye(s), tab.A, M, Ks, dt).apply(v)
+    Md, Kd = la.shared_pattern([M.device(), K.device()])
+    Dil = la.to_dev(D.T.copy().ravel())
+    op = stp._SemilinearJacobianOp(np.eye(s), tab.A, dt, Md, Kd, ks, Dil, None, m, s)
+    x = la.to_dev(v.reshape(s, m).T.copy().ravel())
+    out = la.dev_empty(m * s)
+    op.dev_apply(x, out)
+    got = out.cpu().numpy().reshape(m, s).T.ravel()
+    assert rel(got, ref) < 1e-13
+    # masked variant against the constrained reference form
+    mask = la.dof_mask(m, bd)
+    opm = stp._SemilinearJacobianOp(np.eye(s), tab.A, dt, Md, Kd, ks, Dil, mask, m, s)
+    opm.dev_apply(x, out)
+    refc = irk.ConstrainedStageOperator(irk.KroneckerStageOperator(np.eye(s), tab.A, M, Ks, dt), bd).apply(v)
+    assert rel(out.cpu().numpy().reshape(m, s).T.ravel(), refc) < 1e-13
+    assert torch.isfinite(out).all()
+
+
+# ------------------------------------------------------------------ FGMRES
+
+
+@pytest.mark.parametrize("n", [6, 12, 30])
+def test_fgmres_vs_reference(irk, golden, n):
+    A, b = golden[f"fgmres{n}_A"], golden[f"fgmres{n}_b"]
+    res = irk.fgmres(A, b, settings=irk.KrylovSettings(rtol=1e-12, restart=5, maxit=200))
+    np.testing.assert_allclose(res.x, golden[f"fgmres{n}_x"], rtol=1e-10, atol=1e-11)
+    assert abs(res.iterations - int(golden[f"fgmres{n}_its"])) <= 1
+    assert res.residuals[-1] <= 1e-12 * np.linalg.norm(b)
+
+
+def test_fgmres_behaviours(irk):
+    # identity -> 1 iteration; zero rhs -> 0; x0 exact -> 0; non-finite rejected
+    b = np.arange(1.0, 6.0)
+    r = irk.fgmres(np.eye(5), b)
+    assert r.iterations == 1
+    np.testing.assert_allclose(r.x, b, atol=1e-12)
+    r = irk.fgmres(np.eye(4), np.zeros(4))
+    assert r.iterations == 0 and np.all(r.x == 0)
+    r = irk.fgmres(np.diag([2.0, 4.0]), np.array([2.0, 4.0]), x0=np.array([1.0, 1.0]))
+    assert r.iterations == 0
+    with pytest.raises(ValueError):
+        irk.fgmres(np.eye(2), np.array([1.0, np.nan]))
+    rng = np.random.default_rng(6)
+    A = rng.standard_normal((40, 40)) + 2 * np.eye(40)
+    with pytest.raises(irk.NonConvergenceError) as err:
+        irk.fgmres(A, rng.standard_normal(40), settings=irk.KrylovSettings(rtol=1e-14, maxit=3, restart=2))
+    assert len(err.value.residuals) >= 3
+    # exact inverse as a (host callable) preconditioner -> 1 iteration
+    A = rng.standard_normal((8, 8)) + 8 * np.eye(8)
+    Ainv = np.linalg.inv(A)
+    assert irk.fgmres(A, rng.standard_normal(8), pc=lambda v: Ainv @ v).iterations == 1
+    # left preconditioning and restarts
+    A = rng.standard_normal((25, 25)) + 12 * np.eye(25)
+    b = rng.standard_normal(25)
+    r = irk.fgmres(A, b, settings=irk.KrylovSettings(rtol=1e-10, restart=4, maxit=500))
+    assert np.linalg.norm(b - A @ r.x) <= 1e-9 * np.linalg.norm(b)
+    P = np.diag(1 / np.diag(A))
+    r = irk.fgmres(A, b, pc=lambda v: P @ v, settings=irk.KrylovSettings(rtol=1e-12, right_pc=False))
+    np.testing.assert_allclose(A @ r.x, b, atol=1e-9)
+    r2 = irk.fgmres(A, b, settings=irk.KrylovSettings(rtol=1e-12, reorth=True))
+    np.testing.assert_allclose(A @ r2.x, b, atol=1e-10)
+
+
+def test_fgmres_residual_history_monotone(irk):
+    rng = np.random.default_rng(4)
+    A = rng.standard_normal((30, 30)) + 10 * np.eye(30)
+    res = irk.fgmres(A, rng.standard_normal(30), settings=irk.KrylovSettings(rtol=1e-10))
+    h = np.array(res.residuals)
+    assert np.all(np.diff(h) <= 1e-13 * h[0])
+
+
+# ------------------------------------------------------------- block solves
+
+
+@pytest.mark.parametrize("dim,n", [(2, 33), (3, 9)])
+def test_batched_pcg_vs_oracle(irk, oracle, dim, n):
+    from paper_2403_08084_b200 import _lib
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(dim, n))
+    Mo, Ko = oracle.p1_matrices(dim, n)
+    m = M.nrows
+    alphas, betas = [1.0, 1.0, 0.7], [0.01, 0.2, 1e-3]
+    nb = 3
+    rng = np.random.default_rng(7)
+    B = rng.standard_normal((m, nb))
+    rhs = la.to_dev(B.ravel())
+    x = la.dev_empty(m * nb)
+    mask = la.dof_mask(m, bd)
+    its = np.zeros(8, dtype=np.int32)
+    relres = np.zeros(8)
+    st = _lib.load().irk_pcg(_lib.ctx(), nb, _lib.hptr(np.array(alphas)), _lib.hptr(np.array(betas)),
+                             M.device().handle, K.device().handle, _lib.ptr(None), _lib.ptr(mask),
+                             _lib.ptr(rhs), nb, _lib.ptr(x), nb, 1e-12, 0.0, 5000, _lib.hptr(its),
+                             _lib.hptr(relres))
+    assert st == 0
+    X = x.cpu().numpy().reshape(m, nb)
+    for k in range(nb):
+        C = oracle.dirichlet_identity((alphas[k] * Mo + betas[k] * Ko).tocsr(), bd)
+        exact = sp.linalg.spsolve(C.tocsc(), B[:, k])
+        assert rel(X[:, k], exact) < 1e-9
+        assert relres[k] <= 1e-12 and its[k] > 0
+
+
+def test_cocg_complex_symmetric(irk, oracle):
+    from paper_2403_08084_b200 import _lib
+    from paper_2403_08084_b200 import sparsela as la
+
+    n = 25
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(2, n))
+    Mo, Ko = oracle.p1_matrices(2, n)
+    m = M.nrows
+    coefs = [(1.0 + 0j, 0.01 + 0.004j), (0.5 + 0.2j, 0.003 + 0j)]
+    rng = np.random.default_rng(9)
+    Bc = rng.standard_normal((m, 2)) + 1j * rng.standard_normal((m, 2))
+    il = np.zeros((m, 4))
+    il[:, 0::2], il[:, 1::2] = Bc.real, Bc.imag
+    rhs = la.to_dev(il.ravel())
+    x = la.dev_empty(4 * m)
+    mask = la.dof_mask(m, bd)
+    its = np.zeros(8, dtype=np.int32)
+    rr = np.zeros(8)
+    arr = lambda f: _lib.hptr(np.array([f(c) for c in coefs] + [0.0] * 6))  # noqa: E731
+    st = _lib.load().irk_cocg(_lib.ctx(), 2, arr(lambda c: c[0].real), arr(lambda c: c[0].imag),
+                              arr(lambda c: c[1].real), arr(lambda c: c[1].imag), M.device().handle,
+                              K.device().handle, _lib.ptr(mask), _lib.ptr(rhs), 4, _lib.ptr(x), 4,
+                              1e-12, 0.0, 5000, _lib.hptr(its), _lib.hptr(rr))
+    assert st == 0
+    X = x.cpu().numpy().reshape(m, 4)
+    for k, (a, b) in enumerate(coefs):
+        Z = oracle.dirichlet_identity((a * Mo + b * Ko).tocsr(), bd)
+        exact = sp.linalg.spsolve(Z.tocsc(), Bc[:, k])
+        got = X[:, 2 * k] + 1j * X[:, 2 * k + 1]
+        assert np.linalg.norm(got - exact) / np.linalg.norm(exact) < 1e-9
+
+
+def test_factorize_block(irk):
+    M, K, bd = irk.assemble_heat(irk.StructuredGrid(1, 9))
+    fac = irk.factorize_block(M, K, 2.5, 0.1)
+    rng = np.random.default_rng(1)
+    for _ in range(3):
+        b = rng.standard_normal(10)
+        assert np.linalg.norm(fac.matvec(fac.solve(b)) - b) < 1e-10 * np.linalg.norm(b)
+    dense = M.to_dense() + 0.25 * K.to_dense()
+    b = rng.standard_normal(10)
+    np.testing.assert_allclose(irk.factorize_block(M, K, 1.0, 0.25).solve(b),
+                               np.linalg.solve(dense, b), atol=1e-11)
+    with pytest.raises(irk.FactorizationError):
+        irk.factorize_block(K, K, 0.0, 1.0)  # pure Neumann stiffness is singular
+    with pytest.raises(ValueError):
+        irk.factorize_block(M, irk.assemble_heat(irk.StructuredGrid(1, 4))[1], 1.0, 1.0)
+
+
+# ----------------------------------------------------------- preconditioners
+
+
+@pytest.mark.parametrize("tname", ["radau3", "lobatto3"])
+@pytest.mark.parametrize("kind", ["jacobi", "gs-lower", "gs-upper", "rana-ld", "rana-du"])
+@pytest.mark.parametrize("form", ["ai", "ia"])
+def test_preconditioner_vs_reference(irk, golden, tname, kind, form):
+    key = f"pc_{tname}_{kind}_{form}"
+    if key not in golden.files:
+        pytest.skip("reference rejects this kind/form/tableau")
+    M, K, bd = irk.assemble_heat(irk.StructuredGrid(1, 10))
+    tab = irk.radau_iia(3) if tname == "radau3" else irk.lobatto_iiic(3)
+    pc = irk.build_preconditioner(irk.PreconditionerKind(kind), tab, M, K, 0.05,
+                                  irk.Splitting(form), bd,
+                                  settings=irk.BlockSolveSettings(rtol=1e-14, maxit=1000))
+    assert rel(pc.apply(golden[f"pc_{tname}_v"]), golden[key]) < 1e-10
+
+
+@pytest.mark.parametrize("tab_name", ["gauss-legendre:4", "radau-iia:3", "gauss-legendre:3"])
+@pytest.mark.parametrize("form", ["ai", "ia"])
+def test_schur_preconditioner_vs_oracle(irk, oracle, tab_name, form):
+    n = 5
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(3, n))
+    Mo, Ko = oracle.p1_matrices(3, n)
+    tab = irk.from_spec(tab_name)
+    pc = irk.build_preconditioner(irk.PreconditionerKind.SCHUR, tab, M, K, 5e-3,
+                                  irk.Splitting(form), bd,
+                                  settings=irk.BlockSolveSettings(rtol=1e-14, maxit=2000))
+    v = np.random.default_rng(2).standard_normal(tab.s * M.nrows)
+    # dense reference: (Q (x) I) blockdiag(P_b (x) M + Q_b (x) K)^-1 (Q^T (x) I), constrained
+    At = pc.A_tilde
+    s, m = tab.s, M.nrows
+    if form == "ai":
+        S = np.kron(np.eye(s), Mo.toarray()) + 5e-3 * np.kron(At, Ko.toarray())
+    else:
+        S = np.kron(np.linalg.inv(At), Mo.toarray()) + 5e-3 * np.kron(np.eye(s), Ko.toarray())
+    idx = oracle.stage_index(s, m, bd)
+    keep = np.ones(s * m, bool)
+    keep[idx] = False
+    S[~keep, :] = 0
+    S[:, ~keep] = 0
+    S[idx, idx] = 1.0
+    assert rel(pc.apply(v), np.linalg.solve(S, v)) < 1e-9
