@@ -134,7 +134,9 @@ int irk_spmv(irk_ctx* ctx, const irk_mat* A, int k, const double* x_dev, double*
  * Ks holds nK = 1 matrix or nK = s per-stage matrices (row-indexed: stage row
  * i uses Ks[i], sparsela.py:230-234); all on M's pattern.
  * If rowmask_dev is non-NULL the constrained form is applied: flagged rows
- * are identity and flagged columns are eliminated (bcs.py:99-120).
+ * are identity (bcs.py:99-120); the column elimination is carried by the
+ * matrices, which the caller passes with flagged rows and columns zeroed
+ * (irk_mat_constrain(..., diag_value = 0)).
  * Replaces KroneckerStageOperator.apply (sparsela.py:222-235) and
  * ConstrainedStageOperator.apply (bcs.py:114-120). */
 int irk_stage_apply(irk_ctx* ctx, int s, const double* C1_host, const double* C2_host,
@@ -161,7 +163,8 @@ int irk_stage_mix(irk_ctx* ctx, int64_t m, int s_out, int s_in, const double* Q_
 /* Gauss-Seidel stage coupling of the block preconditioner
  * (StagePreconditioner.apply, precond.py:104-115):
  *   out[r*ld_out] = R[r*s + i] - sum_c C[r,c] * sum_j coef[j] X[c*s + j]
- * with flagged columns of X read as zero and flagged rows left at R. */
+ * flagged rows are left at R; C must come with flagged columns zeroed
+ * (irk_mat_constrain). */
 int irk_stage_couple(irk_ctx* ctx, int s, int i, const double* coef_host, const irk_mat* C,
                      const uint8_t* rowmask_dev, const double* R_dev, const double* X_dev,
                      double* out_dev, int64_t ld_out);
@@ -242,9 +245,10 @@ int irk_all_finite(irk_ctx* ctx, int64_t n, const double* x_dev, int* result_hos
  * Jacobi-preconditioned CG on nb independent SPD systems stored interleaved
  * (m-by-nb).  System k is
  *      B_k = alpha[k]*A + beta[k]*Bm + diag(shift[:, k])
- * (Bm and shift may be NULL) with rows flagged in rowmask_dev replaced by
- * identity rows and their columns eliminated (the treatment factorize_block
- * gives its blocks, sparsela.py:181-183).  Solves start from x = 0 and stop
+ * (Bm and shift may be NULL); rows flagged in rowmask_dev are identity rows
+ * and the caller passes A, Bm with the flagged columns eliminated
+ * (irk_mat_constrain), the treatment factorize_block gives its blocks
+ * (sparsela.py:181-183).  A pre-combined, constrained block needs no mask.  Solves start from x = 0 and stop
  * per system when ||r_k|| <= max(rtol*||b_k||, atol) or after maxit
  * iterations; all loop control stays on the device.
  * its_host[k] / relres_host[k] receive the iteration count and final

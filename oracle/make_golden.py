@@ -185,7 +185,7 @@ def trajectory(irk, k, n, steps=None, full=False):
         kw["newton"] = irk.NewtonSettings(rtol=1e-10, atol=1e-10)
     stp = irk.TimeStepper(prob, rt, cfg["dt"], **kw)
     key = f"traj{k}_n{cfg['n']}"
-    out = {f"{key}_u0": np.asarray(prob.u0)}
+    out = {} if full else {f"{key}_u0": np.asarray(prob.u0)}
     us, stages, its = [], [], []
     t0 = time.time()
     nsteps = steps if steps is not None else cfg["steps"]

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <climits>
 #include <cstdio>
 #include <string>
 
@@ -33,13 +34,25 @@ struct Pattern {
   int* sell_col = nullptr;   // sell_nnz
   int* csr2sell = nullptr;   // nnz: SELL position of CSR entry p
   int* diag_pos = nullptr;   // nrows: SELL position of (r, r) or -1
+  int maxw = 0;              // widest slice (entries per row)
+  // Slot-uniform column compression (a CSR-DU-style delta code for SELL):
+  // slot q = slice_ptr[s]/32 + k covers entry k of the 32 rows of slice s.
+  // colhdr[q] = d when every lane's column is row + d, else kNonUniform
+  // (read sell_col[pos]).
+  int* colhdr = nullptr;     // sell_nnz / 32
 };
+
+constexpr int kNonUniform = INT_MIN;
 
 }  // namespace irk
 
 struct irk_mat {
   irk::Pattern* pat = nullptr;
-  double* val = nullptr;  // SELL order, sell_nnz entries
+  double* val = nullptr;   // SELL order, sell_nnz entries
+  // Slot-uniform value compression (CSR-VI-style): uval[q] = the common
+  // value of slot q when all 32 lanes agree bit for bit, else NaN (read
+  // val[pos]).
+  double* uval = nullptr;  // sell_nnz / 32
 };
 
 struct irk_ctx {
@@ -123,6 +136,22 @@ int pattern_build_sell(irk_ctx* ctx, Pattern* p);
 int mat_alloc(irk_ctx* ctx, Pattern* p, irk_mat** out);
 // Scatter CSR-ordered device values into the SELL array of A.
 int mat_set_csr_values(irk_ctx* ctx, irk_mat* A, const double* csr_val_dev);
+// Recompute the slot-uniform value headers after A->val changed.
+int mat_finalize(irk_ctx* ctx, irk_mat* A);
+
+// Read entry k of row `row` (lane `lane` of slice `s`, slot base `q0`,
+// position base `base`) through the slot-uniform headers.
+__device__ __forceinline__ int sell_col_at(const int* __restrict__ colhdr,
+                                          const int* __restrict__ sell_col, int q, int pos,
+                                          int64_t row) {
+  int h = __ldg(colhdr + q);
+  return h != kNonUniform ? (int)(row + h) : __ldg(sell_col + pos);
+}
+__device__ __forceinline__ double sell_val_at(const double* __restrict__ uval,
+                                              const double* __restrict__ val, int q, int pos) {
+  double u = __ldg(uval + q);
+  return isnan(u) ? __ldg(val + pos) : u;
+}
 
 // warp / block reductions ----------------------------------------------------
 __device__ __forceinline__ double warp_sum(double v) {

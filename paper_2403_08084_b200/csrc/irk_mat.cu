@@ -9,6 +9,7 @@
 //   _p1_matrices / assemble_heat  problems.py:67-99
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <vector>
 
 #include "irk_internal.cuh"
@@ -26,6 +27,7 @@ void pattern_release(Pattern* p) {
     cudaFree(p->sell_col);
     cudaFree(p->csr2sell);
     cudaFree(p->diag_pos);
+    cudaFree(p->colhdr);
     delete p;
   }
 }
@@ -89,6 +91,49 @@ __global__ void k_sell_fill(int64_t nrows, int64_t ncols, const int* __restrict_
   diag_pos[r] = dpos;
 }
 
+// one warp per slice: slot-uniform column offsets
+__global__ void k_colhdr(int64_t nrows, int64_t nslices, const int* __restrict__ slice_ptr,
+                         const int* __restrict__ sell_col, int* __restrict__ colhdr) {
+  int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (s >= nslices) return;
+  int base = slice_ptr[s], width = (slice_ptr[s + 1] - base) / kSlice;
+  int64_t row = s * kSlice + lane;
+  bool full = (s + 1) * kSlice <= nrows;
+  for (int k = 0; k < width; ++k) {
+    int off = sell_col[base + k * kSlice + lane] - (int)row;
+    int off0 = __shfl_sync(0xffffffffu, off, 0);
+    bool uni = __all_sync(0xffffffffu, off == off0) && full;
+    if (lane == 0) colhdr[base / kSlice + k] = uni ? off0 : kNonUniform;
+  }
+}
+
+// one warp per slice: slot-uniform values (bitwise equality), else NaN
+__global__ void k_valhdr(int64_t nrows, int64_t nslices, const int* __restrict__ slice_ptr,
+                         const double* __restrict__ val, double* __restrict__ uval) {
+  int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (s >= nslices) return;
+  int base = slice_ptr[s], width = (slice_ptr[s + 1] - base) / kSlice;
+  bool full = (s + 1) * kSlice <= nrows;
+  for (int k = 0; k < width; ++k) {
+    unsigned long long b = __double_as_longlong(val[base + k * kSlice + lane]);
+    unsigned long long b0 = __shfl_sync(0xffffffffu, b, 0);
+    bool uni = __all_sync(0xffffffffu, b == b0) && full;
+    if (lane == 0) uval[base / kSlice + k] = uni ? __longlong_as_double(b0) : __longlong_as_double(0x7ff8dead00000000ull);
+  }
+}
+
+int mat_finalize(irk_ctx* ctx, irk_mat* A) {
+  const Pattern* p = A->pat;
+  if (p->nslices == 0) return IRK_OK;
+  int64_t threads = p->nslices * 32;
+  k_valhdr<<<(unsigned)((threads + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(
+      p->nrows, p->nslices, p->slice_ptr, A->val, A->uval);
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
 int pattern_build_sell(irk_ctx* ctx, Pattern* p) {
   p->nslices = (p->nrows + kSlice - 1) / kSlice;
   int64_t ns = p->nslices;
@@ -120,6 +165,20 @@ int pattern_build_sell(irk_ctx* ctx, Pattern* p) {
         p->diag_pos, ns);
     IRK_CHECK_LAUNCH(ctx);
   }
+  IRK_CUDA(cudaMalloc(&p->colhdr, ((size_t)total / kSlice + 1) * sizeof(int)));
+  if (ns > 0) {
+    int64_t threads = ns * 32;
+    k_colhdr<<<(unsigned)((threads + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(
+        p->nrows, ns, p->slice_ptr, p->sell_col, p->colhdr);
+    IRK_CHECK_LAUNCH(ctx);
+    std::vector<int> sp(ns + 1);
+    IRK_CUDA(cudaMemcpyAsync(sp.data(), p->slice_ptr, (ns + 1) * sizeof(int),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+    int mw = 0;
+    for (int64_t q = 0; q < ns; ++q) mw = std::max(mw, (sp[q + 1] - sp[q]) / kSlice);
+    p->maxw = mw;
+  }
   return IRK_OK;
 }
 
@@ -135,6 +194,9 @@ int mat_alloc(irk_ctx* ctx, Pattern* p, irk_mat** out) {
     return IRK_ECUDA;
   }
   IRK_CUDA(cudaMemsetAsync(A->val, 0, ((size_t)p->sell_nnz + 1) * sizeof(double), ctx->stream));
+  IRK_CUDA(cudaMalloc(&A->uval, ((size_t)p->sell_nnz / kSlice + 1) * sizeof(double)));
+  IRK_CUDA(cudaMemsetAsync(A->uval, 0, ((size_t)p->sell_nnz / kSlice + 1) * sizeof(double),
+                           ctx->stream));
   *out = A;
   return IRK_OK;
 }
@@ -159,7 +221,7 @@ int mat_set_csr_values(irk_ctx* ctx, irk_mat* A, const double* csr_val_dev) {
   k_scatter_vals<<<grid_for(ctx, nnz), kBlock, 0, ctx->stream>>>(nnz, A->pat->csr2sell,
                                                                    csr_val_dev, A->val);
   IRK_CHECK_LAUNCH(ctx);
-  return IRK_OK;
+  return mat_finalize(ctx, A);
 }
 
 // ------------------------------------------------------------ P1 assembly
@@ -479,7 +541,7 @@ __global__ void k_constrain(int64_t nrows, int64_t nslices, const int* __restric
   if (rowc) {
     if (dpos >= 0)
       val[dpos] = diag_value;
-    else
+    else if (diag_value != 0.0)
       atomicAdd(missing, 1);
   }
 }
@@ -702,6 +764,7 @@ int irk_mat_download(irk_ctx* ctx, const irk_mat* A, int64_t* row_offsets_host,
 int irk_mat_destroy(irk_mat* A) {
   if (!A) return IRK_OK;
   cudaFree(A->val);
+  cudaFree(A->uval);
   pattern_release(A->pat);
   delete A;
   return IRK_OK;
@@ -748,6 +811,8 @@ int irk_mat_union(irk_ctx* ctx, const irk_mat* A, const irk_mat* B, irk_mat** A_
     k_remap_vals<<<grid_for(ctx, pb->nnz), kBlock, 0, ctx->stream>>>(
         pb->nnz, pb->csr2sell, B->val, mapb, U->csr2sell, B2->val);
   IRK_CHECK_LAUNCH(ctx);
+  IRK_TRY(mat_finalize(ctx, A2));
+  IRK_TRY(mat_finalize(ctx, B2));
   IRK_CUDA(cudaStreamSynchronize(ctx->stream));
   cudaFree(mapa);
   cudaFree(mapb);
@@ -767,6 +832,7 @@ int irk_mat_combine(irk_ctx* ctx, double alpha, const irk_mat* A, double beta, c
     k_combine<<<grid_for(ctx, n), kBlock, 0, ctx->stream>>>(n, alpha, A->val, beta, B->val,
                                                            out->val);
   IRK_CHECK_LAUNCH(ctx);
+  IRK_TRY(mat_finalize(ctx, out));
   *C = out;
   return IRK_OK;
 }
@@ -787,6 +853,7 @@ int irk_mat_constrain(irk_ctx* ctx, const irk_mat* A, const uint8_t* mask_dev, d
         P->nrows, P->nslices, P->slice_ptr, P->sell_col, P->diag_pos, mask_dev, diag_value,
         C->val, missing);
   IRK_CHECK_LAUNCH(ctx);
+  IRK_TRY(mat_finalize(ctx, C));
   int h_missing = 0;
   IRK_CUDA(cudaMemcpyAsync(&h_missing, missing, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   IRK_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -808,6 +875,7 @@ int irk_mat_on_pattern(irk_ctx* ctx, const irk_mat* X, const irk_mat* T, irk_mat
   if (px == pt) {
     IRK_CUDA(cudaMemcpyAsync(Y->val, X->val, px->sell_nnz * sizeof(double),
                              cudaMemcpyDeviceToDevice, ctx->stream));
+    IRK_TRY(mat_finalize(ctx, Y));
     *out = Y;
     return IRK_OK;
   }
@@ -832,6 +900,7 @@ int irk_mat_on_pattern(irk_ctx* ctx, const irk_mat* X, const irk_mat* T, irk_mat
     k_remap_vals<<<grid_for(ctx, px->nnz), kBlock, 0, ctx->stream>>>(px->nnz, px->csr2sell, X->val,
                                                                      map, pt->csr2sell, Y->val);
   IRK_CHECK_LAUNCH(ctx);
+  IRK_TRY(mat_finalize(ctx, Y));
   IRK_CUDA(cudaStreamSynchronize(ctx->stream));
   cudaFree(map);
   *out = Y;
@@ -849,6 +918,7 @@ int irk_mat_semilinear_jacobian(irk_ctx* ctx, const irk_mat* M, const irk_mat* K
     k_semi_jac<<<(unsigned)((n + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(
         n, M->pat->slice_ptr, M->pat->sell_col, M->val, K->val, kscale, d_dev, ld, off, J->val);
   IRK_CHECK_LAUNCH(ctx);
+  IRK_TRY(mat_finalize(ctx, J));
   *out = J;
   return IRK_OK;
 }

@@ -23,49 +23,77 @@ struct KPtrs {
 
 // Out_r = C1 (M Y)_r + dt C2 (K Y)_r  (shared K)
 // Out_r,i = (C1 (M Y)_r)_i + dt (K_i (C2 Y))_r,i  (per-stage K_i)
-// MASK: flagged rows are identity, flagged columns read as zero.
-template <int S, bool PERSTAGE, bool MASK>
+// mask: flagged rows are identity; flagged columns must already be
+// eliminated from M and K (irk_mat_constrain with diagonal 0).
+// MAXW > 0: all column indices / values of the row are loaded first, then
+// the stage-vector gathers are issued (one dependency level per row).
+template <int S, bool PERSTAGE, int MAXW>
 __global__ void __launch_bounds__(kBlock)
     k_stage_apply(int64_t m, const int* __restrict__ slice_ptr, const int* __restrict__ sell_col,
                   const double* __restrict__ mval, KPtrs kp, const Coef2 cf, double dt,
                   const uint8_t* __restrict__ mask, const double* __restrict__ Y,
                   double* __restrict__ Out) {
-  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
-  if (MASK && mask[r]) {
+  if (mask && mask[r]) {
 #pragma unroll
     for (int i = 0; i < S; ++i) Out[r * S + i] = Y[r * S + i];
     return;
   }
-  int64_t s = r / kSlice;
-  int lane = (int)(r % kSlice);
-  int base = __ldg(slice_ptr + s), width = (__ldg(slice_ptr + s + 1) - base) / kSlice;
+  const int64_t s = r / kSlice;
+  const int lane = (int)(r % kSlice);
+  const int base = __ldg(slice_ptr + s), width = (__ldg(slice_ptr + s + 1) - base) / kSlice;
   double a[S], b[S];
 #pragma unroll
   for (int i = 0; i < S; ++i) a[i] = b[i] = 0.0;
-  for (int k = 0; k < width; ++k) {
-    int pos = base + k * kSlice + lane;
-    int c = __ldg(sell_col + pos);
-    if (MASK && __ldg(mask + c)) continue;
-    double mv = __ldg(mval + pos);
-    double y[S];
+  if (MAXW > 0 && !PERSTAGE) {
+    int cc[MAXW > 0 ? MAXW : 1];
+    double mv[MAXW > 0 ? MAXW : 1], kv[MAXW > 0 ? MAXW : 1];
 #pragma unroll
-    for (int i = 0; i < S; ++i) y[i] = __ldg(Y + (int64_t)c * S + i);
-    if (!PERSTAGE) {
-      double kv = __ldg(kp.k[0] + pos);
-#pragma unroll
-      for (int i = 0; i < S; ++i) {
-        a[i] += mv * y[i];
-        b[i] += kv * y[i];
+    for (int k = 0; k < MAXW; ++k) {
+      if (k < width) {
+        const int pos = base + k * kSlice + lane;
+        cc[k] = __ldg(sell_col + pos);
+        mv[k] = __ldg(mval + pos);
+        kv[k] = __ldg(kp.k[0] + pos);
       }
-    } else {
+    }
 #pragma unroll
-      for (int i = 0; i < S; ++i) {
-        a[i] += mv * y[i];
-        double w = 0.0;
+    for (int k = 0; k < MAXW; ++k) {
+      if (k < width) {
+        const double* yc = Y + (int64_t)cc[k] * S;
 #pragma unroll
-        for (int j = 0; j < S; ++j) w += cf.c2[i * S + j] * y[j];
-        b[i] += __ldg(kp.k[i] + pos) * w;
+        for (int i = 0; i < S; ++i) {
+          const double y = __ldg(yc + i);
+          a[i] += mv[k] * y;
+          b[i] += kv[k] * y;
+        }
+      }
+    }
+  } else {
+    for (int k = 0; k < width; ++k) {
+      const int pos = base + k * kSlice + lane;
+      const int c = __ldg(sell_col + pos);
+      const double m_ = __ldg(mval + pos);
+      double y[S];
+#pragma unroll
+      for (int i = 0; i < S; ++i) y[i] = __ldg(Y + (int64_t)c * S + i);
+      if (!PERSTAGE) {
+        const double k_ = __ldg(kp.k[0] + pos);
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+          a[i] += m_ * y[i];
+          b[i] += k_ * y[i];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+          a[i] += m_ * y[i];
+          double w = 0.0;
+#pragma unroll
+          for (int j = 0; j < S; ++j) w += cf.c2[i * S + j] * y[j];
+          b[i] += __ldg(kp.k[i] + pos) * w;
+        }
       }
     }
   }
@@ -88,7 +116,7 @@ __global__ void __launch_bounds__(kBlock)
 
 // Semilinear per-stage Jacobian K_i = kscale K + M diag(D_i):
 // Out_r,i = (C1 (M Y))_i + dt*kscale (C2 (K Y))_i + dt (M (D_i o (C2 Y)_i))_r
-template <int S, bool MASK>
+template <int S>
 __global__ void __launch_bounds__(kBlock)
     k_stage_apply_semi(int64_t m, const int* __restrict__ slice_ptr,
                        const int* __restrict__ sell_col, const double* __restrict__ mval,
@@ -97,7 +125,7 @@ __global__ void __launch_bounds__(kBlock)
                        const double* __restrict__ Y, double* __restrict__ Out) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
-  if (MASK && mask[r]) {
+  if (mask && mask[r]) {
 #pragma unroll
     for (int i = 0; i < S; ++i) Out[r * S + i] = Y[r * S + i];
     return;
@@ -111,7 +139,6 @@ __global__ void __launch_bounds__(kBlock)
   for (int k = 0; k < width; ++k) {
     int pos = base + k * kSlice + lane;
     int c = __ldg(sell_col + pos);
-    if (MASK && __ldg(mask + c)) continue;
     double mv = __ldg(mval + pos), kv = __ldg(kval + pos);
     double y[S];
 #pragma unroll
@@ -161,7 +188,7 @@ __global__ void k_stage_mix(int64_t m, int so, int si, const Mat8 Q, const doubl
 }
 
 // out[r*ld] = R[r*s+i] - sum_c C[r,c] sum_j coef[j] X[c*s+j]  (masked)
-template <int S, bool MASK>
+template <int S>
 __global__ void __launch_bounds__(kBlock)
     k_stage_couple(int64_t m, int i, const int* __restrict__ slice_ptr,
                    const int* __restrict__ sell_col, const double* __restrict__ cval,
@@ -171,7 +198,7 @@ __global__ void __launch_bounds__(kBlock)
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
   double rv = R[r * S + i];
-  if (MASK && mask[r]) {
+  if (mask && mask[r]) {
     out[r * ld_out] = rv;
     return;
   }
@@ -182,7 +209,6 @@ __global__ void __launch_bounds__(kBlock)
   for (int k = 0; k < width; ++k) {
     int pos = base + k * kSlice + lane;
     int c = __ldg(sell_col + pos);
-    if (MASK && __ldg(mask + c)) continue;
     double w = 0.0;
 #pragma unroll
     for (int j = 0; j < S; ++j) w += coef.q[j] * __ldg(X + (int64_t)c * S + j);
@@ -452,19 +478,20 @@ int irk_stage_apply(irk_ctx* ctx, int s, const double* C1_host, const double* C2
   int64_t m = P->nrows;
   if (m == 0) return IRK_OK;
   unsigned g = (unsigned)((m + kBlock - 1) / kBlock);
-  bool per = nK > 1, msk = rowmask_dev != nullptr;
-#define IRK_LAUNCH_SA(PER, MSK)                                                        \
-  IRK_STAGE_SWITCH(s, (k_stage_apply<SS, PER, MSK><<<g, kBlock, 0, ctx->stream>>>(    \
+  const bool per = nK > 1;
+  const int mw = P->maxw;
+#define IRK_LAUNCH_SA(PER, W)                                                             \
+  IRK_STAGE_SWITCH(s, (k_stage_apply<SS, PER, W><<<g, kBlock, 0, ctx->stream>>>(          \
                           m, P->slice_ptr, P->sell_col, M->val, kp, cf, dt, rowmask_dev, \
                           Y_dev, Out_dev)))
-  if (!per && !msk) {
-    IRK_LAUNCH_SA(false, false)
-  } else if (!per && msk) {
-    IRK_LAUNCH_SA(false, true)
-  } else if (per && !msk) {
-    IRK_LAUNCH_SA(true, false)
+  if (per) {
+    IRK_LAUNCH_SA(true, 0)
+  } else if (mw <= 8) {
+    IRK_LAUNCH_SA(false, 8)
+  } else if (mw <= 16) {
+    IRK_LAUNCH_SA(false, 16)
   } else {
-    IRK_LAUNCH_SA(true, true)
+    IRK_LAUNCH_SA(false, 0)
   }
 #undef IRK_LAUNCH_SA
   IRK_CHECK_LAUNCH(ctx);
@@ -488,15 +515,9 @@ int irk_stage_apply_semilinear(irk_ctx* ctx, int s, const double* C1_host, const
   int64_t m = P->nrows;
   if (m == 0) return IRK_OK;
   unsigned g = (unsigned)((m + kBlock - 1) / kBlock);
-  if (rowmask_dev) {
-    IRK_STAGE_SWITCH(s, (k_stage_apply_semi<SS, true><<<g, kBlock, 0, ctx->stream>>>(
-                            m, P->slice_ptr, P->sell_col, M->val, K->val, cf, dt, kscale, D_dev,
-                            rowmask_dev, Y_dev, Out_dev)))
-  } else {
-    IRK_STAGE_SWITCH(s, (k_stage_apply_semi<SS, false><<<g, kBlock, 0, ctx->stream>>>(
-                            m, P->slice_ptr, P->sell_col, M->val, K->val, cf, dt, kscale, D_dev,
-                            nullptr, Y_dev, Out_dev)))
-  }
+  IRK_STAGE_SWITCH(s, (k_stage_apply_semi<SS><<<g, kBlock, 0, ctx->stream>>>(
+                          m, P->slice_ptr, P->sell_col, M->val, K->val, cf, dt, kscale, D_dev,
+                          rowmask_dev, Y_dev, Out_dev)))
   IRK_CHECK_LAUNCH(ctx);
   return IRK_OK;
 }
@@ -529,15 +550,9 @@ int irk_stage_couple(irk_ctx* ctx, int s, int i, const double* coef_host, const 
   for (int j = 0; j < s; ++j) cf.q[j] = coef_host[j];
   const Pattern* P = C->pat;
   unsigned g = (unsigned)((m + kBlock - 1) / kBlock);
-  if (rowmask_dev) {
-    IRK_STAGE_SWITCH(s, (k_stage_couple<SS, true><<<g, kBlock, 0, ctx->stream>>>(
-                            m, i, P->slice_ptr, P->sell_col, C->val, cf, rowmask_dev, R_dev,
-                            X_dev, out_dev, ld_out)))
-  } else {
-    IRK_STAGE_SWITCH(s, (k_stage_couple<SS, false><<<g, kBlock, 0, ctx->stream>>>(
-                            m, i, P->slice_ptr, P->sell_col, C->val, cf, nullptr, R_dev, X_dev,
-                            out_dev, ld_out)))
-  }
+  IRK_STAGE_SWITCH(s, (k_stage_couple<SS><<<g, kBlock, 0, ctx->stream>>>(
+                          m, i, P->slice_ptr, P->sell_col, C->val, cf, rowmask_dev, R_dev, X_dev,
+                          out_dev, ld_out)))
   IRK_CHECK_LAUNCH(ctx);
   return IRK_OK;
 }

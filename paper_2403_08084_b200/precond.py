@@ -172,7 +172,8 @@ class StagePreconditioner:
         s, m = self.s, self.m
         if kind is PreconditionerKind.SCHUR:
             return self._apply_schur(R, X)
-        mats = self._device_mats()
+        mk = self.mask()
+        mats = [d.eliminated(mk) for d in self._device_mats()]
         Md, Ks = mats[0], mats[1:]
         if kind is PreconditionerKind.BLOCK_DIAGONAL and len(Ks) == 1:
             a, b = self._block_coefs()
@@ -247,7 +248,7 @@ class StagePreconditioner:
 
     def _apply_schur(self, R, X):
         plan = self._schur_plan()
-        mats = self._device_mats()
+        mats = [d.eliminated(self.mask()) for d in self._device_mats()]
         if len(mats) != 2:
             raise ValueError("the Schur preconditioner needs one shared stiffness matrix")
         Md, Kd = mats

@@ -112,10 +112,11 @@ def _like_input(dev_result, like):
 class DeviceMatrix:
     """Owner of one libirk irk_mat (CSR + SELL-32, float64 values)."""
 
-    __slots__ = ("handle", "nrows", "ncols", "nnz", "__weakref__")
+    __slots__ = ("handle", "nrows", "ncols", "nnz", "_ccache", "__weakref__")
 
     def __init__(self, handle: C.c_void_p):
         self.handle = handle
+        self._ccache = {}
         r, c, z = C.c_int64(), C.c_int64(), C.c_int64()
         call("irk_mat_info", handle, C.byref(r), C.byref(c), C.byref(z))
         self.nrows, self.ncols, self.nnz = r.value, c.value, z.value
@@ -162,6 +163,18 @@ class DeviceMatrix:
         h = C.c_void_p()
         call("irk_mat_constrain", ctx(), self.handle, ptr(mask), float(diag_value), C.byref(h))
         return DeviceMatrix(h)
+
+    def eliminated(self, mask) -> "DeviceMatrix":
+        """Copy with the flagged rows and columns zeroed (cached per mask):
+        the form every masked kernel expects (flagged rows are identity rows
+        in the kernels themselves)."""
+        if mask is None:
+            return self
+        key = (mask.data_ptr(), mask.numel())
+        hit = self._ccache.get(key)
+        if hit is None or hit[0] is not mask:
+            hit = self._ccache[key] = (mask, self.constrain(mask, 0.0))
+        return hit[1]
 
     def diagonal(self):
         out = dev_empty(self.nrows)
@@ -628,7 +641,7 @@ class KroneckerStageOperator:
         return self._mats
 
     def dev_apply(self, Y, Out, mask=None):
-        mats = self._device_mats()
+        mats = [d.eliminated(mask) for d in self._device_mats()]
         Md, Ks = mats[0], mats[1:]
         arr = (C.c_void_p * len(Ks))(*[k.handle.value for k in Ks])
         call("irk_stage_apply", ctx(), self.s, hptr(self.C1), hptr(self.C2), self.dt, Md.handle,

@@ -661,6 +661,7 @@ class _SemilinearJacobianOp(la._DevOp):
     def __init__(self, C1, C2, dt, Md, Kd, kscale, D, mask, m, s):
         self.C1 = np.ascontiguousarray(C1, dtype=np.float64)
         self.C2 = np.ascontiguousarray(C2, dtype=np.float64)
+        Md, Kd = Md.eliminated(mask), Kd.eliminated(mask)
         self.dt, self.Md, self.Kd, self.kscale, self.D, self.mask = dt, Md, Kd, kscale, D, mask
         self.n = m * s
         self.s = s
@@ -761,6 +762,7 @@ def _step_newton_semilinear(stepper, problem):
     wb = np.ascontiguousarray(dt * np.asarray(tab.b))
     call("irk_stage_update", ctx(), m, s, 1.0, ptr(stepper._u_dev), hptr(wb), -1, ptr(x),
          ptr(u_next))
+    stepper._last_stages_dev = x.clone()
     report = StepReport(len(hist) - 1, krylov_total, hist[-1], hist, inner)
     stepper._commit(u_next)
     return u_next, report
@@ -775,7 +777,8 @@ class _SurrogateBlockJacobi:
         self.s, self.m = tab.s, problem.m
         self.alpha = [1.0] * tab.s
         self.beta = [dt * float(tab.A[i, i]) * kscale for i in range(tab.s)]
-        self.shift, self.Md, self.Kd, self.mask = shift, Md, Kd, mask
+        self.shift, self.mask = shift, mask
+        self.Md, self.Kd = Md.eliminated(mask), Kd.eliminated(mask)
         self.settings = settings
         self.inner_iterations = []
 
@@ -904,6 +907,7 @@ def _step_newton_generic(stepper, problem):
         u_next = la.dev_empty(m)
         wb = np.ascontiguousarray(dt * np.asarray(tab.b))
         call("irk_stage_update", ctx(), m, s, 1.0, ptr(u), hptr(wb), -1, ptr(Kv), ptr(u_next))
+    stepper._last_stages_dev = x.clone()
     report = StepReport(len(hist) - 1, krylov_total, hist[-1], hist)
     stepper._commit(u_next)
     return u_next, report

@@ -219,7 +219,8 @@ def test_batched_pcg_vs_oracle(irk, oracle, dim, n):
     its = np.zeros(8, dtype=np.int32)
     relres = np.zeros(8)
     st = _lib.load().irk_pcg(_lib.ctx(), nb, _lib.hptr(np.array(alphas)), _lib.hptr(np.array(betas)),
-                             M.device().handle, K.device().handle, _lib.ptr(None), _lib.ptr(mask),
+                             M.device().eliminated(mask).handle, K.device().eliminated(mask).handle,
+                             _lib.ptr(None), _lib.ptr(mask),
                              _lib.ptr(rhs), nb, _lib.ptr(x), nb, 1e-12, 0.0, 5000, _lib.hptr(its),
                              _lib.hptr(relres))
     assert st == 0
@@ -251,8 +252,9 @@ def test_cocg_complex_symmetric(irk, oracle):
     rr = np.zeros(8)
     arr = lambda f: _lib.hptr(np.array([f(c) for c in coefs] + [0.0] * 6))  # noqa: E731
     st = _lib.load().irk_cocg(_lib.ctx(), 2, arr(lambda c: c[0].real), arr(lambda c: c[0].imag),
-                              arr(lambda c: c[1].real), arr(lambda c: c[1].imag), M.device().handle,
-                              K.device().handle, _lib.ptr(mask), _lib.ptr(rhs), 4, _lib.ptr(x), 4,
+                              arr(lambda c: c[1].real), arr(lambda c: c[1].imag),
+                              M.device().eliminated(mask).handle, K.device().eliminated(mask).handle,
+                              _lib.ptr(mask), _lib.ptr(rhs), 4, _lib.ptr(x), 4,
                               1e-12, 0.0, 5000, _lib.hptr(its), _lib.hptr(rr))
     assert st == 0
     X = x.cpu().numpy().reshape(m, 4)

@@ -1,0 +1,75 @@
+"""Full-size BASELINE.json configs on the GPU vs the CPU goldens (gpu).
+
+tests/golden/full_config{k}.npz hold size-independent fingerprints of every
+step's state (and stage vector) from the reference itself (configs 1, 2, 4:
+unmodified implicitrk, exact SuperLU blocks) or from the oracle restatement
+(configs 3, 5, where the reference is infeasible at full size).  A
+fingerprint carries 32 Gaussian projections and a strided sample; the
+relative L2 error of a difference is read off both.  Bar: 1e-9 (north_star).
+"""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def fingerprint(v, P):
+    return P @ v, v[:: max(1, len(v) // 4096)]
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_full_config_parity(cuda, oracle, k):
+    path = GOLD / f"full_config{k}.npz"
+    if not path.exists():
+        pytest.fail(f"missing golden {path.name}")
+    from paper_2403_08084_b200 import configs
+
+    g = np.load(path)
+    wl = configs.build(k)
+    st, prob = wl.stepper, wl.problem
+    key = f"traj{k}_n{configs.GRID[k][1]}"
+    P = oracle.sketch_rows(prob.m)
+    Ps = oracle.sketch_rows(prob.m * st.tableau.s, seed=77) if f"{key}_x0_proj" in g.files else None
+    worst_u = worst_x = 0.0
+    for i in range(wl.steps):
+        st.step_device(prob)
+        u = st.u
+        proj, samp = fingerprint(u, P)
+        eu = max(np.linalg.norm(proj - g[f"{key}_u{i}_proj"]) / np.linalg.norm(g[f"{key}_u{i}_proj"]),
+                 np.linalg.norm(samp - g[f"{key}_u{i}_sample"]) / np.linalg.norm(g[f"{key}_u{i}_sample"]))
+        worst_u = max(worst_u, eu)
+        if Ps is not None and f"{key}_x{i}_proj" in g.files:
+            x = st._last_stages
+            px = Ps @ x
+            worst_x = max(worst_x, np.linalg.norm(px - g[f"{key}_x{i}_proj"])
+                          / np.linalg.norm(g[f"{key}_x{i}_proj"]))
+    print(f"config {k}: worst state rel L2 {worst_u:.3e}, worst stage-vector rel L2 {worst_x:.3e}")
+    assert worst_u < 1e-9
+    assert worst_x < 1e-9
+
+
+def test_full_size_properties(cuda):
+    """Size-independent invariants at config-2 scale: the heat semigroup is
+    M-norm contractive and the Dirichlet values stay exactly zero."""
+    from paper_2403_08084_b200 import configs, spmv
+
+    wl = configs.build(2)
+    st, prob = wl.stepper, wl.problem
+    bd = prob.dirichlet.dofs
+
+    def mnorm(u):
+        return float(np.sqrt(u @ spmv(prob.mass, u)))
+
+    prev = mnorm(st.u)
+    for _ in range(3):
+        st.step_device(prob)
+        u = st.u
+        assert np.all(u[bd] == 0.0)
+        cur = mnorm(u)
+        assert cur <= prev * (1 + 1e-12)
+        prev = cur
