@@ -102,6 +102,7 @@ struct SysState {
   int code[kMaxSys];  // 0 running/converged, 1 maxit, 2 breakdown
   int done;
   int iter;
+  long long trace[16];  // persistent-kernel phase timestamps (diagnostics)
 };
 
 struct MatView {
@@ -128,17 +129,46 @@ __device__ __forceinline__ bool last_block_inner(unsigned int* counter) {
   return is_last;
 }
 
-// Deterministic reduction of per-block partials part[k*G + b] -> out[k].
-template <typename T>
-__device__ __forceinline__ void reduce_partials(const T* part, int nb, int G, T* out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int k = warp; k < nb; k += kBlock / 32) {
-    T s = s_zero(T{});
-    for (int b = lane; b < G; b += 32) s = s_add(s, part[(int64_t)k * G + b]);
-    s = s_wsum(s);
-    if (lane == 0) out[k] = s;
-  }
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ cplx ld_cg(const cplx* p) {
+  const double2 v = __ldcg(reinterpret_cast<const double2*>(p));
+  return {v.x, v.y};
 }
+
+// Deterministic reduction of per-block partials part[k*G + b] -> out[k]
+// by the whole (last) block: every thread loads its <= 4 partials per
+// system at once (one L2 round trip), then a fixed-order block reduction.
+// Must be called by all threads of the block (G <= 4 * kBlock).
+template <typename T, int NB>
+__device__ __forceinline__ void reduce_partials(const T* part, int G, T* out) {
+  __shared__ T pred[kBlock / 32][NB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T v[NB];
+#pragma unroll
+  for (int k = 0; k < NB; ++k) v[k] = s_zero(T{});
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int b = threadIdx.x + c * kBlock;
+    if (b < G) {
+#pragma unroll
+      for (int k = 0; k < NB; ++k) v[k] = s_add(v[k], ld_cg(part + (int64_t)k * G + b));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NB; ++k) v[k] = s_wsum(v[k]);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NB; ++k) pred[warp][k] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < NB) {
+    T t = s_zero(T{});
+    for (int w = 0; w < kBlock / 32; ++w) t = s_add(t, pred[w][threadIdx.x]);
+    out[threadIdx.x] = t;
+  }
+  __syncthreads();
+}
+
 
 template <typename T, int NB>
 __device__ __forceinline__ void block_reduce_store(T (&v)[NB], T* part) {
@@ -228,8 +258,8 @@ __global__ void __launch_bounds__(kBlock)
   if (last_block_inner(counter)) {
     __shared__ T srho[NB];
     __shared__ double sbb[NB];
-    reduce_partials<T>(pr, NB, G, srho);
-    reduce_partials<double>(pb, NB, G, sbb);
+    reduce_partials<T, NB>(pr, G, srho);
+    reduce_partials<double, NB>(pb, G, sbb);
     __syncthreads();
     if (threadIdx.x == 0) {
       int any = 0;
@@ -352,7 +382,7 @@ __global__ void __launch_bounds__(kBlock, 4)
   block_reduce_store<T, NB>(mu, pp);
   if (last_block_inner(counter)) {
     __shared__ T smu[NB];
-    reduce_partials<T>(pp, NB, G, smu);
+    reduce_partials<T, NB>(pp, G, smu);
     __syncthreads();
     if (threadIdx.x == 0) {
       for (int k = 0; k < NB; ++k) {
@@ -418,8 +448,8 @@ __global__ void __launch_bounds__(kBlock)
   if (last_block_inner(counter)) {
     __shared__ T srho[NB];
     __shared__ double srr[NB];
-    reduce_partials<T>(pr, NB, G, srho);
-    reduce_partials<double>(pb, NB, G, srr);
+    reduce_partials<T, NB>(pr, G, srho);
+    reduce_partials<double, NB>(pb, G, srr);
     __syncthreads();
     if (threadIdx.x == 0) {
       int any = 0;

@@ -8,6 +8,7 @@
 #include <climits>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/irk.h"
 
@@ -40,6 +41,9 @@ struct Pattern {
   // colhdr[q] = d when every lane's column is row + d, else kNonUniform
   // (read sell_col[pos]).
   int* colhdr = nullptr;     // sell_nnz / 32
+  // host copies of each slice's smallest / largest column (halo extents of
+  // the persistent solver's row partitions)
+  std::vector<int> h_cmin, h_cmax;
 };
 
 constexpr int kNonUniform = INT_MIN;

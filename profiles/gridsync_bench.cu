@@ -47,6 +47,45 @@ __global__ void k_atomic(int iters, double* sink) {
   if (threadIdx.x == 0 && blockIdx.x == 0) *sink = acc;
 }
 
+__device__ __forceinline__ double wsum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// the persistent PCG's reduction pattern: block reduce -> partial -> grid
+// barrier -> every block sums all partials in order
+template <int MODE>
+__global__ void k_reduce(int iters, double* part, double* sink) {
+  cg::grid_group g = cg::this_grid();
+  __shared__ double wred[32];
+  __shared__ double bc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x;
+  double acc = 0.0, v = threadIdx.x * 1e-3;
+  for (int i = 0; i < iters; ++i) {
+    double a = wsum(v);
+    if (lane == 0) wred[warp] = a;
+    __syncthreads();
+    if (warp == 0) {
+      double t = lane < (int)(blockDim.x / 32) ? wred[lane] : 0.0;
+      t = wsum(t);
+      if (lane == 0) part[(i & 1) * G + blockIdx.x] = t;
+    }
+    g.sync();
+    if (MODE == 0) {
+      if (warp == 0) {
+        double t = 0.0;
+        for (int q = lane; q < G; q += 32) t += __ldcg(part + (i & 1) * G + q);
+        t = wsum(t);
+        if (lane == 0) bc = t;
+      }
+      __syncthreads();
+      acc += bc;
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) *sink = acc;
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -75,6 +114,22 @@ int main() {
     cudaEventElapsedTime(&ms, a, b);
     printf("atomic bar blocks=%d threads=%d: %.3f us/sync (%s)\n", sms, threads, ms * 1e3 / iters,
            cudaGetErrorString(cudaGetLastError()));
+  }
+  double* part;
+  cudaMalloc(&part, 4096 * sizeof(double));
+  for (int mode = 0; mode < 2; ++mode) {
+    int iters = 2000;
+    void* args[] = {&iters, &part, &sink};
+    void* fn = mode == 0 ? (void*)k_reduce<0> : (void*)k_reduce<1>;
+    cudaLaunchCooperativeKernel(fn, sms, 1024, args, 0, 0);
+    cudaEventRecord(a);
+    cudaLaunchCooperativeKernel(fn, sms, 1024, args, 0, 0);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("reduce pattern mode %d (1 = no partial read): %.3f us/iter (%s)\n", mode,
+           ms * 1e3 / iters, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }

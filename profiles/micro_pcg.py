@@ -38,6 +38,7 @@ def main():
             os.environ["IRK_NO_PERSIST"] = "1"
         else:
             os.environ.pop("IRK_NO_PERSIST", None)
+            os.environ["IRK_PERSIST"] = "1"
         fac.dev_solve(b, x, settings=fixed)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
