@@ -36,6 +36,7 @@ struct Pattern {
   int* csr2sell = nullptr;   // nnz: SELL position of CSR entry p
   int* diag_pos = nullptr;   // nrows: SELL position of (r, r) or -1
   int maxw = 0;              // widest slice (entries per row)
+  int ellw = 0;              // > 0: every slice padded to this width (ELL-32)
   // Slot-uniform column compression (a CSR-DU-style delta code for SELL):
   // slot q = slice_ptr[s]/32 + k covers entry k of the 32 rows of slice s.
   // colhdr[q] = d when every lane's column is row + d, else kNonUniform
@@ -44,6 +45,8 @@ struct Pattern {
   // host copies of each slice's smallest / largest column (halo extents of
   // the persistent solver's row partitions)
   std::vector<int> h_cmin, h_cmax;
+  // max over slot-uniform slices of the window rows (win_layout); 0 if none
+  int win_rows = 0;
 };
 
 constexpr int kNonUniform = INT_MIN;
@@ -155,6 +158,48 @@ __device__ __forceinline__ double sell_val_at(const double* __restrict__ uval,
                                               const double* __restrict__ val, int q, int pos) {
   double u = __ldg(uval + q);
   return isnan(u) ? __ldg(val + pos) : u;
+}
+
+// Window layout of a slot-uniform slice (all lanes of the warp call this;
+// lane k < width holds the slot offset d_k = colhdr[q0 + k]).  Offsets are
+// grouped into windows of stage-block rows: a new window starts at slot 0,
+// at a decreasing offset (ELL padding) or after a gap of more than kWinGap
+// rows; window w covers rows [r0 + dfirst_w, r0 + d_last_w + 32).  Returns
+// the total number of window rows; per lane: `row` = buffer row of slot
+// `lane` for lane 0 of the slice, and on window-end lanes (bit set in
+// `ends`) `rows`, `dfirst` and `wbase` (buffer row of the window start).
+constexpr int kWinGap = 8;
+struct WinLayout {
+  int total, row, rows, dfirst, wbase;
+  unsigned ends;
+};
+__device__ __forceinline__ WinLayout win_layout(int d, int width) {
+  const int lane = threadIdx.x & 31;
+  const int dprev = __shfl_up_sync(0xffffffffu, d, 1);
+  const bool start = lane < width && (lane == 0 || d < dprev || d - dprev > kWinGap);
+  const unsigned sb = __ballot_sync(0xffffffffu, start);
+  const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+  const int first_lane = 31 - __clz(sb & upto);
+  const int dfirst = __shfl_sync(0xffffffffu, d, first_lane & 31);
+  const bool next_start = lane < 31 && ((sb >> (lane + 1)) & 1u);
+  const bool is_end = lane < width && (lane == width - 1 || next_start);
+  const int rows = is_end ? d - dfirst + 32 : 0;
+  int incl = rows;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  WinLayout L;
+  L.total = __shfl_sync(0xffffffffu, incl, 31);
+  L.ends = __ballot_sync(0xffffffffu, is_end);
+  const unsigned from = lane == 0 ? 0xffffffffu : ~((1u << lane) - 1u);
+  const int end_lane = __ffs(L.ends & from) - 1;
+  L.wbase = incl - rows;
+  L.row = __shfl_sync(0xffffffffu, L.wbase, end_lane & 31) + (d - dfirst);
+  L.rows = rows;
+  L.dfirst = dfirst;
+  return L;
 }
 
 // warp / block reductions ----------------------------------------------------

@@ -60,10 +60,17 @@ __global__ void k_slice_sizes(int64_t nrows, int64_t nslices, const int* __restr
   if (gw == nslices - 1 && lane == 0) sizes[nslices] = 0;
 }
 
+// Rows whose columns all lie on the stencil r + stencil[k] (k < W == slice
+// width) are stored stencil-aligned: entry with offset stencil[k] in slot k,
+// absent neighbours as explicit zeros at column r + stencil[k] (or r when
+// that is outside the matrix).  On structured grids this makes the slots of
+// boundary-touching slices slot-uniform too.  Other rows are packed in CSR
+// order and padded with column r.
 __global__ void k_sell_fill(int64_t nrows, int64_t ncols, const int* __restrict__ rowptr,
                             const int* __restrict__ col, const int* __restrict__ slice_ptr,
                             int* __restrict__ sell_col, int* __restrict__ csr2sell,
-                            int* __restrict__ diag_pos, int64_t nslices) {
+                            int* __restrict__ diag_pos, int64_t nslices,
+                            const int* __restrict__ stencil, int W) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t s = r / kSlice;
   if (s >= nslices) return;
@@ -77,15 +84,41 @@ __global__ void k_sell_fill(int64_t nrows, int64_t ncols, const int* __restrict_
   }
   int p0 = rowptr[r], len = rowptr[r + 1] - p0;
   int dpos = -1;
-  for (int k = 0; k < width; ++k) {
-    int pos = base + k * kSlice + lane;
-    if (k < len) {
-      int c = col[p0 + k];
-      sell_col[pos] = c;
-      csr2sell[p0 + k] = pos;
+  bool aligned = stencil != nullptr && W == width && len <= W;
+  if (aligned) {
+    unsigned used = 0;  // W <= 32
+    for (int j = 0; j < len && aligned; ++j) {
+      const int64_t d = (int64_t)col[p0 + j] - r;
+      int k = 0;
+      while (k < W && stencil[k] != d) ++k;
+      if (k == W || ((used >> k) & 1u)) aligned = false;
+      else used |= 1u << k;
+    }
+  }
+  if (aligned) {
+    for (int k = 0; k < W; ++k) {
+      const int64_t c = r + stencil[k];
+      sell_col[base + k * kSlice + lane] = (c >= 0 && c < ncols) ? (int)c : pad;
+    }
+    for (int j = 0; j < len; ++j) {
+      const int c = col[p0 + j];
+      int k = 0;
+      while (stencil[k] != (int64_t)c - r) ++k;
+      const int pos = base + k * kSlice + lane;
+      csr2sell[p0 + j] = pos;
       if (c == r) dpos = pos;
-    } else {
-      sell_col[pos] = pad;
+    }
+  } else {
+    for (int k = 0; k < width; ++k) {
+      int pos = base + k * kSlice + lane;
+      if (k < len) {
+        int c = col[p0 + k];
+        sell_col[pos] = c;
+        csr2sell[p0 + k] = pos;
+        if (c == r) dpos = pos;
+      } else {
+        sell_col[pos] = pad;
+      }
     }
   }
   diag_pos[r] = dpos;
@@ -122,6 +155,20 @@ __global__ void k_colhdr(int64_t nrows, int64_t nslices, const int* __restrict__
     cmin[s] = lo;
     cmax[s] = hi;
   }
+}
+
+// one warp per slice: window rows of slot-uniform slices (max via atomicMax)
+__global__ void k_win_rows(int64_t nslices, const int* __restrict__ slice_ptr,
+                           const int* __restrict__ colhdr, int* __restrict__ out) {
+  int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (s >= nslices) return;
+  int base = slice_ptr[s], width = (slice_ptr[s + 1] - base) / kSlice;
+  if (width > 32) return;
+  const int d = lane < width ? colhdr[base / kSlice + lane] : 0;
+  if (!__all_sync(0xffffffffu, lane >= width || d != kNonUniform)) return;
+  const WinLayout L = win_layout(d, width);
+  if (lane == 0) atomicMax(out, L.total);
 }
 
 // one warp per slice: slot-uniform values (bitwise equality), else NaN
@@ -161,6 +208,29 @@ int pattern_build_sell(irk_ctx* ctx, Pattern* p) {
     k_slice_sizes<<<(unsigned)((threads + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(
         p->nrows, ns, p->rowptr, sizes);
     IRK_CHECK_LAUNCH(ctx);
+    // Pad every slice to the widest one (ELL-32) when that costs <= 5%: the
+    // slice offsets become arithmetic (32 * W * s), so kernels need no
+    // dependent slice_ptr load before their first matrix load.
+    {
+      std::vector<int> hs(ns);
+      IRK_CUDA(cudaMemcpyAsync(hs.data(), sizes, ns * sizeof(int), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+      IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+      int64_t tot = 0;
+      int wmax = 0;
+      for (int64_t q = 0; q < ns; ++q) {
+        tot += hs[q];
+        wmax = std::max(wmax, hs[q] / kSlice);
+      }
+      const int64_t padded = ns * (int64_t)kSlice * wmax;
+      p->ellw = 0;
+      if (wmax > 0 && padded <= tot + tot / 20 && padded < (int64_t)INT32_MAX / 2) {
+        for (int64_t q = 0; q < ns; ++q) hs[q] = wmax * kSlice;
+        IRK_CUDA(cudaMemcpyAsync(sizes, hs.data(), ns * sizeof(int), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        p->ellw = wmax;
+      }
+    }
     IRK_TRY(scan_exclusive(ctx, sizes, p->slice_ptr, ns + 1));
   } else {
     IRK_CUDA(cudaMemsetAsync(p->slice_ptr, 0, sizeof(int), ctx->stream));
@@ -175,20 +245,57 @@ int pattern_build_sell(irk_ctx* ctx, Pattern* p) {
   IRK_CUDA(cudaMalloc(&p->csr2sell, ((size_t)p->nnz + 1) * sizeof(int)));
   IRK_CUDA(cudaMalloc(&p->diag_pos, ((size_t)p->nrows + 1) * sizeof(int)));
   if (ns > 0) {
+    // stencil of ELL patterns: the offsets of a full-width row near the
+    // middle of the matrix (an interior node on structured grids)
+    int* d_stencil = nullptr;
+    int W = 0;
+    if (p->ellw > 0 && p->ellw <= 32) {
+      const int64_t lo = p->nrows / 2, cnt = std::min<int64_t>(p->nrows - lo, 4096);
+      std::vector<int> rp(cnt + 1);
+      IRK_CUDA(cudaMemcpyAsync(rp.data(), p->rowptr + lo, (cnt + 1) * sizeof(int),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+      IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (int64_t q = 0; q < cnt; ++q) {
+        if (rp[q + 1] - rp[q] != p->ellw) continue;
+        std::vector<int> c(p->ellw);
+        IRK_CUDA(cudaMemcpyAsync(c.data(), p->col + rp[q], p->ellw * sizeof(int),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+        IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::vector<int> st(p->ellw);
+        for (int k = 0; k < p->ellw; ++k) st[k] = c[k] - (int)(lo + q);
+        std::sort(st.begin(), st.end());
+        if (std::adjacent_find(st.begin(), st.end()) != st.end()) break;
+        IRK_CUDA(cudaMalloc(&d_stencil, p->ellw * sizeof(int)));
+        IRK_CUDA(cudaMemcpyAsync(d_stencil, st.data(), p->ellw * sizeof(int),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+        W = p->ellw;
+        break;
+      }
+    }
     int64_t threads = ns * kSlice;
     k_sell_fill<<<(unsigned)((threads + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(
         p->nrows, p->ncols, p->rowptr, p->col, p->slice_ptr, p->sell_col, p->csr2sell,
-        p->diag_pos, ns);
+        p->diag_pos, ns, d_stencil, W);
     IRK_CHECK_LAUNCH(ctx);
+    if (d_stencil) {
+      IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+      cudaFree(d_stencil);
+    }
   }
   IRK_CUDA(cudaMalloc(&p->colhdr, ((size_t)total / kSlice + 1) * sizeof(int)));
   if (ns > 0) {
     int64_t threads = ns * 32;
     int* cm = nullptr;
-    IRK_CUDA(cudaMalloc(&cm, 2 * ns * sizeof(int)));
+    IRK_CUDA(cudaMalloc(&cm, (2 * ns + 1) * sizeof(int)));
     k_colhdr<<<(unsigned)((threads + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(
         p->nrows, ns, p->slice_ptr, p->sell_col, p->colhdr, cm, cm + ns);
     IRK_CHECK_LAUNCH(ctx);
+    IRK_CUDA(cudaMemsetAsync(cm + 2 * ns, 0, sizeof(int), ctx->stream));
+    k_win_rows<<<(unsigned)((threads + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(
+        ns, p->slice_ptr, p->colhdr, cm + 2 * ns);
+    IRK_CHECK_LAUNCH(ctx);
+    IRK_CUDA(cudaMemcpyAsync(&p->win_rows, cm + 2 * ns, sizeof(int), cudaMemcpyDeviceToHost,
+                             ctx->stream));
     p->h_cmin.resize(ns);
     p->h_cmax.resize(ns);
     IRK_CUDA(cudaMemcpyAsync(p->h_cmin.data(), cm, ns * sizeof(int), cudaMemcpyDeviceToHost,

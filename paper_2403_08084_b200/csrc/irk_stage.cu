@@ -8,6 +8,8 @@
 //   _stage_value_system            stepper.py:305-313
 //   step_linear update             stepper.py:352-361
 //   step_newton residual/stages    stepper.py:502-524
+#include <cstdlib>
+
 #include "irk_internal.cuh"
 
 namespace irk {
@@ -32,17 +34,23 @@ __global__ void __launch_bounds__(kBlock)
     k_stage_apply(int64_t m, const int* __restrict__ slice_ptr, const int* __restrict__ sell_col,
                   const double* __restrict__ mval, KPtrs kp, const Coef2 cf, double dt,
                   const uint8_t* __restrict__ mask, const double* __restrict__ Y,
-                  double* __restrict__ Out) {
+                  double* __restrict__ Out, int ellw) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
-  if (mask && mask[r]) {
-#pragma unroll
-    for (int i = 0; i < S; ++i) Out[r * S + i] = Y[r * S + i];
-    return;
-  }
+  // no early exit on flagged rows: the row result is computed (the matrices
+  // carry zero rows there) and replaced at the end, so every load issues
+  // without waiting for the mask
+  const bool flagged = mask && mask[r];
   const int64_t s = r / kSlice;
   const int lane = (int)(r % kSlice);
-  const int base = __ldg(slice_ptr + s), width = (__ldg(slice_ptr + s + 1) - base) / kSlice;
+  int base, width;
+  if (ellw) {
+    base = (int)(s * kSlice * ellw);
+    width = ellw;
+  } else {
+    base = __ldg(slice_ptr + s);
+    width = (__ldg(slice_ptr + s + 1) - base) / kSlice;
+  }
   double a[S], b[S];
 #pragma unroll
   for (int i = 0; i < S; ++i) a[i] = b[i] = 0.0;
@@ -110,7 +118,145 @@ __global__ void __launch_bounds__(kBlock)
     } else {
       o += dt * b[i];
     }
-    Out[r * S + i] = o;
+    Out[r * S + i] = flagged ? Y[r * S + i] : o;
+  }
+}
+
+// Windowed variant of K2 (shared K), one warp per SELL slice.  When every
+// slot of the slice has a uniform column offset (slot-uniform header), the
+// stage-block rows the slice touches form a few contiguous windows
+// (offsets closer than kWinGap rows are merged: on the 2D P1 grid the 7
+// offsets give 3 windows of ~34 rows; a decreasing offset, e.g. an ELL
+// padding slot, starts a new window so offsets never decrease inside one).  The warp copies those windows with
+// fully coalesced loads into its shared-memory buffer and every entry's
+// stage values are then read from shared memory; the matrix values are
+// still streamed per entry (16 B/nnz, the column index is implied by the
+// header).  Other slices use the per-entry gather path.
+
+constexpr int kWinBatch = 4;  // buffer rows per lane with loads in flight
+
+template <int S, int MAXW>
+__global__ void __launch_bounds__(kBlock, MAXW <= 10 ? 3 : 2)
+    k_stage_apply_win(int64_t m, int64_t nslices, const int* __restrict__ slice_ptr,
+                      const int* __restrict__ sell_col, const int* __restrict__ colhdr,
+                      const double* __restrict__ mval, const double* __restrict__ kval,
+                      const Coef2 cf, double dt, const uint8_t* __restrict__ mask,
+                      const double* __restrict__ Y, double* __restrict__ Out, int ellw,
+                      int wrows) {
+  extern __shared__ double wsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t sl = (int64_t)blockIdx.x * (kBlock / 32) + warp;
+  if (sl >= nslices) return;
+  constexpr int SP = (S % 2 == 0) ? S + 1 : S;  // odd row stride: no bank conflicts
+  double* buf = wsm + (size_t)warp * wrows * SP;
+  const int64_t r0 = sl * kSlice, r = r0 + lane;
+  int base, width;
+  if (ellw) {
+    base = (int)(sl * kSlice * ellw);
+    width = ellw;
+  } else {
+    base = __ldg(slice_ptr + sl);
+    width = (__ldg(slice_ptr + sl + 1) - base) / kSlice;
+  }
+  const int q0 = base / kSlice;
+  const bool flagged = r < m && mask && mask[r];
+  // matrix values of the row (coalesced across the warp), issued first
+  double mv[MAXW], kv[MAXW];
+#pragma unroll
+  for (int k = 0; k < MAXW; ++k) {
+    if (k < width) {
+      mv[k] = __ldg(mval + base + k * kSlice + lane);
+      kv[k] = __ldg(kval + base + k * kSlice + lane);
+    }
+  }
+  // slot offsets: lane k < width holds d_k
+  const int d = lane < width ? __ldg(colhdr + q0 + lane) : 0;
+  bool uni = __all_sync(0xffffffffu, lane >= width || d != kNonUniform);
+  double a[S], b[S];
+#pragma unroll
+  for (int i = 0; i < S; ++i) a[i] = b[i] = 0.0;
+  if (uni) {
+    const WinLayout L = win_layout(d, width);
+    if (L.total <= wrows) {
+      // copy the windows into the buffer: lane l moves buffer rows l, l+32,
+      // ... (S doubles each), kWinBatch rows per batch with all loads issued
+      // before the stores; global row = buffer row + r0 + dfirst_w - wbase_w
+      const int rshift = (int)r0 + L.dfirst - L.wbase;  // valid on end lanes
+      for (int g = 0; g < L.total; g += 32 * kWinBatch) {
+        int sh[kWinBatch];
+#pragma unroll
+        for (int c = 0; c < kWinBatch; ++c) sh[c] = 0;
+        unsigned ends = L.ends;
+        while (ends) {
+          const int e = __ffs(ends) - 1;
+          ends &= ends - 1;
+          const int wb = __shfl_sync(0xffffffffu, L.wbase, e);
+          const int sf = __shfl_sync(0xffffffffu, rshift, e);
+#pragma unroll
+          for (int c = 0; c < kWinBatch; ++c)
+            if (g + c * 32 + lane >= wb) sh[c] = sf;
+        }
+        double v[kWinBatch][S];
+#pragma unroll
+        for (int c = 0; c < kWinBatch; ++c) {
+          const int br = g + c * 32 + lane;
+          const int64_t gr = (int64_t)br + sh[c];
+          const bool in = br < L.total && gr >= 0 && gr < m;
+#pragma unroll
+          for (int i = 0; i < S; ++i) v[c][i] = in ? __ldg(Y + gr * S + i) : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < kWinBatch; ++c) {
+          const int br = g + c * 32 + lane;
+          if (br < L.total) {
+#pragma unroll
+            for (int i = 0; i < S; ++i) buf[br * SP + i] = v[c][i];
+          }
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < MAXW; ++k) {
+        if (k < width) {
+          const int o = __shfl_sync(0xffffffffu, L.row, k);
+          const double* yr = buf + (o + lane) * SP;
+#pragma unroll
+          for (int i = 0; i < S; ++i) {
+            const double y = yr[i];
+            a[i] += mv[k] * y;
+            b[i] += kv[k] * y;
+          }
+        }
+      }
+    } else {
+      uni = false;
+    }
+  }
+  if (!uni && r < m) {
+#pragma unroll
+    for (int k = 0; k < MAXW; ++k) {
+      if (k < width) {
+        const int c = __ldg(sell_col + base + k * kSlice + lane);
+        const double* yc = Y + (int64_t)c * S;
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+          const double y = __ldg(yc + i);
+          a[i] += mv[k] * y;
+          b[i] += kv[k] * y;
+        }
+      }
+    }
+  }
+  if (r >= m) return;
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    double o = 0.0, t = 0.0;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      o += cf.c1[i * S + j] * a[j];
+      t += cf.c2[i * S + j] * b[j];
+    }
+    Out[r * S + i] = flagged ? Y[r * S + i] : o + dt * t;
   }
 }
 
@@ -453,6 +599,14 @@ using namespace irk;
     case 8: { constexpr int SS = 8; CALL; } break;                             \
     default: break;                                                           \
   }
+#define IRK_STAGE_SWITCH4(S_, CALL)                                           \
+  switch (S_) {                                                               \
+    case 1: { constexpr int SS = 1; CALL; } break;                             \
+    case 2: { constexpr int SS = 2; CALL; } break;                             \
+    case 3: { constexpr int SS = 3; CALL; } break;                             \
+    case 4: { constexpr int SS = 4; CALL; } break;                             \
+    default: break;                                                           \
+  }
 
 extern "C" {
 
@@ -483,7 +637,45 @@ int irk_stage_apply(irk_ctx* ctx, int s, const double* C1_host, const double* C2
 #define IRK_LAUNCH_SA(PER, W)                                                             \
   IRK_STAGE_SWITCH(s, (k_stage_apply<SS, PER, W><<<g, kBlock, 0, ctx->stream>>>(          \
                           m, P->slice_ptr, P->sell_col, M->val, kp, cf, dt, rowmask_dev, \
-                          Y_dev, Out_dev)))
+                          Y_dev, Out_dev, P->ellw)))
+  static const bool win_off = getenv("IRK_NO_WINDOW") != nullptr;
+  const int wrows = P->win_rows;
+  const size_t wsmem = (size_t)(kBlock / 32) * wrows * (s % 2 == 0 ? s + 1 : s) * sizeof(double);
+  constexpr size_t kWinSmemMax = 96 * 1024;
+  if (!per && !win_off && s <= 4 && mw <= 16 && wrows > 0 && wsmem <= kWinSmemMax) {
+    const int64_t ns = P->nslices;
+    const unsigned gw = (unsigned)((ns + kBlock / 32 - 1) / (kBlock / 32));
+#define IRK_LAUNCH_WIN(W)                                                                       \
+  IRK_STAGE_SWITCH4(s, (k_stage_apply_win<SS, W><<<gw, kBlock, wsmem, ctx->stream>>>(            \
+                          m, ns, P->slice_ptr, P->sell_col, P->colhdr, M->val, kp.k[0], cf, dt, \
+                          rowmask_dev, Y_dev, Out_dev, P->ellw, wrows)))
+    static bool attr_set = false;
+    if (!attr_set) {
+      for (int ss = 1; ss <= 4; ++ss) {
+#define IRK_WIN_ATTR(W)                                                              \
+  IRK_STAGE_SWITCH4(ss, (cudaFuncSetAttribute(k_stage_apply_win<SS, W>,              \
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                              (int)kWinSmemMax)))
+        IRK_WIN_ATTR(4) IRK_WIN_ATTR(8) IRK_WIN_ATTR(10) IRK_WIN_ATTR(12) IRK_WIN_ATTR(16)
+#undef IRK_WIN_ATTR
+      }
+      attr_set = true;
+    }
+    if (mw <= 4) {
+      IRK_LAUNCH_WIN(4)
+    } else if (mw <= 8) {
+      IRK_LAUNCH_WIN(8)
+    } else if (mw <= 10) {
+      IRK_LAUNCH_WIN(10)
+    } else if (mw <= 12) {
+      IRK_LAUNCH_WIN(12)
+    } else {
+      IRK_LAUNCH_WIN(16)
+    }
+#undef IRK_LAUNCH_WIN
+    IRK_CHECK_LAUNCH(ctx);
+    return IRK_OK;
+  }
   if (per) {
     IRK_LAUNCH_SA(true, 0)
   } else if (mw <= 8) {
