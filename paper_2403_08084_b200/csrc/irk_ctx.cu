@@ -100,6 +100,8 @@ int irk_ctx_destroy(irk_ctx* ctx) {
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   delete ctx;
   return IRK_OK;
 }

@@ -27,6 +27,7 @@
 //    flagged columns are already eliminated (irk_mat_constrain).
 #pragma once
 
+#include <cstdlib>
 #include <vector>
 
 #include "irk_internal.cuh"
@@ -114,6 +115,9 @@ struct MatView {
   const double* ua;  // slot-uniform headers of A
   const double* b;   // values of Bm (or nullptr)
   const double* ub;
+  int ellw;          // > 0: ELL-32 (slice base = 32 * ellw * slice)
+  int win_rows;      // window rows of slot-uniform slices (0: none)
+  int64_t nslices;
 };
 
 __device__ __forceinline__ bool last_block_inner(unsigned int* counter) {
@@ -322,8 +326,14 @@ __global__ void __launch_bounds__(kBlock, 4)
     } else {
       const int64_t sl = row / kSlice;
       const int lane = (int)(row % kSlice);
-      const int base = __ldg(A.slice_ptr + sl);
-      const int width = (__ldg(A.slice_ptr + sl + 1) - base) / kSlice;
+      int base, width;
+      if (A.ellw) {
+        base = (int)(sl * kSlice * A.ellw);
+        width = A.ellw;
+      } else {
+        base = __ldg(A.slice_ptr + sl);
+        width = (__ldg(A.slice_ptr + sl + 1) - base) / kSlice;
+      }
       const int q0 = base / kSlice;
       if (MAXW > 0) {
         int cc[MAXW > 0 ? MAXW : 1];
@@ -424,20 +434,63 @@ __global__ void __launch_bounds__(kBlock)
     rho[k] = s_zero(T{});
     rr[k] = 0.0;
   }
-  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < m;
-       row += (int64_t)gridDim.x * blockDim.x) {
+  // small NB: U rows per thread per pass with every load issued before the
+  // stores (memory-level parallelism); large NB: one row, system by system
+  constexpr int NW = NB * (int)(sizeof(T) / 8);
+  constexpr int U = NW <= 1 ? 2 : 1;
+  const int64_t TT = (int64_t)gridDim.x * blockDim.x;
+  if constexpr (NW <= 2) {
+    for (int64_t row0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row0 < m;
+         row0 += U * TT) {
+      T pk[U][NB], qk[U][NB], dk[U][NB], xk[U][NB], rk[U][NB];
 #pragma unroll
-    for (int k = 0; k < NB; ++k) {
-      if (!act[k]) continue;
-      const int64_t qi = row * NB + k;
-      T pk = p[qi];
-      x[qi] = s_add(x[qi], s_mul(alpha[k], pk));
-      T rk = s_sub(r[qi], s_mul(alpha[k], q[qi]));
-      r[qi] = rk;
-      T zk = s_mul(dinv[qi], rk);
-      z[qi] = zk;
-      rho[k] = s_add(rho[k], s_mul(rk, zk));
-      rr[k] += s_abs2(rk);
+      for (int u = 0; u < U; ++u) {
+        const int64_t row = row0 + u * TT;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          if (row < m && act[k]) {
+            const int64_t qi = row * NB + k;
+            pk[u][k] = p[qi];
+            qk[u][k] = q[qi];
+            dk[u][k] = dinv[qi];
+            xk[u][k] = x[qi];
+            rk[u][k] = r[qi];
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t row = row0 + u * TT;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          if (row < m && act[k]) {
+            const int64_t qi = row * NB + k;
+            x[qi] = s_add(xk[u][k], s_mul(alpha[k], pk[u][k]));
+            T rn = s_sub(rk[u][k], s_mul(alpha[k], qk[u][k]));
+            r[qi] = rn;
+            T zn = s_mul(dk[u][k], rn);
+            z[qi] = zn;
+            rho[k] = s_add(rho[k], s_mul(rn, zn));
+            rr[k] += s_abs2(rn);
+          }
+        }
+      }
+    }
+  } else {
+    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < m; row += TT) {
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        if (!act[k]) continue;
+        const int64_t qi = row * NB + k;
+        T pk = p[qi];
+        x[qi] = s_add(x[qi], s_mul(alpha[k], pk));
+        T rk = s_sub(r[qi], s_mul(alpha[k], q[qi]));
+        r[qi] = rk;
+        T zk = s_mul(dinv[qi], rk);
+        z[qi] = zk;
+        rho[k] = s_add(rho[k], s_mul(rk, zk));
+        rr[k] += s_abs2(rk);
+      }
     }
   }
   const int G = gridDim.x;
@@ -534,16 +587,36 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   const int chunk = m < 65536 ? 8 : 16;
   int issued = 0, c = 0;
   T* pbuf[2] = {w.p0, w.p1};
+  // one chunk = `n` iterations starting at parity `par` of the p buffers
+  auto chunk_body = [&](cudaStream_t cs, int n, int par) -> int {
+    for (int t = 0; t < n; ++t) {
+      T* pold = pbuf[(par + t) & 1];
+      T* pnew = pbuf[(par + t + 1) & 1];
+      k_cg_spmv<T, NB, HASB, MAXW><<<G, kBlock, 0, cs>>>(m, A, P, shift, mask, w.z, pold, pnew,
+                                                         w.q, w.st, ctx->red, cnt);
+      IRK_CHECK_LAUNCH(ctx);
+      k_cg_update<T, NB><<<G, kBlock, 0, cs>>>(m, pnew, w.q, w.dinv, w.x, w.r, w.z, maxit, w.st,
+                                               ctx->red, cnt);
+      IRK_CHECK_LAUNCH(ctx);
+    }
+    return IRK_OK;
+  };
+  // full chunks replay a cached CUDA graph (host launch cost is paid once
+  // per chunk instead of per kernel); the key holds every launch argument
+  GraphKey key;
+  key.add((const void*)&k_cg_spmv<T, NB, HASB, MAXW>).add((const void*)&k_cg_update<T, NB>);
+  key.add(m).add(G).add(A).add(P).add(shift).add(mask).add(w).add(ctx->red).add(cnt);
+  key.add(maxit).add(chunk);
   for (;;) {
-    for (int t = 0; t < chunk && issued < maxit; ++t, ++issued) {
-      T* pold = pbuf[issued & 1];
-      T* pnew = pbuf[(issued + 1) & 1];
-      k_cg_spmv<T, NB, HASB, MAXW><<<G, kBlock, 0, s>>>(m, A, P, shift, mask, w.z, pold, pnew,
-                                                        w.q, w.st, ctx->red, cnt);
-      IRK_CHECK_LAUNCH(ctx);
-      k_cg_update<T, NB><<<G, kBlock, 0, s>>>(m, pnew, w.q, w.dinv, w.x, w.r, w.z, maxit, w.st,
-                                              ctx->red, cnt);
-      IRK_CHECK_LAUNCH(ctx);
+    if (issued + chunk <= maxit) {
+      const int par = issued & 1;
+      GraphKey kp = key;
+      kp.add(par);
+      IRK_TRY(graph_launch(ctx, kp.k, [&](cudaStream_t cs) { return chunk_body(cs, chunk, par); }));
+      issued += chunk;
+    } else {
+      IRK_TRY(chunk_body(s, maxit - issued, issued & 1));
+      issued = maxit;
     }
     IRK_CUDA(cudaMemcpyAsync(hst[c & 1], w.st, sizeof(SysState<T>), cudaMemcpyDeviceToHost, s));
     IRK_CUDA(cudaEventRecord(ctx->ev[c & 1], s));
@@ -602,7 +675,8 @@ int dispatch_flags(irk_ctx* ctx, int64_t m, int maxw, const MatView& A, const Sy
 inline MatView make_view(const irk_mat* A, const irk_mat* Bm) {
   const Pattern* p = A->pat;
   return MatView{p->slice_ptr, p->sell_col, p->colhdr, p->diag_pos, A->val, A->uval,
-                 Bm ? Bm->val : nullptr, Bm ? Bm->uval : nullptr};
+                 Bm ? Bm->val : nullptr, Bm ? Bm->uval : nullptr, p->ellw, p->win_rows,
+                 p->nslices};
 }
 
 }  // namespace irk

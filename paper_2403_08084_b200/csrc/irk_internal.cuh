@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <climits>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -78,6 +79,16 @@ struct irk_ctx {
   char* pinned = nullptr;
   size_t pinned_cap = 0;
   cudaEvent_t ev[2] = {nullptr, nullptr};
+  // CUDA-graph cache for fixed launch sequences (inner-solver chunks): a
+  // graph is a pure function of its key (kernels + every launch argument),
+  // captured on a private stream and replayed on `stream`.
+  struct GraphEntry {
+    std::string key;
+    cudaGraphExec_t exec;
+    int64_t kernels;
+  };
+  std::vector<GraphEntry> graphs;
+  cudaStream_t cap_stream = nullptr;
 };
 
 namespace irk {
@@ -124,6 +135,55 @@ constexpr int kNumCounters = 16;
 int ensure_red(irk_ctx* ctx, size_t doubles);
 int ensure_work(irk_ctx* ctx, size_t bytes);
 int ensure_pinned(irk_ctx* ctx, size_t bytes);
+// Byte-string key builder for the graph cache.
+struct GraphKey {
+  std::string k;
+  template <class V>
+  GraphKey& add(const V& v) {
+    k.append(reinterpret_cast<const char*>(&v), sizeof(V));
+    return *this;
+  }
+};
+
+// Replay the cached graph for `key`, or capture `body(stream)` (a fixed
+// kernel sequence that must not synchronise) into one, then replay it on
+// ctx->stream.  IRK_NO_GRAPH=1 runs body directly on ctx->stream.
+template <class F>
+int graph_launch(irk_ctx* ctx, const std::string& key, F&& body) {
+  static const bool off = getenv("IRK_NO_GRAPH") != nullptr;
+  if (off) return body(ctx->stream);
+  for (auto& g : ctx->graphs) {
+    if (g.key == key) {
+      IRK_CUDA(cudaGraphLaunch(g.exec, ctx->stream));
+      ctx->launches += g.kernels;
+      return IRK_OK;
+    }
+  }
+  if (!ctx->cap_stream)
+    IRK_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+  const int64_t l0 = ctx->launches;
+  IRK_CUDA(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+  const int rc = body(ctx->cap_stream);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &graph);
+  if (rc != IRK_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  IRK_CUDA(e);
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  IRK_CUDA(ei);
+  if (ctx->graphs.size() >= 64) {
+    cudaGraphExecDestroy(ctx->graphs.front().exec);
+    ctx->graphs.erase(ctx->graphs.begin());
+  }
+  ctx->graphs.push_back({key, exec, ctx->launches - l0});
+  IRK_CUDA(cudaGraphLaunch(exec, ctx->stream));
+  return IRK_OK;
+}
+
 inline int grid_for(const irk_ctx* ctx, int64_t work_items, int per_block = kBlock,
                     int blocks_per_sm = 8) {
   int64_t g = (work_items + per_block - 1) / per_block;
