@@ -27,6 +27,7 @@
 //    flagged columns are already eliminated (irk_mat_constrain).
 #pragma once
 
+#include <algorithm>
 #include <cstdlib>
 #include <vector>
 
@@ -116,8 +117,8 @@ struct MatView {
   const double* b;   // values of Bm (or nullptr)
   const double* ub;
   int ellw;          // > 0: ELL-32 (slice base = 32 * ellw * slice)
-  int win_rows;      // window rows of slot-uniform slices (0: none)
-  int64_t nslices;
+  int sw;            // > 0: stencil-aligned ELL pattern with offsets sd[0..sw)
+  int sd[16];
 };
 
 __device__ __forceinline__ bool last_block_inner(unsigned int* counter) {
@@ -411,6 +412,93 @@ __global__ void __launch_bounds__(kBlock, 4)
   }
 }
 
+// Stencil variant of k_cg_spmv (one real system, stencil-aligned ELL
+// pattern of width W, e.g. the P1/Q1 grid operators).  The gathers of
+// p = z + beta p_old at the W stencil offsets are issued immediately, in
+// parallel with the slice's slot headers (lane k loads slot k once per
+// slice); z and p_old carry `pad` >= max |offset| readable elements on both
+// sides, so speculative gathers of boundary rows stay inside the
+// allocation.  A slice whose headers all match the stencil with uniform
+// values (the interior) then needs one shuffle + FMA per entry; any other
+// slice is recomputed through the SELL arrays.
+template <int W, bool HASB>
+__global__ void __launch_bounds__(kBlock, 4)
+    k_cg_spmv_st(int m, MatView A, const SysParams<double> P, const double* __restrict__ shift,
+                 const uint8_t* __restrict__ mask, const double* __restrict__ z,
+                 const double* __restrict__ pold, double* __restrict__ pnew,
+                 double* __restrict__ q, SysState<double>* st, double* __restrict__ part,
+                 unsigned int* counter) {
+  if (st->done) return;
+  const double beta = st->beta[0];
+  const bool act = st->active[0] != 0;
+  const int lane = threadIdx.x & 31;
+  const int nsl = (m + kSlice - 1) / kSlice;
+  const int wstride = gridDim.x * (blockDim.x / 32);
+  const double al = P.alpha[0], be = P.beta[0];
+  double mu = 0.0;
+  for (int sl = (blockIdx.x * blockDim.x + threadIdx.x) / 32; sl < nsl; sl += wstride) {
+    const int row = sl * kSlice + lane;
+    const bool valid = row < m;
+    const int q0 = sl * W;
+    const bool hl = lane < W;
+    const int hd = hl ? __ldg(A.colhdr + q0 + lane) : 0;
+    const double ha = hl ? __ldg(A.ua + q0 + lane) : 0.0;
+    const double hb = (HASB && hl) ? __ldg(A.ub + q0 + lane) : 0.0;
+    const double pr = z[row] + beta * pold[row];
+    const bool flagged = valid && mask && mask[row];
+    double ps[W];
+#pragma unroll
+    for (int kk = 0; kk < W; ++kk) {
+      const int c = row + A.sd[kk];
+      ps[kk] = z[c] + beta * pold[c];
+    }
+    const bool ok = __all_sync(0xffffffffu, !hl || (hd == A.sd[lane < W ? lane : 0] &&
+                                                    !isnan(ha) && !(HASB && isnan(hb))));
+    double acc = 0.0;
+    if (ok) {
+      const double hc = HASB ? al * ha + be * hb : al * ha;
+#pragma unroll
+      for (int kk = 0; kk < W; ++kk) acc += __shfl_sync(0xffffffffu, hc, kk) * ps[kk];
+    } else if (valid) {
+      const int base = sl * kSlice * W;
+#pragma unroll
+      for (int kk = 0; kk < W; ++kk) {
+        const int pos = base + kk * kSlice + lane;
+        const int c = sell_col_at(A.colhdr, A.sell_col, q0 + kk, pos, row);
+        const double av = sell_val_at(A.ua, A.a, q0 + kk, pos);
+        const double bv = HASB ? sell_val_at(A.ub, A.b, q0 + kk, pos) : 0.0;
+        acc += (HASB ? al * av + be * bv : al * av) * (z[c] + beta * pold[c]);
+      }
+    }
+    if (shift && valid) acc += shift[row] * pr;
+    if (flagged) acc = pr;
+    if (valid && act) {
+      pnew[row] = pr;
+      q[row] = acc;
+      mu += pr * acc;
+    }
+  }
+  const int G = gridDim.x;
+  double mus[1] = {mu};
+  block_reduce_store<double, 1>(mus, part);
+  if (last_block_inner(counter)) {
+    __shared__ double smu[1];
+    reduce_partials<double, 1>(part, G, smu);
+    __syncthreads();
+    if (threadIdx.x == 0 && st->active[0]) {
+      const double muk = smu[0];
+      st->mu[0] = muk;
+      if (!isfinite(muk) || muk == 0.0) {
+        st->active[0] = 0;
+        st->code[0] = 2;
+        st->alpha[0] = 0.0;
+      } else {
+        st->alpha[0] = st->rho[0] / muk;
+      }
+    }
+  }
+}
+
 // x += alpha p, r -= alpha q, z = D^-1 r; rho' = r^T z, rr = ||r||^2;
 // convergence / cap / beta by the last block.
 template <typename T, int NB>
@@ -547,21 +635,30 @@ template <typename T>
 struct Workspace {
   SysState<T>* st;
   T *x, *r, *z, *p0, *p1, *q, *dinv;
+  int64_t pad;  // readable elements before/after z, p0, p1 (stencil gathers)
 };
 
+// pad > 0: z, p0 and p1 get `pad` extra elements (zeroed) on both sides
 template <typename T>
-int carve(irk_ctx* ctx, int64_t m, int nb, Workspace<T>& w) {
+int carve(irk_ctx* ctx, int64_t m, int nb, Workspace<T>& w, int64_t pad = 0) {
   size_t vec = (size_t)m * nb * sizeof(T);
   vec = (vec + 255) & ~(size_t)255;
+  size_t pb = ((size_t)pad * nb * sizeof(T) + 255) & ~(size_t)255;
   size_t head = (sizeof(SysState<T>) + 255) & ~(size_t)255;
-  IRK_TRY(ensure_work(ctx, head + 7 * vec));
+  IRK_TRY(ensure_work(ctx, head + 7 * vec + 6 * pb));
   char* b = ctx->work;
   w.st = reinterpret_cast<SysState<T>*>(b);
   b += head;
-  T** v[7] = {&w.x, &w.r, &w.z, &w.p0, &w.p1, &w.q, &w.dinv};
+  w.pad = pad;
+  T** v[7] = {&w.x, &w.r, &w.q, &w.dinv, &w.z, &w.p0, &w.p1};
   for (int i = 0; i < 7; ++i) {
+    if (i >= 4) {
+      if (pb) IRK_CUDA(cudaMemsetAsync(b, 0, 2 * pb + vec, ctx->stream));
+      b += pb;
+    }
     *v[i] = reinterpret_cast<T*>(b);
     b += vec;
+    if (i >= 4) b += pb;
   }
   return IRK_OK;
 }
@@ -571,7 +668,12 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
            const uint8_t* mask, const T* rhs, int64_t ld_rhs, T* xout, int64_t ld_x, double rtol,
            double atol, int maxit, int* its_host, double* relres_host) {
   Workspace<T> w;
-  IRK_TRY(carve<T>(ctx, m, NB, w));
+  int64_t pad = 0;
+  if (NB == 1 && sizeof(T) == 8 && A.sw > 0) {
+    for (int k = 0; k < A.sw; ++k) pad = std::max<int64_t>(pad, std::abs(A.sd[k]));
+    pad += kSlice;
+  }
+  IRK_TRY(carve<T>(ctx, m, NB, w, pad));
   const int G = grid_for(ctx, m, kBlock, 4);
   IRK_TRY(ensure_red(ctx, (size_t)G * NB * 4 + 64));
   IRK_TRY(ensure_pinned(ctx, 2 * sizeof(SysState<T>) + 64));
@@ -585,6 +687,10 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
                          reinterpret_cast<SysState<T>*>(ctx->pinned) + 1};
   // Chunked issue with one chunk in flight ahead of the host check.
   const int chunk = m < 65536 ? 8 : 16;
+  constexpr bool kStencil = NB == 1 && sizeof(T) == 8 && MAXW > 0;
+  static const bool stencil_off = getenv("IRK_NO_STENCIL") != nullptr;
+  const bool stencil = kStencil && !stencil_off && w.pad > 0 && m < INT_MAX / 2 &&
+                       (A.sw == 3 || A.sw == 5 || A.sw == 7 || A.sw == 9);
   int issued = 0, c = 0;
   T* pbuf[2] = {w.p0, w.p1};
   // one chunk = `n` iterations starting at parity `par` of the p buffers
@@ -592,8 +698,27 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
     for (int t = 0; t < n; ++t) {
       T* pold = pbuf[(par + t) & 1];
       T* pnew = pbuf[(par + t + 1) & 1];
-      k_cg_spmv<T, NB, HASB, MAXW><<<G, kBlock, 0, cs>>>(m, A, P, shift, mask, w.z, pold, pnew,
-                                                         w.q, w.st, ctx->red, cnt);
+      if constexpr (kStencil) {
+        if (stencil) {
+          const double* zz = reinterpret_cast<const double*>(w.z);
+          const double* po = reinterpret_cast<const double*>(pold);
+          double* pn = reinterpret_cast<double*>(pnew);
+          double* qq = reinterpret_cast<double*>(w.q);
+          const SysParams<double>& Pd = reinterpret_cast<const SysParams<double>&>(P);
+          SysState<double>* sd = reinterpret_cast<SysState<double>*>(w.st);
+#define IRK_ST(WW)                                                                           \
+  k_cg_spmv_st<WW, HASB><<<G, kBlock, 0, cs>>>((int)m, A, Pd, shift, mask, zz, po, pn, qq, sd, \
+                                              ctx->red, cnt)
+          if (A.sw == 7) IRK_ST(7);
+          else if (A.sw == 9) IRK_ST(9);
+          else if (A.sw == 5) IRK_ST(5);
+          else IRK_ST(3);
+#undef IRK_ST
+        }
+      }
+      if (!stencil)
+        k_cg_spmv<T, NB, HASB, MAXW><<<G, kBlock, 0, cs>>>(m, A, P, shift, mask, w.z, pold,
+                                                           pnew, w.q, w.st, ctx->red, cnt);
       IRK_CHECK_LAUNCH(ctx);
       k_cg_update<T, NB><<<G, kBlock, 0, cs>>>(m, pnew, w.q, w.dinv, w.x, w.r, w.z, maxit, w.st,
                                                ctx->red, cnt);
@@ -605,6 +730,7 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   // per chunk instead of per kernel); the key holds every launch argument
   GraphKey key;
   key.add((const void*)&k_cg_spmv<T, NB, HASB, MAXW>).add((const void*)&k_cg_update<T, NB>);
+  key.add(stencil);
   key.add(m).add(G).add(A).add(P).add(shift).add(mask).add(w).add(ctx->red).add(cnt);
   key.add(maxit).add(chunk);
   for (;;) {
@@ -674,9 +800,13 @@ int dispatch_flags(irk_ctx* ctx, int64_t m, int maxw, const MatView& A, const Sy
 
 inline MatView make_view(const irk_mat* A, const irk_mat* Bm) {
   const Pattern* p = A->pat;
-  return MatView{p->slice_ptr, p->sell_col, p->colhdr, p->diag_pos, A->val, A->uval,
-                 Bm ? Bm->val : nullptr, Bm ? Bm->uval : nullptr, p->ellw, p->win_rows,
-                 p->nslices};
+  MatView v{p->slice_ptr, p->sell_col, p->colhdr, p->diag_pos, A->val, A->uval,
+            Bm ? Bm->val : nullptr, Bm ? Bm->uval : nullptr, p->ellw, 0, {}};
+  if (p->ellw > 0 && (int)p->stencil.size() == p->ellw && p->ellw <= 16) {
+    v.sw = p->ellw;
+    for (int k = 0; k < v.sw; ++k) v.sd[k] = p->stencil[k];
+  }
+  return v;
 }
 
 }  // namespace irk

@@ -48,6 +48,9 @@ struct Pattern {
   std::vector<int> h_cmin, h_cmax;
   // max over slot-uniform slices of the window rows (win_layout); 0 if none
   int win_rows = 0;
+  // stencil-aligned ELL patterns: the ellw column offsets of every full row
+  // (slot k of a stencil row holds column row + stencil[k]); else empty
+  std::vector<int> stencil;
 };
 
 constexpr int kNonUniform = INT_MIN;

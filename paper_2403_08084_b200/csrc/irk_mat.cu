@@ -269,6 +269,7 @@ int pattern_build_sell(irk_ctx* ctx, Pattern* p) {
         IRK_CUDA(cudaMemcpyAsync(d_stencil, st.data(), p->ellw * sizeof(int),
                                  cudaMemcpyHostToDevice, ctx->stream));
         W = p->ellw;
+        p->stencil = st;
         break;
       }
     }

@@ -20,8 +20,9 @@ def main():
     from paper_2403_08084_b200 import sparsela as la
     from paper_2403_08084_b200.stepper import _SPLIT
 
-    k = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-    iters = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    k = int(args[0]) if len(args) > 0 else 2
+    iters = int(args[1]) if len(args) > 1 else 200
     wl = configs.build(k)
     st, prob = wl.stepper, wl.problem
     if st.formulation.name == "DIRK":
@@ -42,6 +43,13 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1) * 1e3 / max(its, 1))
+    if "--prof" in sys.argv:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fac.dev_solve(b, x, settings=fixed)
+            torch.cuda.synchronize()
+        print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=6,
+                                        max_name_column_width=60))
     conv = la.BlockSolveSettings(rtol=1e-6)
     its_conv = fac.dev_solve(b, x, settings=conv)
     print(f"config {k} m={m}: {best:.2f} us/PCG iteration ({its} its fixed); "
