@@ -91,7 +91,7 @@ struct SysParams {
 
 // Device-resident loop state (one block of memory, polled by the host).
 template <typename T>
-struct SysState {
+struct alignas(16) SysState {
   T rho[kMaxSys];    // r^T z
   T mu[kMaxSys];     // p^T A p
   T alpha[kMaxSys];  // step
@@ -174,6 +174,64 @@ __device__ __forceinline__ void reduce_partials(const T* part, int G, T* out) {
   __syncthreads();
 }
 
+
+// Three reductions at once (one L2 round trip, one barrier pair): the mu
+// and rho partials (T) and the ||r||^2 partials (double) of the previous
+// kernels.  Same fixed summation order as reduce_partials.
+template <typename T, int NB>
+__device__ __forceinline__ void reduce_partials3(const T* pa, const T* pb, const double* pc,
+                                                 int G, T* oa, T* ob, double* oc) {
+  __shared__ T ra[kBlock / 32][NB], rb[kBlock / 32][NB];
+  __shared__ double rc[kBlock / 32][NB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T va[NB], vb[NB];
+  double vc[NB];
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    va[k] = vb[k] = s_zero(T{});
+    vc[k] = 0.0;
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int b = threadIdx.x + c * kBlock;
+    if (b < G) {
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        va[k] = s_add(va[k], ld_cg(pa + (int64_t)k * G + b));
+        vb[k] = s_add(vb[k], ld_cg(pb + (int64_t)k * G + b));
+        vc[k] += __ldcg(pc + (int64_t)k * G + b);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    va[k] = s_wsum(va[k]);
+    vb[k] = s_wsum(vb[k]);
+    vc[k] = warp_sum(vc[k]);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      ra[warp][k] = va[k];
+      rb[warp][k] = vb[k];
+      rc[warp][k] = vc[k];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < NB) {
+    T ta = s_zero(T{}), tb = s_zero(T{});
+    double tc = 0.0;
+    for (int w = 0; w < kBlock / 32; ++w) {
+      ta = s_add(ta, ra[w][threadIdx.x]);
+      tb = s_add(tb, rb[w][threadIdx.x]);
+      tc += rc[w][threadIdx.x];
+    }
+    oa[threadIdx.x] = ta;
+    ob[threadIdx.x] = tb;
+    oc[threadIdx.x] = tc;
+  }
+  __syncthreads();
+}
 
 template <typename T, int NB>
 __device__ __forceinline__ void block_reduce_store(T (&v)[NB], T* part) {
@@ -292,6 +350,139 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// --------------------------------------------- tail-free iteration control
+// Iteration k is two kernels, A_k (SpMV + direction) and B_k (update), with
+// parity c = k & 1.  Neither kernel ends in a last-block reduction: each
+// writes per-block partials, and every block of the NEXT kernel reduces
+// them redundantly (same fixed order in every block, so all blocks take
+// bitwise-identical decisions).  The loop state is double-buffered:
+// A_k reads st[c^1] (written by A_{k-1}, or by the init kernel for k = 0),
+// applies the convergence / breakdown / cap decisions of iteration k-1 and
+// block 0 writes the result to st[c]; B_k reads st[c].  A finished state is
+// propagated by every later A (block 0 copies it forward).
+template <typename T, int NB>
+struct CgPart {
+  T* mu;
+  T* rz;
+  double* rr;
+};
+
+template <typename T, int NB>
+__host__ __device__ __forceinline__ size_t cg_part_doubles(int G) {
+  // rounded to 256 B so every buffer (complex ones included) stays aligned
+  return ((size_t)G * NB * (2 * sizeof(T) / 8 + 1) + 31) & ~(size_t)31;
+}
+
+template <typename T, int NB>
+__host__ __device__ __forceinline__ CgPart<T, NB> cg_part(double* red, int G, int c) {
+  double* b = red + c * cg_part_doubles<T, NB>(G);
+  T* t = reinterpret_cast<T*>(b);
+  return {t, t + (size_t)G * NB, b + 2 * (size_t)G * NB * (sizeof(T) / 8)};
+}
+
+template <typename T>
+__device__ __forceinline__ void state_copy(SysState<T>* dst, const SysState<T>* src) {
+  constexpr int nw = sizeof(SysState<T>) / 4;
+  for (int i = threadIdx.x; i < nw; i += blockDim.x)
+    reinterpret_cast<int*>(dst)[i] = __ldcg(reinterpret_cast<const int*>(src) + i);
+}
+
+// Prologue of A_k: returns true when the solve is finished (all threads).
+template <typename T, int NB>
+__device__ __forceinline__ bool cg_enter_a(const SysState<T>* sin, SysState<T>* sout,
+                                           double* red, int c, int first, int maxit,
+                                           T (&beta)[NB], bool (&act)[NB]) {
+  __shared__ SysState<T> S;
+  __shared__ T smu[NB], srz[NB];
+  __shared__ double srr[NB];
+  const int G = gridDim.x;
+  state_copy(&S, sin);
+  if (!first) {
+    // issued together with the state loads; reduce_partials3 synchronises
+    const CgPart<T, NB> pin = cg_part<T, NB>(red, G, c ^ 1);
+    reduce_partials3<T, NB>(pin.mu, pin.rz, pin.rr, G, smu, srz, srr);
+  } else {
+    __syncthreads();
+  }
+  if (S.done) {
+    if (blockIdx.x == 0) {
+      constexpr int nw = sizeof(SysState<T>) / 4;
+      for (int i = threadIdx.x; i < nw; i += blockDim.x)
+        reinterpret_cast<int*>(sout)[i] = reinterpret_cast<const int*>(&S)[i];
+    }
+    return true;
+  }
+  if (!first) {
+    if (threadIdx.x == 0) {
+      int any = 0;
+      for (int k = 0; k < NB; ++k) {
+        if (!S.active[k]) continue;
+        const T muk = smu[k];
+        if (!s_finite(muk) || s_isnull(muk)) {  // B_{k-1} skipped the update
+          S.active[k] = 0;
+          S.code[k] = 2;
+          continue;
+        }
+        S.mu[k] = muk;
+        S.its[k] += 1;
+        S.rr[k] = srr[k];
+        if (!(srr[k] > S.tol2[k])) {
+          S.active[k] = 0;  // converged (or NaN residual: flagged below)
+          if (!isfinite(srr[k])) S.code[k] = 2;
+        } else if (S.its[k] >= maxit) {
+          S.active[k] = 0;
+          S.code[k] = 1;
+        } else if (!s_finite(srz[k]) || s_isnull(srz[k])) {
+          S.active[k] = 0;
+          S.code[k] = 2;
+        } else {
+          S.beta[k] = s_div(srz[k], S.rho[k]);
+          S.rho[k] = srz[k];
+        }
+        any |= S.active[k];
+      }
+      S.iter += 1;
+      S.done = any ? 0 : 1;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    beta[k] = S.beta[k];
+    act[k] = S.active[k] != 0;
+  }
+  const bool done = S.done != 0;
+  if (blockIdx.x == 0) {
+    constexpr int nw = sizeof(SysState<T>) / 4;
+    for (int i = threadIdx.x; i < nw; i += blockDim.x)
+      reinterpret_cast<int*>(sout)[i] = reinterpret_cast<const int*>(&S)[i];
+  }
+  __syncthreads();
+  return done;
+}
+
+// Prologue of B_k: alpha = rho / mu from A_k's partials; true when finished.
+template <typename T, int NB>
+__device__ __forceinline__ bool cg_enter_b(const SysState<T>* st, double* red, int c,
+                                           T (&alpha)[NB], bool (&act)[NB]) {
+  __shared__ T smu[NB], srho[NB];
+  __shared__ int sact[NB], sdone;
+  if (threadIdx.x < NB) {
+    srho[threadIdx.x] = ld_cg(&st->rho[threadIdx.x]);
+    sact[threadIdx.x] = __ldcg(&st->active[threadIdx.x]);
+  }
+  if (threadIdx.x == 0) sdone = __ldcg(&st->done);
+  reduce_partials<T, NB>(cg_part<T, NB>(red, gridDim.x, c).mu, gridDim.x, smu);
+  if (sdone) return true;
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    const T muk = smu[k];
+    act[k] = sact[k] && s_finite(muk) && !s_isnull(muk);
+    alpha[k] = act[k] ? s_div(srho[k], muk) : s_zero(T{});
+  }
+  return false;
+}
+
 // ------------------------------------------------- SpMV + direction update
 // p_new = z + beta p_old (computed on the fly for every gathered column),
 // q = B p_new, mu = p_new^T q;  alpha = rho / mu by the last block.
@@ -300,15 +491,11 @@ __global__ void __launch_bounds__(kBlock, 4)
     k_cg_spmv(int64_t m, MatView A, const SysParams<T> P, const double* __restrict__ shift,
               const uint8_t* __restrict__ mask, const T* __restrict__ z,
               const T* __restrict__ pold, T* __restrict__ pnew, T* __restrict__ q,
-              SysState<T>* st, double* __restrict__ part, unsigned int* counter) {
-  if (st->done) return;
+              const SysState<T>* sin, SysState<T>* sout, double* red, int c, int first,
+              int maxit) {
   T beta[NB];
   bool act[NB];
-#pragma unroll
-  for (int k = 0; k < NB; ++k) {
-    beta[k] = st->beta[k];
-    act[k] = st->active[k] != 0;
-  }
+  if (cg_enter_a<T, NB>(sin, sout, red, c, first, maxit, beta, act)) return;
   T mu[NB];
 #pragma unroll
   for (int k = 0; k < NB; ++k) mu[k] = s_zero(T{});
@@ -388,28 +575,7 @@ __global__ void __launch_bounds__(kBlock, 4)
       mu[k] = s_add(mu[k], s_mul(pr[k], acc[k]));
     }
   }
-  const int G = gridDim.x;
-  T* pp = reinterpret_cast<T*>(part);
-  block_reduce_store<T, NB>(mu, pp);
-  if (last_block_inner(counter)) {
-    __shared__ T smu[NB];
-    reduce_partials<T, NB>(pp, G, smu);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int k = 0; k < NB; ++k) {
-        if (!st->active[k]) continue;
-        T muk = smu[k];
-        st->mu[k] = muk;
-        if (!s_finite(muk) || s_isnull(muk)) {
-          st->active[k] = 0;
-          st->code[k] = 2;
-          st->alpha[k] = s_zero(T{});
-        } else {
-          st->alpha[k] = s_div(st->rho[k], muk);
-        }
-      }
-    }
-  }
+  block_reduce_store<T, NB>(mu, cg_part<T, NB>(red, gridDim.x, c).mu);
 }
 
 // Stencil variant of k_cg_spmv (one real system, stencil-aligned ELL
@@ -426,11 +592,13 @@ __global__ void __launch_bounds__(kBlock, 4)
     k_cg_spmv_st(int m, MatView A, const SysParams<double> P, const double* __restrict__ shift,
                  const uint8_t* __restrict__ mask, const double* __restrict__ z,
                  const double* __restrict__ pold, double* __restrict__ pnew,
-                 double* __restrict__ q, SysState<double>* st, double* __restrict__ part,
-                 unsigned int* counter) {
-  if (st->done) return;
-  const double beta = st->beta[0];
-  const bool act = st->active[0] != 0;
+                 double* __restrict__ q, const SysState<double>* sin, SysState<double>* sout,
+                 double* red, int cpar, int first, int maxit) {
+  double betas[1];
+  bool acts[1];
+  if (cg_enter_a<double, 1>(sin, sout, red, cpar, first, maxit, betas, acts)) return;
+  const double beta = betas[0];
+  const bool act = acts[0];
   const int lane = threadIdx.x & 31;
   const int nsl = (m + kSlice - 1) / kSlice;
   const int wstride = gridDim.x * (blockDim.x / 32);
@@ -478,43 +646,20 @@ __global__ void __launch_bounds__(kBlock, 4)
       mu += pr * acc;
     }
   }
-  const int G = gridDim.x;
   double mus[1] = {mu};
-  block_reduce_store<double, 1>(mus, part);
-  if (last_block_inner(counter)) {
-    __shared__ double smu[1];
-    reduce_partials<double, 1>(part, G, smu);
-    __syncthreads();
-    if (threadIdx.x == 0 && st->active[0]) {
-      const double muk = smu[0];
-      st->mu[0] = muk;
-      if (!isfinite(muk) || muk == 0.0) {
-        st->active[0] = 0;
-        st->code[0] = 2;
-        st->alpha[0] = 0.0;
-      } else {
-        st->alpha[0] = st->rho[0] / muk;
-      }
-    }
-  }
+  block_reduce_store<double, 1>(mus, cg_part<double, 1>(red, gridDim.x, cpar).mu);
 }
 
-// x += alpha p, r -= alpha q, z = D^-1 r; rho' = r^T z, rr = ||r||^2;
-// convergence / cap / beta by the last block.
+// x += alpha p, r -= alpha q, z = D^-1 r; partials of rho' = r^T z and
+// rr = ||r||^2 (the next A kernel decides convergence / cap / beta).
 template <typename T, int NB>
 __global__ void __launch_bounds__(kBlock)
     k_cg_update(int64_t m, const T* __restrict__ p, const T* __restrict__ q,
                 const T* __restrict__ dinv, T* __restrict__ x, T* __restrict__ r,
-                T* __restrict__ z, int maxit, SysState<T>* st, double* __restrict__ part,
-                unsigned int* counter) {
-  if (st->done) return;
+                T* __restrict__ z, const SysState<T>* st, double* red, int c) {
   T alpha[NB];
   bool act[NB];
-#pragma unroll
-  for (int k = 0; k < NB; ++k) {
-    alpha[k] = st->alpha[k];
-    act[k] = st->active[k] != 0;
-  }
+  if (cg_enter_b<T, NB>(st, red, c, alpha, act)) return;
   T rho[NB];
   double rr[NB];
 #pragma unroll
@@ -581,42 +726,9 @@ __global__ void __launch_bounds__(kBlock)
       }
     }
   }
-  const int G = gridDim.x;
-  T* pr = reinterpret_cast<T*>(part);
-  double* pb = reinterpret_cast<double*>(pr + (int64_t)NB * G);
-  block_reduce_store<T, NB>(rho, pr);
-  block_reduce_store_d<NB>(rr, pb);
-  if (last_block_inner(counter)) {
-    __shared__ T srho[NB];
-    __shared__ double srr[NB];
-    reduce_partials<T, NB>(pr, G, srho);
-    reduce_partials<double, NB>(pb, G, srr);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int any = 0;
-      for (int k = 0; k < NB; ++k) {
-        if (!st->active[k]) continue;
-        st->its[k] += 1;
-        st->rr[k] = srr[k];
-        if (!(srr[k] > st->tol2[k])) {
-          st->active[k] = 0;  // converged (or NaN residual: flagged below)
-          if (!isfinite(srr[k])) st->code[k] = 2;
-        } else if (st->its[k] >= maxit) {
-          st->active[k] = 0;
-          st->code[k] = 1;
-        } else if (!s_finite(srho[k]) || s_isnull(srho[k])) {
-          st->active[k] = 0;
-          st->code[k] = 2;
-        } else {
-          st->beta[k] = s_div(srho[k], st->rho[k]);
-          st->rho[k] = srho[k];
-        }
-        any |= st->active[k];
-      }
-      st->iter += 1;
-      if (!any) st->done = 1;
-    }
-  }
+  const CgPart<T, NB> po = cg_part<T, NB>(red, gridDim.x, c);
+  block_reduce_store<T, NB>(rho, po.rz);
+  block_reduce_store_d<NB>(rr, po.rr);
 }
 
 template <typename T, int NB>
@@ -644,7 +756,7 @@ int carve(irk_ctx* ctx, int64_t m, int nb, Workspace<T>& w, int64_t pad = 0) {
   size_t vec = (size_t)m * nb * sizeof(T);
   vec = (vec + 255) & ~(size_t)255;
   size_t pb = ((size_t)pad * nb * sizeof(T) + 255) & ~(size_t)255;
-  size_t head = (sizeof(SysState<T>) + 255) & ~(size_t)255;
+  size_t head = (2 * sizeof(SysState<T>) + 255) & ~(size_t)255;  // st[0], st[1]
   IRK_TRY(ensure_work(ctx, head + 7 * vec + 6 * pb));
   char* b = ctx->work;
   w.st = reinterpret_cast<SysState<T>*>(b);
@@ -675,92 +787,119 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   }
   IRK_TRY(carve<T>(ctx, m, NB, w, pad));
   const int G = grid_for(ctx, m, kBlock, 4);
-  IRK_TRY(ensure_red(ctx, (size_t)G * NB * 4 + 64));
-  IRK_TRY(ensure_pinned(ctx, 2 * sizeof(SysState<T>) + 64));
+  IRK_TRY(ensure_red(ctx, 2 * cg_part_doubles<T, NB>(G) + (size_t)G * NB * 4 + 64));
+  IRK_TRY(ensure_pinned(ctx, 4 * sizeof(SysState<T>) + 64));
   cudaStream_t s = ctx->stream;
   unsigned int* cnt = ctx->counters + 4;
+  SysState<T>* st0 = w.st;
+  SysState<T>* st1 = w.st + 1;
+  // init: state "before iteration 0" in st[1]; its partials go past the
+  // two iteration partial buffers
+  double* red = ctx->red;
   k_cg_init<T, NB, HASB><<<G, kBlock, 0, s>>>(m, A, P, shift, mask, rhs, ld_rhs, w.x, w.r, w.z,
-                                              w.p0, w.dinv, rtol * rtol, atol * atol, w.st,
-                                              ctx->red, cnt);
+                                              w.p0, w.dinv, rtol * rtol, atol * atol, st1,
+                                              red + 2 * cg_part_doubles<T, NB>(G), cnt);
   IRK_CHECK_LAUNCH(ctx);
-  SysState<T>* hst[2] = {reinterpret_cast<SysState<T>*>(ctx->pinned),
-                         reinterpret_cast<SysState<T>*>(ctx->pinned) + 1};
-  // Chunked issue with one chunk in flight ahead of the host check.
+  // pinned mirrors: two polls in flight, each of both states
+  SysState<T>* hst = reinterpret_cast<SysState<T>*>(ctx->pinned);
   const int chunk = m < 65536 ? 8 : 16;
   constexpr bool kStencil = NB == 1 && sizeof(T) == 8 && MAXW > 0;
   static const bool stencil_off = getenv("IRK_NO_STENCIL") != nullptr;
   const bool stencil = kStencil && !stencil_off && w.pad > 0 && m < INT_MAX / 2 &&
                        (A.sw == 3 || A.sw == 5 || A.sw == 7 || A.sw == 9);
-  int issued = 0, c = 0;
   T* pbuf[2] = {w.p0, w.p1};
-  // one chunk = `n` iterations starting at parity `par` of the p buffers
-  auto chunk_body = [&](cudaStream_t cs, int n, int par) -> int {
-    for (int t = 0; t < n; ++t) {
-      T* pold = pbuf[(par + t) & 1];
-      T* pnew = pbuf[(par + t + 1) & 1];
-      if constexpr (kStencil) {
-        if (stencil) {
-          const double* zz = reinterpret_cast<const double*>(w.z);
-          const double* po = reinterpret_cast<const double*>(pold);
-          double* pn = reinterpret_cast<double*>(pnew);
-          double* qq = reinterpret_cast<double*>(w.q);
-          const SysParams<double>& Pd = reinterpret_cast<const SysParams<double>&>(P);
-          SysState<double>* sd = reinterpret_cast<SysState<double>*>(w.st);
-#define IRK_ST(WW)                                                                           \
-  k_cg_spmv_st<WW, HASB><<<G, kBlock, 0, cs>>>((int)m, A, Pd, shift, mask, zz, po, pn, qq, sd, \
-                                              ctx->red, cnt)
-          if (A.sw == 7) IRK_ST(7);
-          else if (A.sw == 9) IRK_ST(9);
-          else if (A.sw == 5) IRK_ST(5);
-          else IRK_ST(3);
+  // kernel A of iteration `it` (first: iteration 0, state from the init)
+  auto launch_a = [&](cudaStream_t cs, int it, int first) -> int {
+    const int c = it & 1;
+    T* pold = pbuf[c];
+    T* pnew = pbuf[c ^ 1];
+    SysState<T>* sin = c ? st0 : st1;
+    SysState<T>* sout = c ? st1 : st0;
+    if constexpr (kStencil) {
+      if (stencil) {
+        const double* zz = reinterpret_cast<const double*>(w.z);
+        const double* po = reinterpret_cast<const double*>(pold);
+        double* pn = reinterpret_cast<double*>(pnew);
+        double* qq = reinterpret_cast<double*>(w.q);
+        const SysParams<double>& Pd = reinterpret_cast<const SysParams<double>&>(P);
+        const SysState<double>* si = reinterpret_cast<const SysState<double>*>(sin);
+        SysState<double>* so = reinterpret_cast<SysState<double>*>(sout);
+#define IRK_ST(WW)                                                                            \
+  k_cg_spmv_st<WW, HASB><<<G, kBlock, 0, cs>>>((int)m, A, Pd, shift, mask, zz, po, pn, qq, si, \
+                                              so, red, c, first, maxit)
+        if (A.sw == 7) IRK_ST(7);
+        else if (A.sw == 9) IRK_ST(9);
+        else if (A.sw == 5) IRK_ST(5);
+        else IRK_ST(3);
 #undef IRK_ST
-        }
       }
-      if (!stencil)
-        k_cg_spmv<T, NB, HASB, MAXW><<<G, kBlock, 0, cs>>>(m, A, P, shift, mask, w.z, pold,
-                                                           pnew, w.q, w.st, ctx->red, cnt);
-      IRK_CHECK_LAUNCH(ctx);
-      k_cg_update<T, NB><<<G, kBlock, 0, cs>>>(m, pnew, w.q, w.dinv, w.x, w.r, w.z, maxit, w.st,
-                                               ctx->red, cnt);
-      IRK_CHECK_LAUNCH(ctx);
+    }
+    if (!stencil)
+      k_cg_spmv<T, NB, HASB, MAXW><<<G, kBlock, 0, cs>>>(m, A, P, shift, mask, w.z, pold, pnew,
+                                                         w.q, sin, sout, red, c, first, maxit);
+    IRK_CHECK_LAUNCH(ctx);
+    return IRK_OK;
+  };
+  auto launch_b = [&](cudaStream_t cs, int it) -> int {
+    const int c = it & 1;
+    k_cg_update<T, NB><<<G, kBlock, 0, cs>>>(m, pbuf[c ^ 1], w.q, w.dinv, w.x, w.r, w.z,
+                                             c ? st1 : st0, red, c);
+    IRK_CHECK_LAUNCH(ctx);
+    return IRK_OK;
+  };
+  // iterations [it0, it0 + n)
+  auto chunk_body = [&](cudaStream_t cs, int it0, int n) -> int {
+    for (int t = 0; t < n; ++t) {
+      IRK_TRY(launch_a(cs, it0 + t, 0));
+      IRK_TRY(launch_b(cs, it0 + t));
     }
     return IRK_OK;
   };
-  // full chunks replay a cached CUDA graph (host launch cost is paid once
-  // per chunk instead of per kernel); the key holds every launch argument
+  // Chunked issue with one chunk in flight ahead of the host check; full
+  // chunks replay a cached CUDA graph (host launch cost once per chunk).
+  // The key holds every launch argument (iteration parity included).
   GraphKey key;
   key.add((const void*)&k_cg_spmv<T, NB, HASB, MAXW>).add((const void*)&k_cg_update<T, NB>);
   key.add(stencil);
-  key.add(m).add(G).add(A).add(P).add(shift).add(mask).add(w).add(ctx->red).add(cnt);
+  key.add(m).add(G).add(A).add(P).add(shift).add(mask).add(w).add(red);
   key.add(maxit).add(chunk);
+  int issued = 0, poll = 0;
+  if (maxit > 0) {
+    IRK_TRY(launch_a(s, 0, 1));
+    IRK_TRY(launch_b(s, 0));
+    issued = 1;
+  }
   for (;;) {
+    if (issued >= maxit) break;
     if (issued + chunk <= maxit) {
-      const int par = issued & 1;
       GraphKey kp = key;
-      kp.add(par);
-      IRK_TRY(graph_launch(ctx, kp.k, [&](cudaStream_t cs) { return chunk_body(cs, chunk, par); }));
+      kp.add(issued & 1);
+      const int it0 = issued;
+      IRK_TRY(graph_launch(ctx, kp.k, [&](cudaStream_t cs) { return chunk_body(cs, it0, chunk); }));
       issued += chunk;
     } else {
-      IRK_TRY(chunk_body(s, maxit - issued, issued & 1));
+      IRK_TRY(chunk_body(s, issued, maxit - issued));
       issued = maxit;
     }
-    IRK_CUDA(cudaMemcpyAsync(hst[c & 1], w.st, sizeof(SysState<T>), cudaMemcpyDeviceToHost, s));
-    IRK_CUDA(cudaEventRecord(ctx->ev[c & 1], s));
-    if (issued >= maxit) {
-      IRK_CUDA(cudaEventSynchronize(ctx->ev[c & 1]));
-      break;
+    SysState<T>* hp = hst + 2 * (poll & 1);
+    IRK_CUDA(cudaMemcpyAsync(hp, w.st, 2 * sizeof(SysState<T>), cudaMemcpyDeviceToHost, s));
+    IRK_CUDA(cudaEventRecord(ctx->ev[poll & 1], s));
+    if (poll > 0) {
+      IRK_CUDA(cudaEventSynchronize(ctx->ev[(poll - 1) & 1]));
+      const SysState<T>* hq = hst + 2 * ((poll - 1) & 1);
+      if (hq[0].done || hq[1].done) break;
     }
-    if (c > 0) {
-      IRK_CUDA(cudaEventSynchronize(ctx->ev[(c - 1) & 1]));
-      if (hst[(c - 1) & 1]->done) break;
-    }
-    c++;
+    poll++;
   }
-  IRK_CUDA(cudaMemcpyAsync(hst[0], w.st, sizeof(SysState<T>), cudaMemcpyDeviceToHost, s));
+  // finalising A: applies the decisions of the last issued iteration (cap)
+  IRK_TRY(launch_a(s, issued, issued == 0 ? 1 : 0));
+  IRK_CUDA(cudaMemcpyAsync(hst, w.st, 2 * sizeof(SysState<T>), cudaMemcpyDeviceToHost, s));
   k_cg_store<T, NB><<<grid_for(ctx, m), kBlock, 0, s>>>(m, w.x, xout, ld_x);
   IRK_CHECK_LAUNCH(ctx);
   IRK_CUDA(cudaStreamSynchronize(s));
-  const SysState<T>& fs = *hst[0];
+  // the latest state: the finished one (or the later iteration)
+  const SysState<T>& fs = (hst[0].done != hst[1].done) ? (hst[0].done ? hst[0] : hst[1])
+                          : (hst[0].iter >= hst[1].iter ? hst[0] : hst[1]);
   int status = IRK_OK;
   for (int k = 0; k < NB; ++k) {
     if (its_host) its_host[k] = fs.its[k];
