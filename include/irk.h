@@ -294,6 +294,23 @@ int irk_semilinear_residual(irk_ctx* ctx, int s, const double* A_host, double dt
                             const double* X_dev, const double* F_dev,
                             const uint8_t* rowmask_dev, double* R_dev, double* D_dev);
 
+/* ---- finite-element load vectors and error norms (SURVEY §8 f) ---------
+ * Structured grids of the manufactured-solution problems: dim 1 (P1
+ * intervals) or 2 (Q1 squares), N cells per direction, 2-point Gauss rule
+ * per direction (problems.py:158-191).  Quadrature data are q-major:
+ * value at point q of element e at [q*nelem + e].  */
+/* out = (f, phi_v) element by element, in the reference's accumulation
+ * order (assemble_load, problems.py:194-202): bitwise equal for equal f. */
+int irk_fe_load(irk_ctx* ctx, int dim, int64_t N, const double* f_dev, double* out_dev);
+/* f at the quadrature points of the built-in manufactured solutions:
+ * kind 1 = heat_mms_1d, 2 = heat_mms_2d (problems.py:113-149). */
+int irk_fe_mms_forcing(irk_ctx* ctx, int kind, int64_t N, double t, double* f_dev);
+/* sum_q w_q sum_e [(u_h - uex)^2 + |grad u_h - gex|^2] (gradient part when
+ * gex_dev != NULL, layout [(q*dim + d)*nelem + e]; uex_dev NULL = 0):
+ * squared l2_error / h1_error (problems.py:205-232).  Synchronous. */
+int irk_fe_error_sq(irk_ctx* ctx, int dim, int64_t N, const double* u_dev, const double* uex_dev,
+                    const double* gex_dev, double* result_host);
+
 #ifdef __cplusplus
 }
 #endif

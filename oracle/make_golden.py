@@ -6,6 +6,7 @@ seeded inputs.  The fixtures pin both the CPU oracle (oracle/irk_oracle.py)
 and, on the GPU box, the CUDA path.
 
   python oracle/make_golden.py small          # seconds: unit + small trajectories
+  python oracle/make_golden.py mms            # seconds: MMS loads / norms / CLI sweeps
   python oracle/make_golden.py full K [K...]  # full-size config sketches (minutes-hours)
 
 Pieces the reference lacks are fed to it from the oracle (P1 matrices,
@@ -255,11 +256,63 @@ def make_full(k):
     print("wrote", GOLDEN / f"full_config{k}.npz", f"{time.time() - t0:.1f}s")
 
 
+def make_mms():
+    """Manufactured-solution layer (SURVEY §8 f rows 2-3): the reference's
+    load vectors, error norms, an MMS trajectory and its CLI sweeps."""
+    irk = ref()
+    import tempfile
+
+    from implicitrk import cli as rcli
+
+    out = {}
+    t = 0.3
+    for dim, n in ((1, 10), (2, 8)):
+        grid = irk.StructuredGrid(dim, n)
+        mms = irk.heat_mms_2d() if dim == 2 else irk.heat_mms_1d()
+        out[f"load{dim}d"] = irk.assemble_load(grid, mms.f, t)
+        uh = irk.interpolate(grid, mms.u, t)
+        uh = uh + 0.01 * np.random.default_rng(5 + dim).standard_normal(uh.shape)
+        out[f"uh{dim}d"] = uh
+        out[f"l2_{dim}d"] = irk.l2_error(grid, uh, mms.u, t)
+        out[f"h1_{dim}d"] = irk.h1_error(grid, uh, mms.u, mms.grad, t)
+        out[f"norm_{dim}d"] = irk.fe_l2_norm(grid, uh)
+    # MMS trajectory through the reference stepper (2D Q1, RadauIIA(2), rana-ld)
+    grid = irk.StructuredGrid(2, 8)
+    prob = irk.mms_heat_problem(grid)
+    st = irk.TimeStepper(prob, irk.radau_iia(2), 0.1, krylov=irk.KrylovSettings(rtol=1e-12),
+                         pc_kind=irk.PreconditionerKind.RANA_LD)
+    u, _ = irk.advance(st, prob, 0.5)
+    out["mms_u"] = u
+    mms = irk.heat_mms_2d()
+    out["mms_l2"] = irk.l2_error(grid, u, mms.u, 0.5)
+    out["mms_h1"] = irk.h1_error(grid, u, mms.u, mms.grad, 0.5)
+    # CLI: spatial convergence sweep and the DAE/ODE boundary contrast
+    with tempfile.TemporaryDirectory() as td:
+        rc = rcli.main(["converge", "--mode", "spatial", "--n-list", "4", "8", "--tfinal", "0.2",
+                        "--rtol", "1e-12", "--out", f"{td}/conv.csv"])
+        assert rc == 0
+        out["cli_converge"] = np.loadtxt(f"{td}/conv.csv", delimiter=",", skiprows=1)
+        rc = rcli.main(["converge", "--mode", "temporal", "--problem", "dahlquist",
+                        "--dt-list", "0.2", "0.1", "--tfinal", "1.0", "--out", f"{td}/temp.csv"])
+        assert rc == 0
+        out["cli_temporal"] = np.genfromtxt(f"{td}/temp.csv", delimiter=",", skip_header=1)
+        rc = rcli.main(["bc-compare", "--nx", "6", "--dt", "0.1", "--tfinal", "0.3",
+                        "--rtol", "1e-12", "--out", f"{td}/bc"])
+        assert rc == 0
+        out["cli_dae"] = np.loadtxt(f"{td}/bc/daenorm.csv", delimiter=",", skiprows=1)
+        out["cli_ode"] = np.loadtxt(f"{td}/bc/odenorm.csv", delimiter=",", skiprows=1)
+    GOLDEN.mkdir(parents=True, exist_ok=True)
+    np.savez_compressed(GOLDEN / "reference_mms.npz", **out)
+    print("wrote", GOLDEN / "reference_mms.npz")
+
+
 if __name__ == "__main__":
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
     if what == "small":
         make_small()
+    elif what == "mms":
+        make_mms()
     else:
         for k in map(int, sys.argv[2:]):
             make_full(k)

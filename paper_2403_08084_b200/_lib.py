@@ -80,6 +80,9 @@ _SIGS = {
                       _int],
     "irk_semilinear_residual": [_vp, _int, _vp, _dbl, _vp, _vp, _dbl, _int, _vp, _vp, _vp, _vp,
                                 _vp, _vp, _vp],
+    "irk_fe_load": [_vp, _int, _i64, _vp, _vp],
+    "irk_fe_mms_forcing": [_vp, _int, _i64, _dbl, _vp],
+    "irk_fe_error_sq": [_vp, _int, _i64, _vp, _vp, _vp, _vp],
 }
 _RESTYPES = {
     "irk_last_error": C.c_char_p,

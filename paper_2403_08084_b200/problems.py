@@ -22,7 +22,7 @@ import ctypes as C
 import numpy as np
 
 from . import sparsela as la
-from ._lib import call, ctx
+from ._lib import call, ctx, ptr
 from .bcs import DirichletBC
 from .sparsela import SparseMatrix
 from .stepper import SemidiscreteProblem, SemilinearForm, zero_load
@@ -98,6 +98,177 @@ def interpolate(grid: StructuredGrid, fn: Callable, t: float) -> np.ndarray:
     """Vertex interpolant of fn(t, x[, y[, z]])."""
     X = grid.coords()
     return np.asarray(fn(t, *(X[:, d] for d in range(grid.dim))), dtype=float)
+
+
+# ------------------------------------------- manufactured solutions (MMS)
+# SURVEY §8 f row 3: load vectors and error norms of the forced heat
+# problems, assembled / reduced on the device (libirk irk_fe_*).
+
+_GAUSS2 = ((0.5 - 0.5 / np.sqrt(3.0), 0.5), (0.5 + 0.5 / np.sqrt(3.0), 0.5))
+
+
+@dataclass(frozen=True)
+class ManufacturedSolution:
+    """Exact solution with its time derivative, gradient and forcing
+    f = u_t - Lap u (problems.py:102-111)."""
+
+    dim: int
+    u: Callable
+    u_t: Callable
+    grad: tuple
+    f: Callable
+
+
+def _device_forcing(fn, kind):
+    fn._irk_mms_kind = kind  # evaluated by irk_fe_mms_forcing on the device
+    return fn
+
+
+def heat_mms_2d() -> ManufacturedSolution:
+    """u(t, x, y) = exp(-0.1 t) sin(pi x) cos(pi y) (problems.py:113-129)."""
+
+    def u(t, x, y):
+        return np.exp(-0.1 * t) * np.sin(np.pi * x) * np.cos(np.pi * y)
+
+    def gx(t, x, y):
+        return np.pi * np.exp(-0.1 * t) * np.cos(np.pi * x) * np.cos(np.pi * y)
+
+    def gy(t, x, y):
+        return -np.pi * np.exp(-0.1 * t) * np.sin(np.pi * x) * np.sin(np.pi * y)
+
+    def f(t, x, y):
+        return (2 * np.pi**2 - 0.1) * u(t, x, y)
+
+    return ManufacturedSolution(dim=2, u=u, u_t=lambda t, x, y: -0.1 * u(t, x, y),
+                                grad=(gx, gy), f=_device_forcing(f, 2))
+
+
+def heat_mms_1d() -> ManufacturedSolution:
+    """u(t, x) = exp(-0.1 t) sin(pi x) (problems.py:132-149)."""
+
+    def u(t, x):
+        return np.exp(-0.1 * t) * np.sin(np.pi * x)
+
+    def f(t, x):
+        return (np.pi**2 - 0.1) * u(t, x)
+
+    return ManufacturedSolution(
+        dim=1, u=u, u_t=lambda t, x: -0.1 * u(t, x),
+        grad=(lambda t, x: np.pi * np.exp(-0.1 * t) * np.cos(np.pi * x),),
+        f=_device_forcing(f, 1))
+
+
+def _fe_grid(grid: StructuredGrid):
+    if grid.dim not in (1, 2):
+        raise ValueError("the manufactured-solution problems are 1D (P1) or 2D (Q1)")
+    return grid.n ** grid.dim
+
+
+def _quad_points(grid: StructuredGrid):
+    """Physical quadrature points, one tuple of per-element coordinate arrays
+    per point of the 2-point Gauss rule (xi outer, eta inner;
+    problems.py:171-191)."""
+    h, n = grid.h, grid.n
+    if grid.dim == 1:
+        xl = np.arange(n) * h
+        return [(xl + xi * h,) for xi, _ in _GAUSS2]
+    ex, ey = np.meshgrid(np.arange(n), np.arange(n), indexing="xy")
+    xl, yl = (ex * h).ravel(), (ey * h).ravel()
+    return [(xl + xi * h, yl + eta * h) for xi, _ in _GAUSS2 for eta, _ in _GAUSS2]
+
+
+def _qdata(grid, fns, t):
+    """Device tensor of fn(t, x_q) for every quadrature point q (outer), the
+    functions in `fns` (middle) and elements (inner)."""
+    ne = _fe_grid(grid)
+    cols = []
+    for xq in _quad_points(grid):
+        for fn in fns:
+            v = np.asarray(fn(t, *xq), dtype=np.float64)
+            cols.append(np.broadcast_to(v, (ne,)))
+    return la.to_dev(np.concatenate(cols))
+
+
+def assemble_load_device(grid: StructuredGrid, f: Callable, t: float):
+    """Load vector (f(t, .), phi_j) as a CUDA tensor: the built-in forcings
+    are evaluated on the device, any other callable on the host at the
+    quadrature points; the element accumulation runs on the device in the
+    reference's order (problems.py:194-202)."""
+    ne = _fe_grid(grid)
+    kind = getattr(f, "_irk_mms_kind", 0)
+    if kind == grid.dim:
+        fq = la.dev_empty(ne * 2 ** grid.dim)
+        call("irk_fe_mms_forcing", ctx(), kind, grid.n, float(t), ptr(fq))
+    else:
+        fq = _qdata(grid, (f,), t)
+    out = la.dev_empty(grid.npoints)
+    call("irk_fe_load", ctx(), grid.dim, grid.n, ptr(fq), ptr(out))
+    return out
+
+
+def assemble_load(grid: StructuredGrid, f: Callable, t: float) -> np.ndarray:
+    """Load vector (f(t, .), phi_j) (problems.py:194-202), numpy out."""
+    return la.to_host(assemble_load_device(grid, f, t))
+
+
+def _err_sq(grid, u_h, uex, grads, t):
+    _fe_grid(grid)
+    u = la.to_dev(u_h)
+    ue = _qdata(grid, (uex,), t) if uex is not None else None
+    ge = _qdata(grid, grads, t) if grads is not None else None
+    out = C.c_double()
+    call("irk_fe_error_sq", ctx(), grid.dim, grid.n, ptr(u),
+         ptr(ue) if ue is not None else None, ptr(ge) if ge is not None else None,
+         C.byref(out))
+    return out.value
+
+
+def l2_error(grid: StructuredGrid, u_h, u_exact: Callable, t: float) -> float:
+    """Quadrature L2 norm of u_h - u_exact(t, .) (problems.py:205-212)."""
+    return float(np.sqrt(_err_sq(grid, u_h, u_exact, None, t)))
+
+
+def h1_error(grid: StructuredGrid, u_h, u_exact: Callable, grad_exact: tuple, t: float) -> float:
+    """Full H1 norm of the error, L2 plus gradient part (problems.py:215-232)."""
+    return float(np.sqrt(_err_sq(grid, u_h, u_exact, tuple(grad_exact), t)))
+
+
+def fe_l2_norm(grid: StructuredGrid, u_h) -> float:
+    """L2 norm of a finite-element function (problems.py:235-239)."""
+    return float(np.sqrt(_err_sq(grid, u_h, None, None, 0.0)))
+
+
+def mms_heat_problem(grid: StructuredGrid,
+                     mms: Optional[ManufacturedSolution] = None) -> SemidiscreteProblem:
+    """Heat equation with manufactured forcing (device load assembly) and
+    Dirichlet data from the exact solution on every boundary vertex
+    (problems.py:250-272)."""
+    if mms is None:
+        mms = heat_mms_2d() if grid.dim == 2 else heat_mms_1d()
+    if mms.dim != grid.dim:
+        raise ValueError("manufactured solution dimension mismatch")
+    M, K, bd = assemble_heat(grid)
+    Xb = grid.coords()[bd]
+    args = tuple(Xb[:, d] for d in range(grid.dim))
+    bc = DirichletBC(dofs=bd, g=lambda t: mms.u(t, *args), g_dot=lambda t: mms.u_t(t, *args))
+    return SemidiscreteProblem(
+        m=grid.npoints, mass=M, stiffness=K,
+        load=lambda t: assemble_load_device(grid, mms.f, t),
+        dirichlet=bc, u0=interpolate(grid, mms.u, 0.0), grid=grid,
+        name=f"heat-mms-{grid.dim}d-n{grid.n}")
+
+
+def incompatible_heat_1d(n: int = 10) -> SemidiscreteProblem:
+    """1D heat problem, zero initial data, g = 1 at both ends: the DAE
+    boundary treatment sees the incompatibility, the ODE one (g' = 0) never
+    does (problems.py:275-295)."""
+    grid = StructuredGrid(1, n)
+    M, K, bd = assemble_heat(grid)
+    ones, zeros = np.ones(len(bd)), np.zeros(len(bd))
+    bc = DirichletBC(dofs=bd, g=lambda t: ones, g_dot=lambda t: zeros)
+    return SemidiscreteProblem(m=grid.npoints, mass=M, stiffness=K, load=zero_load(grid.npoints),
+                               dirichlet=bc, u0=np.zeros(grid.npoints), grid=grid,
+                               name=f"heat-incompatible-1d-n{n}")
 
 
 # ------------------------------------------------------- bench problems
