@@ -104,7 +104,6 @@ struct alignas(16) SysState {
   int code[kMaxSys];  // 0 running/converged, 1 maxit, 2 breakdown
   int done;
   int iter;
-  long long trace[16];  // persistent-kernel phase timestamps (diagnostics)
 };
 
 struct MatView {

@@ -43,9 +43,6 @@ struct Pattern {
   // colhdr[q] = d when every lane's column is row + d, else kNonUniform
   // (read sell_col[pos]).
   int* colhdr = nullptr;     // sell_nnz / 32
-  // host copies of each slice's smallest / largest column (halo extents of
-  // the persistent solver's row partitions)
-  std::vector<int> h_cmin, h_cmax;
   // max over slot-uniform slices of the window rows (win_layout); 0 if none
   int win_rows = 0;
   // stencil-aligned ELL patterns: the ellw column offsets of every full row

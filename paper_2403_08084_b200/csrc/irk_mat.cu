@@ -126,34 +126,19 @@ __global__ void k_sell_fill(int64_t nrows, int64_t ncols, const int* __restrict_
 
 // one warp per slice: slot-uniform column offsets
 __global__ void k_colhdr(int64_t nrows, int64_t nslices, const int* __restrict__ slice_ptr,
-                         const int* __restrict__ sell_col, int* __restrict__ colhdr,
-                         int* __restrict__ cmin, int* __restrict__ cmax) {
+                         const int* __restrict__ sell_col, int* __restrict__ colhdr) {
   int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (s >= nslices) return;
   int base = slice_ptr[s], width = (slice_ptr[s + 1] - base) / kSlice;
   int64_t row = s * kSlice + lane;
   bool full = (s + 1) * kSlice <= nrows;
-  int lo = INT_MAX, hi = INT_MIN;
   for (int k = 0; k < width; ++k) {
     const int c = sell_col[base + k * kSlice + lane];
-    if (row < nrows) {
-      lo = min(lo, c);
-      hi = max(hi, c);
-    }
     int off = c - (int)row;
     int off0 = __shfl_sync(0xffffffffu, off, 0);
     bool uni = __all_sync(0xffffffffu, off == off0) && full;
     if (lane == 0) colhdr[base / kSlice + k] = uni ? off0 : kNonUniform;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  if (lane == 0) {
-    cmin[s] = lo;
-    cmax[s] = hi;
   }
 }
 
@@ -287,22 +272,15 @@ int pattern_build_sell(irk_ctx* ctx, Pattern* p) {
   if (ns > 0) {
     int64_t threads = ns * 32;
     int* cm = nullptr;
-    IRK_CUDA(cudaMalloc(&cm, (2 * ns + 1) * sizeof(int)));
+    IRK_CUDA(cudaMalloc(&cm, sizeof(int)));
     k_colhdr<<<(unsigned)((threads + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(
-        p->nrows, ns, p->slice_ptr, p->sell_col, p->colhdr, cm, cm + ns);
+        p->nrows, ns, p->slice_ptr, p->sell_col, p->colhdr);
     IRK_CHECK_LAUNCH(ctx);
-    IRK_CUDA(cudaMemsetAsync(cm + 2 * ns, 0, sizeof(int), ctx->stream));
+    IRK_CUDA(cudaMemsetAsync(cm, 0, sizeof(int), ctx->stream));
     k_win_rows<<<(unsigned)((threads + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(
-        ns, p->slice_ptr, p->colhdr, cm + 2 * ns);
+        ns, p->slice_ptr, p->colhdr, cm);
     IRK_CHECK_LAUNCH(ctx);
-    IRK_CUDA(cudaMemcpyAsync(&p->win_rows, cm + 2 * ns, sizeof(int), cudaMemcpyDeviceToHost,
-                             ctx->stream));
-    p->h_cmin.resize(ns);
-    p->h_cmax.resize(ns);
-    IRK_CUDA(cudaMemcpyAsync(p->h_cmin.data(), cm, ns * sizeof(int), cudaMemcpyDeviceToHost,
-                             ctx->stream));
-    IRK_CUDA(cudaMemcpyAsync(p->h_cmax.data(), cm + ns, ns * sizeof(int), cudaMemcpyDeviceToHost,
-                             ctx->stream));
+    IRK_CUDA(cudaMemcpyAsync(&p->win_rows, cm, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     IRK_CUDA(cudaStreamSynchronize(ctx->stream));
     cudaFree(cm);
     std::vector<int> sp(ns + 1);

@@ -207,6 +207,78 @@ __global__ void __launch_bounds__(kB, 4) spmv_rt(int m, Offs o, int w, const dou
   }
 }
 
+
+// ablation of the library's stencil SpMV main loop (no prologue):
+// F bit0: lane-distributed headers + vote + shuffle (else per-thread header loads)
+//     bit1: fallback path present
+//     bit2: mask load
+template <int F>
+__global__ void __launch_bounds__(kB, 4) spmv_lib(int m, Offs o, const int* __restrict__ colhdr,
+                                                 const double* __restrict__ ua,
+                                                 const int* __restrict__ sell_col,
+                                                 const double* __restrict__ aval,
+                                                 const unsigned char* __restrict__ mask,
+                                                 const double* __restrict__ z,
+                                                 const double* __restrict__ po,
+                                                 double* __restrict__ pn, double* __restrict__ q,
+                                                 double beta, double* part) {
+  constexpr int W = 7;
+  const int lane = threadIdx.x & 31;
+  const int nsl = (m + 31) / 32;
+  const int wstride = gridDim.x * (blockDim.x / 32);
+  double mu = 0.0;
+  for (int sl = (blockIdx.x * blockDim.x + threadIdx.x) / 32; sl < nsl; sl += wstride) {
+    const int row = sl * 32 + lane;
+    const bool valid = row < m;
+    const int q0 = sl * W;
+    double pr = z[row] + beta * po[row];
+    const bool flagged = (F & 4) ? (valid && mask[row]) : false;
+    double ps[W];
+#pragma unroll
+    for (int kk = 0; kk < W; ++kk) {
+      const int c = row + o.d[kk];
+      ps[kk] = z[c] + beta * po[c];
+    }
+    double acc = 0.0;
+    if (F & 1) {
+      const bool hl = lane < W;
+      const int hd = hl ? __ldg(colhdr + q0 + lane) : 0;
+      const double ha = hl ? __ldg(ua + q0 + lane) : 0.0;
+      const bool ok = __all_sync(0xffffffffu, !hl || (hd == o.d[lane < W ? lane : 0] && !isnan(ha)));
+      if (ok) {
+#pragma unroll
+        for (int kk = 0; kk < W; ++kk) acc += __shfl_sync(0xffffffffu, ha, kk) * ps[kk];
+      } else if ((F & 2) && valid) {
+        const int base = sl * 32 * W;
+#pragma unroll
+        for (int kk = 0; kk < W; ++kk) {
+          const int pos = base + kk * 32 + lane;
+          const int c = sell_col[pos];
+          acc += aval[pos] * (z[c] + beta * po[c]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < W; ++kk) acc += __ldg(ua + q0 + kk) * ps[kk];
+    }
+    if (flagged) acc = pr;
+    if (valid) {
+      pn[row] = pr;
+      q[row] = acc;
+      mu += pr * acc;
+    }
+  }
+  __shared__ double red[8];
+  mu = wsum(mu);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mu;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0;
+    for (int w2 = 0; w2 < 8; ++w2) a += red[w2];
+    part[blockIdx.x] = a;
+  }
+}
+
 int main() {
   const int n1 = 1025, m = n1 * n1;
   int sms;
@@ -276,6 +348,28 @@ int main() {
     cudaMemset(zp, 0, (size_t)m * 16);
     int G = sms * 4;
     timeit("spmv rt-offsets separate", [&](cudaStream_t st) { spmv_rt<0><<<G, kB, 0, st>>>(m, o, 7, hv, v[5], v[0], zp, v[6], v[1], 0.5, part); });
+    int* colhdr; double* ua; int* scol; double* aval; unsigned char* msk;
+    {
+      int ns = (m + 31) / 32;
+      std::vector<int> h((size_t)ns * 7);
+      std::vector<double> hv((size_t)ns * 7);
+      for (int q0 = 0; q0 < ns; ++q0) for (int k = 0; k < 7; ++k) { h[(size_t)q0 * 7 + k] = o.d[k]; hv[(size_t)q0 * 7 + k] = 0.1 * k; }
+      cudaMalloc(&colhdr, h.size() * 4); cudaMemcpy(colhdr, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
+      cudaMalloc(&ua, hv.size() * 8); cudaMemcpy(ua, hv.data(), hv.size() * 8, cudaMemcpyHostToDevice);
+      cudaMalloc(&scol, (size_t)ns * 32 * 7 * 4); cudaMemset(scol, 0, (size_t)ns * 32 * 7 * 4);
+      cudaMalloc(&aval, (size_t)ns * 32 * 7 * 8); cudaMemset(aval, 0, (size_t)ns * 32 * 7 * 8);
+      cudaMalloc(&msk, m); cudaMemset(msk, 0, m);
+    }
+    // z / po with halo: use interior pointers of padded buffers
+    double *zb, *pb;
+    cudaMalloc(&zb, (size_t)(m + 4096) * 8); cudaMemset(zb, 0, (size_t)(m + 4096) * 8);
+    cudaMalloc(&pb, (size_t)(m + 4096) * 8); cudaMemset(pb, 0, (size_t)(m + 4096) * 8);
+    double* zz = zb + 2048; double* pp = pb + 2048;
+    timeit("lib F=0 (thread headers)", [&](cudaStream_t st) { spmv_lib<0><<<G, kB, 0, st>>>(m, o, colhdr, ua, scol, aval, msk, zz, pp, v[6], v[1], 0.5, part); });
+    timeit("lib F=1 (vote+shfl)", [&](cudaStream_t st) { spmv_lib<1><<<G, kB, 0, st>>>(m, o, colhdr, ua, scol, aval, msk, zz, pp, v[6], v[1], 0.5, part); });
+    timeit("lib F=3 (vote+fallback)", [&](cudaStream_t st) { spmv_lib<3><<<G, kB, 0, st>>>(m, o, colhdr, ua, scol, aval, msk, zz, pp, v[6], v[1], 0.5, part); });
+    timeit("lib F=7 (vote+fallback+mask)", [&](cudaStream_t st) { spmv_lib<7><<<G, kB, 0, st>>>(m, o, colhdr, ua, scol, aval, msk, zz, pp, v[6], v[1], 0.5, part); });
+    timeit("lib F=4 (thread headers+mask)", [&](cudaStream_t st) { spmv_lib<4><<<G, kB, 0, st>>>(m, o, colhdr, ua, scol, aval, msk, zz, pp, v[6], v[1], 0.5, part); });
     timeit("spmv rt-offsets interleaved", [&](cudaStream_t st) { spmv_rt<1><<<G, kB, 0, st>>>(m, o, 7, hv, v[5], v[0], zp, v[6], v[1], 0.5, part); });
   }
   for (int R : {1024, 2048, 4096}) {
