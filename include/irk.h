@@ -311,6 +311,27 @@ int irk_fe_mms_forcing(irk_ctx* ctx, int kind, int64_t N, double t, double* f_de
 int irk_fe_error_sq(irk_ctx* ctx, int dim, int64_t N, const double* u_dev, const double* uex_dev,
                     const double* gex_dev, double* result_host);
 
+/* ---- geometric multigrid for the P1 stage blocks ------------------------
+ * Replaces the exact block factorisations (sparsela.py:149-191) for blocks
+ * assembled on structured grids: level l is the block re-assembled with
+ * N_l = N_0 / 2^l cells per direction ((N_l+1)^dim rows, identity rows at
+ * masks[l] != 0); prolongation = P1 interpolation on the nested grids,
+ * restriction its transpose, Chebyshev smoothing (nu steps pre/post) and
+ * `ncoarse` Chebyshev steps on the coarsest level.  The handle keeps
+ * pointers to the level matrices and masks (they must outlive it). */
+typedef struct irk_mg irk_mg;
+int irk_mg_create(irk_ctx* ctx, int dim, int nlev, const int64_t* N_host,
+                  const irk_mat* const* A_levels, const uint8_t* const* masks, int nu,
+                  int ncoarse, irk_mg** out);
+int irk_mg_destroy(irk_mg* mg);
+/* z = V(r): one V-cycle from a zero start (r != z). */
+int irk_mg_vcycle(irk_ctx* ctx, irk_mg* mg, const double* r_dev, double* z_dev);
+/* CG on the level-0 block preconditioned by one V-cycle per iteration;
+ * strided rhs/x as irk_pcg; status as irk_pcg. */
+int irk_mg_pcg(irk_ctx* ctx, irk_mg* mg, const double* rhs_dev, int64_t ld_rhs, double* x_dev,
+               int64_t ld_x, double rtol, double atol, int maxit, int* its_host,
+               double* relres_host);
+
 #ifdef __cplusplus
 }
 #endif

@@ -83,6 +83,10 @@ _SIGS = {
     "irk_fe_load": [_vp, _int, _i64, _vp, _vp],
     "irk_fe_mms_forcing": [_vp, _int, _i64, _dbl, _vp],
     "irk_fe_error_sq": [_vp, _int, _i64, _vp, _vp, _vp, _vp],
+    "irk_mg_create": [_vp, _int, _int, _vp, _vp, _vp, _int, _int, _vp],
+    "irk_mg_destroy": [_vp],
+    "irk_mg_vcycle": [_vp, _vp, _vp, _vp],
+    "irk_mg_pcg": [_vp, _vp, _vp, _i64, _vp, _i64, _dbl, _dbl, _int, _vp, _vp],
 }
 _RESTYPES = {
     "irk_last_error": C.c_char_p,

@@ -104,6 +104,7 @@ struct alignas(16) SysState {
   int code[kMaxSys];  // 0 running/converged, 1 maxit, 2 breakdown
   int done;
   int iter;
+  int fresh;  // 1: written by the init kernel, no iteration decided yet
 };
 
 struct MatView {
@@ -345,6 +346,7 @@ __global__ void __launch_bounds__(kBlock)
       }
       st->done = any ? 0 : 1;
       st->iter = 0;
+      st->fresh = 1;
     }
   }
 }
@@ -389,20 +391,20 @@ __device__ __forceinline__ void state_copy(SysState<T>* dst, const SysState<T>* 
 // Prologue of A_k: returns true when the solve is finished (all threads).
 template <typename T, int NB>
 __device__ __forceinline__ bool cg_enter_a(const SysState<T>* sin, SysState<T>* sout,
-                                           double* red, int c, int first, int maxit,
+                                           double* red, int c, int maxit,
                                            T (&beta)[NB], bool (&act)[NB]) {
   __shared__ SysState<T> S;
   __shared__ T smu[NB], srz[NB];
   __shared__ double srr[NB];
   const int G = gridDim.x;
   state_copy(&S, sin);
-  if (!first) {
-    // issued together with the state loads; reduce_partials3 synchronises
+  {
+    // issued together with the state loads (unused when the state is fresh
+    // from the init kernel); reduce_partials3 synchronises
     const CgPart<T, NB> pin = cg_part<T, NB>(red, G, c ^ 1);
     reduce_partials3<T, NB>(pin.mu, pin.rz, pin.rr, G, smu, srz, srr);
-  } else {
-    __syncthreads();
   }
+  const bool first = S.fresh != 0;
   if (S.done) {
     if (blockIdx.x == 0) {
       constexpr int nw = sizeof(SysState<T>) / 4;
@@ -443,8 +445,9 @@ __device__ __forceinline__ bool cg_enter_a(const SysState<T>* sin, SysState<T>* 
       S.iter += 1;
       S.done = any ? 0 : 1;
     }
-    __syncthreads();
   }
+  if (threadIdx.x == 0) S.fresh = 0;
+  __syncthreads();
 #pragma unroll
   for (int k = 0; k < NB; ++k) {
     beta[k] = S.beta[k];
@@ -490,11 +493,10 @@ __global__ void __launch_bounds__(kBlock, 4)
     k_cg_spmv(int64_t m, MatView A, const SysParams<T> P, const double* __restrict__ shift,
               const uint8_t* __restrict__ mask, const T* __restrict__ z,
               const T* __restrict__ pold, T* __restrict__ pnew, T* __restrict__ q,
-              const SysState<T>* sin, SysState<T>* sout, double* red, int c, int first,
-              int maxit) {
+              const SysState<T>* sin, SysState<T>* sout, double* red, int c, int maxit) {
   T beta[NB];
   bool act[NB];
-  if (cg_enter_a<T, NB>(sin, sout, red, c, first, maxit, beta, act)) return;
+  if (cg_enter_a<T, NB>(sin, sout, red, c, maxit, beta, act)) return;
   T mu[NB];
 #pragma unroll
   for (int k = 0; k < NB; ++k) mu[k] = s_zero(T{});
@@ -592,10 +594,10 @@ __global__ void __launch_bounds__(kBlock, 4)
                  const uint8_t* __restrict__ mask, const double* __restrict__ z,
                  const double* __restrict__ pold, double* __restrict__ pnew,
                  double* __restrict__ q, const SysState<double>* sin, SysState<double>* sout,
-                 double* red, int cpar, int first, int maxit) {
+                 double* red, int cpar, int maxit) {
   double betas[1];
   bool acts[1];
-  if (cg_enter_a<double, 1>(sin, sout, red, cpar, first, maxit, betas, acts)) return;
+  if (cg_enter_a<double, 1>(sin, sout, red, cpar, maxit, betas, acts)) return;
   const double beta = betas[0];
   const bool act = acts[0];
   const int lane = threadIdx.x & 31;
@@ -651,7 +653,9 @@ __global__ void __launch_bounds__(kBlock, 4)
 
 // x += alpha p, r -= alpha q, z = D^-1 r; partials of rho' = r^T z and
 // rr = ||r||^2 (the next A kernel decides convergence / cap / beta).
-template <typename T, int NB>
+// EXTZ: an external preconditioner forms z (and the r.z partials) after
+// this kernel; only x, r and ||r||^2 are updated here.
+template <typename T, int NB, bool EXTZ = false>
 __global__ void __launch_bounds__(kBlock)
     k_cg_update(int64_t m, const T* __restrict__ p, const T* __restrict__ q,
                 const T* __restrict__ dinv, T* __restrict__ x, T* __restrict__ r,
@@ -684,7 +688,7 @@ __global__ void __launch_bounds__(kBlock)
             const int64_t qi = row * NB + k;
             pk[u][k] = p[qi];
             qk[u][k] = q[qi];
-            dk[u][k] = dinv[qi];
+            dk[u][k] = EXTZ ? s_zero(T{}) : dinv[qi];
             xk[u][k] = x[qi];
             rk[u][k] = r[qi];
           }
@@ -700,9 +704,11 @@ __global__ void __launch_bounds__(kBlock)
             x[qi] = s_add(xk[u][k], s_mul(alpha[k], pk[u][k]));
             T rn = s_sub(rk[u][k], s_mul(alpha[k], qk[u][k]));
             r[qi] = rn;
-            T zn = s_mul(dk[u][k], rn);
-            z[qi] = zn;
-            rho[k] = s_add(rho[k], s_mul(rn, zn));
+            if (!EXTZ) {
+              T zn = s_mul(dk[u][k], rn);
+              z[qi] = zn;
+              rho[k] = s_add(rho[k], s_mul(rn, zn));
+            }
             rr[k] += s_abs2(rn);
           }
         }
@@ -718,17 +724,78 @@ __global__ void __launch_bounds__(kBlock)
         x[qi] = s_add(x[qi], s_mul(alpha[k], pk));
         T rk = s_sub(r[qi], s_mul(alpha[k], q[qi]));
         r[qi] = rk;
-        T zk = s_mul(dinv[qi], rk);
-        z[qi] = zk;
-        rho[k] = s_add(rho[k], s_mul(rk, zk));
+        if (!EXTZ) {
+          T zk = s_mul(dinv[qi], rk);
+          z[qi] = zk;
+          rho[k] = s_add(rho[k], s_mul(rk, zk));
+        }
         rr[k] += s_abs2(rk);
       }
     }
   }
   const CgPart<T, NB> po = cg_part<T, NB>(red, gridDim.x, c);
-  block_reduce_store<T, NB>(rho, po.rz);
+  if (!EXTZ) block_reduce_store<T, NB>(rho, po.rz);
   block_reduce_store_d<NB>(rr, po.rr);
 }
+
+// r.z partials of iteration parity c after an external preconditioner
+// (real, one system).  Same grid as the A/B kernels.
+static __global__ void __launch_bounds__(kBlock)
+    k_cg_dot_rz(int64_t m, const double* __restrict__ r, const double* __restrict__ z,
+                double* red, int c) {
+  double v = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v += r[i] * z[i];
+  double vs[1] = {v};
+  block_reduce_store<double, 1>(vs, cg_part<double, 1>(red, gridDim.x, c).rz);
+}
+
+// After the init kernel: rho = r.z for an external preconditioner's z
+// (last-block reduction, once per solve); breakdown ends the solve.
+static __global__ void __launch_bounds__(kBlock)
+    k_cg_rho_init(int64_t m, const double* __restrict__ r, const double* __restrict__ z,
+                  SysState<double>* st, double* part, unsigned int* counter) {
+  double v = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v += r[i] * z[i];
+  double vs[1] = {v};
+  block_reduce_store<double, 1>(vs, part);
+  if (last_block_inner(counter)) {
+    __shared__ double srho[1];
+    reduce_partials<double, 1>(part, gridDim.x, srho);
+    if (threadIdx.x == 0 && !st->done) {
+      st->rho[0] = srho[0];
+      if (st->active[0] && (!isfinite(srho[0]) || srho[0] == 0.0)) {
+        st->active[0] = 0;
+        st->code[0] = 2;
+        st->done = 1;
+      }
+    }
+  }
+}
+
+// Loop condition of the graph-resident CG loop: continue while neither
+// state buffer is finished.
+template <typename T>
+__global__ void k_cg_cond(cudaGraphConditionalHandle h, const SysState<T>* a,
+                          const SysState<T>* b) {
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    cudaGraphSetConditional(h, (__ldcg(&a->done) || __ldcg(&b->done)) ? 0u : 1u);
+}
+
+// External preconditioner z = P^-1 r for the real one-system CG (the
+// geometric multigrid of irk_mg.cu): a fixed, graph-capturable kernel
+// sequence on the given stream.
+struct CgPrec {
+  uint64_t uid = 0;  // unique per instance (graph-cache key; addresses get reused)
+  // stop: device flag; when nonzero at run time the kernels do nothing (the
+  // solve finished inside a graph-resident loop)
+  virtual int apply(irk_ctx* ctx, cudaStream_t s, const double* r, double* z,
+                    const int* stop) = 0;
+  virtual ~CgPrec() {}
+};
 
 template <typename T, int NB>
 __global__ void k_cg_store(int64_t m, const T* __restrict__ x, T* __restrict__ out,
@@ -777,7 +844,9 @@ int carve(irk_ctx* ctx, int64_t m, int nb, Workspace<T>& w, int64_t pad = 0) {
 template <typename T, int NB, bool HASB, int MAXW>
 int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, const double* shift,
            const uint8_t* mask, const T* rhs, int64_t ld_rhs, T* xout, int64_t ld_x, double rtol,
-           double atol, int maxit, int* its_host, double* relres_host) {
+           double atol, int maxit, int* its_host, double* relres_host, CgPrec* prec = nullptr) {
+  constexpr bool kExtOk = NB == 1 && sizeof(T) == 8;
+  IRK_REQUIRE(!prec || kExtOk, "run_cg: external preconditioner needs one real system");
   Workspace<T> w;
   int64_t pad = 0;
   if (NB == 1 && sizeof(T) == 8 && A.sw > 0) {
@@ -799,6 +868,16 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
                                               w.p0, w.dinv, rtol * rtol, atol * atol, st1,
                                               red + 2 * cg_part_doubles<T, NB>(G), cnt);
   IRK_CHECK_LAUNCH(ctx);
+  if constexpr (kExtOk) {
+    if (prec) {
+      double* rr_ = reinterpret_cast<double*>(w.r);
+      double* zz_ = reinterpret_cast<double*>(w.z);
+      IRK_TRY(prec->apply(ctx, s, rr_, zz_, nullptr));
+      k_cg_rho_init<<<G, kBlock, 0, s>>>(m, rr_, zz_, reinterpret_cast<SysState<double>*>(st1),
+                                         red + 2 * cg_part_doubles<T, NB>(G), cnt);
+      IRK_CHECK_LAUNCH(ctx);
+    }
+  }
   // pinned mirrors: two polls in flight, each of both states
   SysState<T>* hst = reinterpret_cast<SysState<T>*>(ctx->pinned);
   const int chunk = m < 65536 ? 8 : 16;
@@ -807,8 +886,9 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   const bool stencil = kStencil && !stencil_off && w.pad > 0 && m < INT_MAX / 2 &&
                        (A.sw == 3 || A.sw == 5 || A.sw == 7 || A.sw == 9);
   T* pbuf[2] = {w.p0, w.p1};
-  // kernel A of iteration `it` (first: iteration 0, state from the init)
-  auto launch_a = [&](cudaStream_t cs, int it, int first) -> int {
+  // kernel A of iteration `it` (parity it & 1; the state says whether it
+  // is the first one after the init)
+  auto launch_a = [&](cudaStream_t cs, int it) -> int {
     const int c = it & 1;
     T* pold = pbuf[c];
     T* pnew = pbuf[c ^ 1];
@@ -825,7 +905,7 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
         SysState<double>* so = reinterpret_cast<SysState<double>*>(sout);
 #define IRK_ST(WW)                                                                            \
   k_cg_spmv_st<WW, HASB><<<G, kBlock, 0, cs>>>((int)m, A, Pd, shift, mask, zz, po, pn, qq, si, \
-                                              so, red, c, first, maxit)
+                                              so, red, c, maxit)
         if (A.sw == 7) IRK_ST(7);
         else if (A.sw == 9) IRK_ST(9);
         else if (A.sw == 5) IRK_ST(5);
@@ -835,12 +915,25 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
     }
     if (!stencil)
       k_cg_spmv<T, NB, HASB, MAXW><<<G, kBlock, 0, cs>>>(m, A, P, shift, mask, w.z, pold, pnew,
-                                                         w.q, sin, sout, red, c, first, maxit);
+                                                         w.q, sin, sout, red, c, maxit);
     IRK_CHECK_LAUNCH(ctx);
     return IRK_OK;
   };
   auto launch_b = [&](cudaStream_t cs, int it) -> int {
     const int c = it & 1;
+    if constexpr (kExtOk) {
+      if (prec) {
+        k_cg_update<T, NB, true><<<G, kBlock, 0, cs>>>(m, pbuf[c ^ 1], w.q, w.dinv, w.x, w.r,
+                                                       w.z, c ? st1 : st0, red, c);
+        IRK_CHECK_LAUNCH(ctx);
+        double* rr_ = reinterpret_cast<double*>(w.r);
+        double* zz_ = reinterpret_cast<double*>(w.z);
+        IRK_TRY(prec->apply(ctx, cs, rr_, zz_, &(c ? st1 : st0)->done));
+        k_cg_dot_rz<<<G, kBlock, 0, cs>>>(m, rr_, zz_, red, c);
+        IRK_CHECK_LAUNCH(ctx);
+        return IRK_OK;
+      }
+    }
     k_cg_update<T, NB><<<G, kBlock, 0, cs>>>(m, pbuf[c ^ 1], w.q, w.dinv, w.x, w.r, w.z,
                                              c ? st1 : st0, red, c);
     IRK_CHECK_LAUNCH(ctx);
@@ -849,49 +942,72 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   // iterations [it0, it0 + n)
   auto chunk_body = [&](cudaStream_t cs, int it0, int n) -> int {
     for (int t = 0; t < n; ++t) {
-      IRK_TRY(launch_a(cs, it0 + t, 0));
+      IRK_TRY(launch_a(cs, it0 + t));
       IRK_TRY(launch_b(cs, it0 + t));
     }
     return IRK_OK;
   };
-  // Chunked issue with one chunk in flight ahead of the host check; full
-  // chunks replay a cached CUDA graph (host launch cost once per chunk).
-  // The key holds every launch argument (iteration parity included).
+  // The key holds every launch argument of the loop kernels.
   GraphKey key;
   key.add((const void*)&k_cg_spmv<T, NB, HASB, MAXW>).add((const void*)&k_cg_update<T, NB>);
   key.add(stencil);
   key.add(m).add(G).add(A).add(P).add(shift).add(mask).add(w).add(red);
-  key.add(maxit).add(chunk);
-  int issued = 0, poll = 0;
-  if (maxit > 0) {
-    IRK_TRY(launch_a(s, 0, 1));
-    IRK_TRY(launch_b(s, 0));
-    issued = 1;
-  }
-  for (;;) {
-    if (issued >= maxit) break;
-    if (issued + chunk <= maxit) {
-      GraphKey kp = key;
-      kp.add(issued & 1);
-      const int it0 = issued;
-      IRK_TRY(graph_launch(ctx, kp.k, [&](cudaStream_t cs) { return chunk_body(cs, it0, chunk); }));
-      issued += chunk;
-    } else {
-      IRK_TRY(chunk_body(s, issued, maxit - issued));
-      issued = maxit;
+  key.add(maxit).add(prec ? prec->uid : (uint64_t)0);
+  static const bool graph_off = getenv("IRK_NO_GRAPH") != nullptr;
+  int64_t body_kernels = 0;  // kernels per pass of the graph-resident loop
+  if (maxit > 0 && !graph_off) {
+    // The whole iteration loop is ONE graph: a conditional WHILE node whose
+    // body runs two iterations (both parities) and then sets the loop
+    // condition from the device state; termination never returns to the
+    // host.  The body's kernels do nothing once the state is finished.
+    GraphKey kw = key;
+    kw.add(1);
+    IRK_TRY(graph_launch_while(
+        ctx, kw.k,
+        [&](cudaStream_t cs, cudaGraphConditionalHandle h) -> int {
+          IRK_TRY(chunk_body(cs, 0, 2));
+          k_cg_cond<T><<<1, 32, 0, cs>>>(h, st0, st1);
+          IRK_CHECK_LAUNCH(ctx);
+          return IRK_OK;
+        },
+        &body_kernels));
+  } else {
+    // Chunked issue with one chunk in flight ahead of the host check; full
+    // chunks replay a cached CUDA graph (host launch cost once per chunk).
+    const int chunk = m < 65536 ? 8 : 16;
+    int issued = 0, poll = 0;
+    if (maxit > 0) {
+      IRK_TRY(launch_a(s, 0));
+      IRK_TRY(launch_b(s, 0));
+      issued = 1;
     }
-    SysState<T>* hp = hst + 2 * (poll & 1);
-    IRK_CUDA(cudaMemcpyAsync(hp, w.st, 2 * sizeof(SysState<T>), cudaMemcpyDeviceToHost, s));
-    IRK_CUDA(cudaEventRecord(ctx->ev[poll & 1], s));
-    if (poll > 0) {
-      IRK_CUDA(cudaEventSynchronize(ctx->ev[(poll - 1) & 1]));
-      const SysState<T>* hq = hst + 2 * ((poll - 1) & 1);
-      if (hq[0].done || hq[1].done) break;
+    for (;;) {
+      if (issued >= maxit) break;
+      if (issued + chunk <= maxit && !graph_off) {
+        GraphKey kp = key;
+        kp.add(issued & 1).add(chunk);
+        const int it0 = issued;
+        IRK_TRY(graph_launch(ctx, kp.k,
+                             [&](cudaStream_t cs) { return chunk_body(cs, it0, chunk); }));
+        issued += chunk;
+      } else {
+        const int n = std::min(chunk, maxit - issued);
+        IRK_TRY(chunk_body(s, issued, n));
+        issued += n;
+      }
+      SysState<T>* hp = hst + 2 * (poll & 1);
+      IRK_CUDA(cudaMemcpyAsync(hp, w.st, 2 * sizeof(SysState<T>), cudaMemcpyDeviceToHost, s));
+      IRK_CUDA(cudaEventRecord(ctx->ev[poll & 1], s));
+      if (poll > 0) {
+        IRK_CUDA(cudaEventSynchronize(ctx->ev[(poll - 1) & 1]));
+        const SysState<T>* hq = hst + 2 * ((poll - 1) & 1);
+        if (hq[0].done || hq[1].done) break;
+      }
+      poll++;
     }
-    poll++;
+    // finalising A: applies the decisions of the last issued iteration (cap)
+    IRK_TRY(launch_a(s, issued));
   }
-  // finalising A: applies the decisions of the last issued iteration (cap)
-  IRK_TRY(launch_a(s, issued, issued == 0 ? 1 : 0));
   IRK_CUDA(cudaMemcpyAsync(hst, w.st, 2 * sizeof(SysState<T>), cudaMemcpyDeviceToHost, s));
   k_cg_store<T, NB><<<grid_for(ctx, m), kBlock, 0, s>>>(m, w.x, xout, ld_x);
   IRK_CHECK_LAUNCH(ctx);
@@ -899,6 +1015,9 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   // the latest state: the finished one (or the later iteration)
   const SysState<T>& fs = (hst[0].done != hst[1].done) ? (hst[0].done ? hst[0] : hst[1])
                           : (hst[0].iter >= hst[1].iter ? hst[0] : hst[1]);
+  // body passes executed by the graph-resident loop: iterations in pairs,
+  // plus the pass in which the finished state was observed
+  if (body_kernels) ctx->launches += body_kernels * ((int64_t)fs.iter / 2 + 1);
   int status = IRK_OK;
   for (int k = 0; k < NB; ++k) {
     if (its_host) its_host[k] = fs.its[k];

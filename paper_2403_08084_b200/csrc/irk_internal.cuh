@@ -184,6 +184,69 @@ int graph_launch(irk_ctx* ctx, const std::string& key, F&& body) {
   return IRK_OK;
 }
 
+// Graph-resident loop: a graph holding one conditional WHILE node whose
+// body is `body(stream, handle)` (captured; the body sets the condition
+// with cudaGraphSetConditional, default 1 at every launch).  Cached like
+// graph_launch; replayed on ctx->stream.
+// *body_kernels (optional) receives the kernel count of one body pass.
+template <class F>
+int graph_launch_while(irk_ctx* ctx, const std::string& key, F&& body,
+                       int64_t* body_kernels = nullptr) {
+  for (auto& g : ctx->graphs) {
+    if (g.key == key) {
+      IRK_CUDA(cudaGraphLaunch(g.exec, ctx->stream));
+      if (body_kernels) *body_kernels = g.kernels;
+      return IRK_OK;
+    }
+  }
+  if (!ctx->cap_stream)
+    IRK_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+  cudaGraph_t graph = nullptr;
+  IRK_CUDA(cudaGraphCreate(&graph, 0));
+  cudaGraphConditionalHandle h;
+  cudaError_t e = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault);
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (e == cudaSuccess) e = cudaGraphAddNode(&node, graph, nullptr, 0, &np);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    IRK_CUDA(e);
+  }
+  cudaGraph_t bodyg = np.conditional.phGraph_out[0];
+  const int64_t l0 = ctx->launches;
+  e = cudaStreamBeginCaptureToGraph(ctx->cap_stream, bodyg, nullptr, nullptr, 0,
+                                    cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    IRK_CUDA(e);
+  }
+  const int rc = body(ctx->cap_stream, h);
+  cudaGraph_t got = nullptr;
+  e = cudaStreamEndCapture(ctx->cap_stream, &got);
+  if (rc != IRK_OK || e != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    if (rc != IRK_OK) return rc;
+    IRK_CUDA(e);
+  }
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  IRK_CUDA(e);
+  if (ctx->graphs.size() >= 64) {
+    cudaGraphExecDestroy(ctx->graphs.front().exec);
+    ctx->graphs.erase(ctx->graphs.begin());
+  }
+  ctx->graphs.push_back({key, exec, ctx->launches - l0});
+  ctx->launches = l0;  // counted per executed body pass by the caller
+  if (body_kernels) *body_kernels = ctx->graphs.back().kernels;
+  IRK_CUDA(cudaGraphLaunch(exec, ctx->stream));
+  return IRK_OK;
+}
+
 inline int grid_for(const irk_ctx* ctx, int64_t work_items, int per_block = kBlock,
                     int blocks_per_sm = 8) {
   int64_t g = (work_items + per_block - 1) / per_block;

@@ -73,8 +73,13 @@ def _assemble(kind: str, grid: StructuredGrid):
         call("irk_mat_assemble_q1", ctx(), grid.n, C.byref(hM), C.byref(hK))
     else:
         call("irk_mat_assemble_p1", ctx(), grid.dim, grid.n, C.byref(hM), C.byref(hK))
-    return (SparseMatrix._from_device(la.DeviceMatrix(hM)),
-            SparseMatrix._from_device(la.DeviceMatrix(hK)))
+    M = SparseMatrix._from_device(la.DeviceMatrix(hM))
+    K = SparseMatrix._from_device(la.DeviceMatrix(hK))
+    if kind == "p1":
+        # nested P1 grids: blocks built from this pair get the geometric
+        # multigrid inner solver (sparsela.BlockFactorization)
+        M._p1_grid = K._p1_grid = (grid.dim, grid.n)
+    return M, K
 
 
 def assemble_heat(grid: StructuredGrid):

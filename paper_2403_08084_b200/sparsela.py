@@ -474,23 +474,100 @@ def as_dev_op(obj, n):
 class BlockSolveSettings:
     """Inner diagonal-block solver (replaces SuperLU, sparsela.py:149-191).
 
-    method: "pcg" (Jacobi-preconditioned CG) or "chebyshev" (Jacobi-Chebyshev,
+    method: "auto" (multigrid-preconditioned CG for blocks of P1 grid
+    operators, Jacobi-PCG otherwise), "mg" (multigrid required), "pcg"
+    (Jacobi-preconditioned CG) or "chebyshev" (Jacobi-Chebyshev,
     ``cheb_iters`` sweeps with Gershgorin/Lanczos-free bounds).
+    mg_nu / mg_coarse_steps: Chebyshev smoothing steps per level and on the
+    coarsest level of the multigrid V-cycle.
     raise_on_maxit: when False (preconditioner use) an unconverged block
     returns its last iterate, FGMRES being flexible."""
 
-    method: str = "pcg"
+    method: str = "auto"
     rtol: float = 1e-6
     atol: float = 0.0
     maxit: int = 20000
     raise_on_maxit: bool = False
     cheb_iters: int = 50
+    mg_nu: int = 2
+    mg_coarse_steps: int = 8
 
     def __post_init__(self):
-        if self.method not in ("pcg", "chebyshev"):
+        if self.method not in ("auto", "pcg", "mg", "chebyshev"):
             raise ValueError(f"unknown block solver {self.method!r}")
         if self.rtol < 0 or self.atol < 0 or self.maxit < 0:
             raise ValueError("block solver tolerances must be non-negative")
+
+
+class _MgHierarchy:
+    """Geometric multigrid levels of a P1 stage block alpha*M + beta*K
+    (libirk irk_mg_*): level l re-assembles the operator with N/2^l cells per
+    direction (nested P1 grids: the Galerkin operator), Dirichlet rows where
+    the coincident fine node is constrained.  Coarsening stops at odd N, at
+    N < 4, or once the level is mass-dominated (beta/(alpha H^2) <= 1/2),
+    where a few Chebyshev steps solve it."""
+
+    def __init__(self, handle, keep):
+        self.handle = handle
+        self._keep = keep  # level matrices and masks referenced by the handle
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.load().irk_mg_destroy(self.handle)
+        except Exception:  # interpreter shutdown
+            pass
+
+    @staticmethod
+    def build(M, K, alpha, beta, mask, B, settings):
+        grid = getattr(M, "_p1_grid", None)
+        if grid is None or getattr(K, "_p1_grid", None) != grid or alpha <= 0 or beta < 0:
+            return None
+        dim, N = grid
+        torch = _torch()
+        n1 = N + 1
+        if mask is not None:
+            # only the full-boundary Dirichlet set (the coarse masks are the
+            # boundaries of the coarse grids)
+            idx = torch.arange(n1 ** dim, device=mask.device)
+            on = torch.zeros_like(idx, dtype=torch.bool)
+            for d in range(dim):
+                k = (idx // n1 ** d) % n1
+                on |= (k == 0) | (k == N)
+            if not torch.equal(on, mask.bool()):
+                return None
+        Ns, mats, masks = [N], [B], [mask]
+        while Ns[-1] % 2 == 0 and Ns[-1] // 2 >= 4 and len(Ns) < 12:
+            H = 1.0 / Ns[-1]
+            if beta / (alpha * H * H) <= 0.5:
+                break
+            Nc = Ns[-1] // 2
+            hM, hK = C.c_void_p(), C.c_void_p()
+            call("irk_mat_assemble_p1", ctx(), dim, Nc, C.byref(hM), C.byref(hK))
+            Mc, Kc = DeviceMatrix(hM), DeviceMatrix(hK)
+            Bc = Mc.combine(alpha, Kc, beta)
+            mc = None
+            if mask is not None:
+                shape = (Ns[-1] + 1,) * dim
+                prev = masks[-1]
+                mc = prev.reshape(shape)[(slice(None, None, 2),) * dim].contiguous().reshape(-1)
+                Bc = Bc.constrain(mc, 1.0)
+            Ns.append(Nc)
+            mats.append(Bc)
+            masks.append(mc)
+        L = len(Ns)
+        Nh = np.ascontiguousarray(Ns, dtype=np.int64)
+        hm = (C.c_void_p * L)(*[A.handle for A in mats])
+        mp = (C.c_void_p * L)(*[ptr(m) if m is not None else None for m in masks])
+        h = C.c_void_p()
+        call("irk_mg_create", ctx(), dim, L, hptr(Nh), C.cast(hm, C.c_void_p),
+             C.cast(mp, C.c_void_p), int(settings.mg_nu), int(settings.mg_coarse_steps),
+             C.byref(h))
+        return _MgHierarchy(h, (mats, masks))
+
+    @property
+    def levels(self):
+        return len(self._keep[0])
 
 
 class BlockFactorization:
@@ -517,6 +594,13 @@ class BlockFactorization:
         self.last_iterations = 0
         self.last_relres = 0.0
         self._check_regular()
+        self._mg = None
+        if self.settings.method in ("auto", "mg"):
+            self._mg = _MgHierarchy.build(M, K, self.alpha, self.beta, self.mask, B,
+                                          self.settings)
+            if self._mg is None and self.settings.method == "mg":
+                raise ValueError("multigrid block solver needs M, K from assemble_p1 "
+                                 "(nested structured-grid P1 operators)")
 
     def _check_regular(self):
         torch = _torch()
@@ -542,10 +626,15 @@ class BlockFactorization:
         its = np.zeros(8, dtype=np.int32)
         rel = np.zeros(8, dtype=np.float64)
         one = np.ones(8)
-        status = _lib.load().irk_pcg(
-            ctx(), 1, hptr(one), C.c_void_p(), self._B.handle, C.c_void_p(), C.c_void_p(),
-            C.c_void_p(), ptr(rhs), int(ld_rhs), ptr(x), int(ld_x), float(st.rtol), float(st.atol),
-            int(st.maxit), hptr(its), hptr(rel))
+        if self._mg is not None and st.method in ("auto", "mg"):
+            status = _lib.load().irk_mg_pcg(
+                ctx(), self._mg.handle, ptr(rhs), int(ld_rhs), ptr(x), int(ld_x),
+                float(st.rtol), float(st.atol), int(st.maxit), hptr(its), hptr(rel))
+        else:
+            status = _lib.load().irk_pcg(
+                ctx(), 1, hptr(one), C.c_void_p(), self._B.handle, C.c_void_p(), C.c_void_p(),
+                C.c_void_p(), ptr(rhs), int(ld_rhs), ptr(x), int(ld_x), float(st.rtol),
+                float(st.atol), int(st.maxit), hptr(its), hptr(rel))
         self.last_iterations = int(its[0])
         self.last_relres = float(rel[0])
         if status == _lib.IRK_ENOCONV:

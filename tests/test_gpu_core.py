@@ -325,3 +325,57 @@ def test_schur_preconditioner_vs_oracle(irk, oracle, tab_name, form):
     S[:, ~keep] = 0
     S[idx, idx] = 1.0
     assert rel(pc.apply(v), np.linalg.solve(S, v)) < 1e-9
+
+
+# ------------------------------------------------------- geometric multigrid
+
+
+def _p1_block(irk, dim, n, alpha, beta):
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(dim, n))
+    st = la.BlockSolveSettings(rtol=1e-12, raise_on_maxit=True)
+    fac = la.BlockFactorization(M, K, alpha, beta, bd, st)
+    return M, K, bd, fac
+
+
+@pytest.mark.gpu
+def test_mg_vcycle_is_symmetric(cuda, irk):
+    from paper_2403_08084_b200 import _lib
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd, fac = _p1_block(irk, 2, 64, 1.0, 2e-3)
+    assert fac._mg is not None and fac._mg.levels >= 3
+    rng = np.random.default_rng(3)
+    a = la.to_dev(rng.standard_normal(M.nrows))
+    b = la.to_dev(rng.standard_normal(M.nrows))
+    va, vb = la.dev_empty(M.nrows), la.dev_empty(M.nrows)
+    lib = _lib.load()
+    assert lib.irk_mg_vcycle(_lib.ctx(), fac._mg.handle, _lib.ptr(a), _lib.ptr(va)) == 0
+    assert lib.irk_mg_vcycle(_lib.ctx(), fac._mg.handle, _lib.ptr(b), _lib.ptr(vb)) == 0
+    x, y = float((va * b).sum()), float((a * vb).sum())
+    assert abs(x - y) <= 1e-12 * max(abs(x), 1.0)
+    assert float((va * a).sum()) > 0  # positive
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,n,beta", [(2, 32, 5e-3), (2, 64, 1e-2), (3, 16, 5e-3)])
+def test_mg_pcg_solves_block(cuda, irk, oracle, dim, n, beta):
+    import scipy.sparse.linalg as spla
+
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd, fac = _p1_block(irk, dim, n, 1.0, beta)
+    assert fac._mg is not None
+    Mo, Ko = oracle.p1_matrices(dim, n)
+    B = oracle.dirichlet_identity((Mo + beta * Ko).tocsr(), bd)
+    rhs = np.random.default_rng(11).standard_normal(M.nrows)
+    x = fac.solve(rhs)
+    ref = spla.spsolve(B.tocsc(), rhs)
+    assert rel(x, ref) < 1e-9
+    its_mg = fac.last_iterations
+    jac = la.BlockFactorization(M, K, 1.0, beta, bd,
+                                la.BlockSolveSettings(method="pcg", rtol=1e-12,
+                                                      raise_on_maxit=True))
+    jac.solve(rhs)
+    assert its_mg < jac.last_iterations / 3, (its_mg, jac.last_iterations)
