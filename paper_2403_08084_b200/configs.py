@@ -57,7 +57,7 @@ def initial_state(k: int, grid: pb.StructuredGrid) -> np.ndarray:
     return 0.1 * noise
 
 
-def build(k: int, n: int | None = None, inner_rtol: float = 1e-6) -> Workload:
+def build(k: int, n: int | None = None, inner_rtol: float = 1e-6, **block) -> Workload:
     dim, n0 = GRID[k]
     grid = pb.StructuredGrid(dim, n or n0)
     u0 = initial_state(k, grid)
@@ -75,7 +75,7 @@ def build(k: int, n: int | None = None, inner_rtol: float = 1e-6) -> Workload:
     pc = {1: PreconditionerKind.BLOCK_DIAGONAL, 2: PreconditionerKind.BLOCK_LOWER,
           3: PreconditionerKind.SCHUR, 4: None, 5: PreconditionerKind.BLOCK_DIAGONAL}[k]
     kw = dict(formulation=form, krylov=KrylovSettings(rtol=1e-10 if k == 5 else 1e-12),
-              pc_kind=pc, block_solver=BlockSolveSettings(rtol=inner_rtol))
+              pc_kind=pc, block_solver=BlockSolveSettings(rtol=inner_rtol, **block))
     if k == 5:
         kw["newton"] = NewtonSettings(rtol=1e-10, atol=1e-10)
     st = TimeStepper(prob, tab, DT[k], **kw)

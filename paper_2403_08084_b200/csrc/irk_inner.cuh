@@ -813,8 +813,20 @@ template <typename T>
 struct Workspace {
   SysState<T>* st;
   T *x, *r, *z, *p0, *p1, *q, *dinv;
+  T* rb;        // right-hand side staged contiguously (graph-stable address)
   int64_t pad;  // readable elements before/after z, p0, p1 (stencil gathers)
 };
+
+// rb[row*NB + k] = rhs[row*ld + k]
+template <typename T, int NB>
+__global__ void k_cg_stage_rhs(int64_t m, const T* __restrict__ rhs, int64_t ld,
+                               T* __restrict__ rb) {
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < m;
+       row += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < NB; ++k) rb[row * NB + k] = rhs[row * ld + k];
+  }
+}
 
 // pad > 0: z, p0 and p1 get `pad` extra elements (zeroed) on both sides
 template <typename T>
@@ -823,11 +835,13 @@ int carve(irk_ctx* ctx, int64_t m, int nb, Workspace<T>& w, int64_t pad = 0) {
   vec = (vec + 255) & ~(size_t)255;
   size_t pb = ((size_t)pad * nb * sizeof(T) + 255) & ~(size_t)255;
   size_t head = (2 * sizeof(SysState<T>) + 255) & ~(size_t)255;  // st[0], st[1]
-  IRK_TRY(ensure_work(ctx, head + 7 * vec + 6 * pb));
+  IRK_TRY(ensure_work(ctx, head + 8 * vec + 6 * pb));
   char* b = ctx->work;
   w.st = reinterpret_cast<SysState<T>*>(b);
   b += head;
   w.pad = pad;
+  w.rb = reinterpret_cast<T*>(b);
+  b += vec;
   T** v[7] = {&w.x, &w.r, &w.q, &w.dinv, &w.z, &w.p0, &w.p1};
   for (int i = 0; i < 7; ++i) {
     if (i >= 4) {
@@ -862,20 +876,41 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   SysState<T>* st0 = w.st;
   SysState<T>* st1 = w.st + 1;
   // init: state "before iteration 0" in st[1]; its partials go past the
-  // two iteration partial buffers
+  // two iteration partial buffers.  The right-hand side is first staged into
+  // the workspace so the init sequence (init kernel, and for an external
+  // preconditioner its first application and rho = r.z) has fixed launch
+  // arguments and replays as one cached graph.
   double* red = ctx->red;
-  k_cg_init<T, NB, HASB><<<G, kBlock, 0, s>>>(m, A, P, shift, mask, rhs, ld_rhs, w.x, w.r, w.z,
-                                              w.p0, w.dinv, rtol * rtol, atol * atol, st1,
-                                              red + 2 * cg_part_doubles<T, NB>(G), cnt);
+  static const bool graph_off = getenv("IRK_NO_GRAPH") != nullptr;
+  k_cg_stage_rhs<T, NB><<<grid_for(ctx, m), kBlock, 0, s>>>(m, rhs, ld_rhs, w.rb);
   IRK_CHECK_LAUNCH(ctx);
-  if constexpr (kExtOk) {
-    if (prec) {
-      double* rr_ = reinterpret_cast<double*>(w.r);
-      double* zz_ = reinterpret_cast<double*>(w.z);
-      IRK_TRY(prec->apply(ctx, s, rr_, zz_, nullptr));
-      k_cg_rho_init<<<G, kBlock, 0, s>>>(m, rr_, zz_, reinterpret_cast<SysState<double>*>(st1),
-                                         red + 2 * cg_part_doubles<T, NB>(G), cnt);
-      IRK_CHECK_LAUNCH(ctx);
+  auto init_body = [&](cudaStream_t cs) -> int {
+    k_cg_init<T, NB, HASB><<<G, kBlock, 0, cs>>>(m, A, P, shift, mask, w.rb, NB, w.x, w.r, w.z,
+                                                 w.p0, w.dinv, rtol * rtol, atol * atol, st1,
+                                                 red + 2 * cg_part_doubles<T, NB>(G), cnt);
+    IRK_CHECK_LAUNCH(ctx);
+    if constexpr (kExtOk) {
+      if (prec) {
+        double* rr_ = reinterpret_cast<double*>(w.r);
+        double* zz_ = reinterpret_cast<double*>(w.z);
+        IRK_TRY(prec->apply(ctx, cs, rr_, zz_, nullptr));
+        k_cg_rho_init<<<G, kBlock, 0, cs>>>(m, rr_, zz_,
+                                            reinterpret_cast<SysState<double>*>(st1),
+                                            red + 2 * cg_part_doubles<T, NB>(G), cnt);
+        IRK_CHECK_LAUNCH(ctx);
+      }
+    }
+    return IRK_OK;
+  };
+  {
+    GraphKey ki;
+    ki.add((const void*)&k_cg_init<T, NB, HASB>).add(m).add(G).add(A).add(P).add(shift);
+    ki.add(mask).add(w).add(red).add(cnt).add(rtol).add(atol);
+    ki.add(prec ? prec->uid : (uint64_t)0);
+    if (graph_off) {
+      IRK_TRY(init_body(s));
+    } else {
+      IRK_TRY(graph_launch(ctx, ki.k, init_body));
     }
   }
   // pinned mirrors: two polls in flight, each of both states
@@ -953,7 +988,6 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   key.add(stencil);
   key.add(m).add(G).add(A).add(P).add(shift).add(mask).add(w).add(red);
   key.add(maxit).add(prec ? prec->uid : (uint64_t)0);
-  static const bool graph_off = getenv("IRK_NO_GRAPH") != nullptr;
   int64_t body_kernels = 0;  // kernels per pass of the graph-resident loop
   if (maxit > 0 && !graph_off) {
     // The whole iteration loop is ONE graph: a conditional WHILE node whose

@@ -22,7 +22,9 @@
 //                 are solved exactly (identity rows)
 //   coarsest:     `ncoarse` Chebyshev steps (the coarsest operator is
 //                 mass-dominated: beta / (alpha H^2) small)
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -88,6 +90,78 @@ __global__ void __launch_bounds__(kBlock)
     const double dn = (cd != 0.0 ? cd * d[i] : 0.0) + cr * dinv[i] * res;
     d[i] = dn;
     xout[i] = x0 + dn;
+  }
+}
+
+// Stencil row product for stencil-aligned ELL patterns (A.sw == W): the
+// W gathers at the stencil offsets are issued at once (x carries a readable
+// halo of max|offset| + 32 elements on both sides), the slice's slot headers
+// are loaded by lanes 0..W-1 and checked with one warp vote; slices that
+// are not plain stencil slices take the generic path.  All 32 lanes of the
+// warp must call it (one SELL slice per warp).
+template <int W>
+__device__ __forceinline__ double st_dot(const MatView& A, int64_t sl, int64_t row, bool valid,
+                                         const double* __restrict__ x) {
+  const int lane = threadIdx.x & 31;
+  const int q0 = (int)(sl * W);
+  const bool hl = lane < W;
+  const int hd = hl ? __ldg(A.colhdr + q0 + lane) : 0;
+  const double ha = hl ? __ldg(A.ua + q0 + lane) : 0.0;
+  double ps[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) ps[k] = __ldg(x + row + A.sd[k]);
+  const bool ok = __all_sync(0xffffffffu, !hl || (hd == A.sd[hl ? lane : 0] && !isnan(ha)));
+  double acc = 0.0;
+  if (ok) {
+#pragma unroll
+    for (int k = 0; k < W; ++k) acc += __shfl_sync(0xffffffffu, ha, k) * ps[k];
+  } else if (valid) {
+    acc = row_dot(A, row, x);
+  }
+  return acc;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBlock)
+    k_mg_cheb_st(int64_t m, MatView A, const uint8_t* __restrict__ mask,
+                 const double* __restrict__ dinv, const double* __restrict__ b,
+                 const double* __restrict__ xin, double* __restrict__ d,
+                 double* __restrict__ xout, double cd, double cr, const int* stop) {
+  if (stop && *stop) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nsl = (m + kSlice - 1) / kSlice;
+  const int64_t ws = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; sl < nsl; sl += ws) {
+    const int64_t i = sl * kSlice + lane;
+    const bool valid = i < m;
+    const double ax = st_dot<W>(A, sl, i, valid, xin);
+    if (!valid) continue;
+    const double bi = b[i];
+    if (mask && mask[i]) {
+      d[i] = 0.0;
+      xout[i] = bi;
+      continue;
+    }
+    const double dn = (cd != 0.0 ? cd * d[i] : 0.0) + cr * dinv[i] * (bi - ax);
+    d[i] = dn;
+    xout[i] = xin[i] + dn;
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBlock)
+    k_mg_residual_st(int64_t m, MatView A, const uint8_t* __restrict__ mask,
+                     const double* __restrict__ b, const double* __restrict__ x,
+                     double* __restrict__ r, const int* stop) {
+  if (stop && *stop) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nsl = (m + kSlice - 1) / kSlice;
+  const int64_t ws = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; sl < nsl; sl += ws) {
+    const int64_t i = sl * kSlice + lane;
+    const bool valid = i < m;
+    const double ax = st_dot<W>(A, sl, i, valid, x);
+    if (valid) r[i] = (mask && mask[i]) ? 0.0 : b[i] - ax;
   }
 }
 
@@ -210,6 +284,7 @@ struct MgLevel {
   double* d = nullptr;
   double* r = nullptr;
   double lmax = 2.0;
+  int st = 0;  // stencil width of the fast kernels (0: generic row products)
 };
 
 static std::atomic<uint64_t> g_mg_uid{1};
@@ -251,8 +326,18 @@ struct irk_mg : public irk::CgPrec {
       const int dst = cur == 0 ? 1 : 0;
       const double* xin = cur < 0 ? nullptr : L.x[cur];
       double* xo = (k == n - 1 && out) ? out : L.x[dst];
-      k_mg_cheb<<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, L.dinv, b, xin, L.d, xo,
-                                                      cd[k], cr[k], stop);
+      if (xin && L.st == 7)
+        k_mg_cheb_st<7><<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, L.dinv, b, xin,
+                                                             L.d, xo, cd[k], cr[k], stop);
+      else if (xin && L.st == 15)
+        k_mg_cheb_st<15><<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, L.dinv, b, xin,
+                                                              L.d, xo, cd[k], cr[k], stop);
+      else if (xin && L.st == 3)
+        k_mg_cheb_st<3><<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, L.dinv, b, xin,
+                                                             L.d, xo, cd[k], cr[k], stop);
+      else
+        k_mg_cheb<<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, L.dinv, b, xin, L.d,
+                                                        xo, cd[k], cr[k], stop);
       if (cudaPeekAtLastError() != cudaSuccess) return -1;
       ctx->launches++;
       cur = xo == out ? 2 : dst;
@@ -269,7 +354,18 @@ struct irk_mg : public irk::CgPrec {
     if (l == (int)lev.size() - 1) return smooth(ctx, s, l, b, -1, ncoarse, 0.05, out, stop);
     const int c = smooth(ctx, s, l, b, -1, nu, 0.25, nullptr, stop);
     if (c < 0) return -1;
-    k_mg_residual<<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, b, L.x[c], L.r, stop);
+    if (L.st == 7)
+      k_mg_residual_st<7><<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, b, L.x[c],
+                                                                 L.r, stop);
+    else if (L.st == 15)
+      k_mg_residual_st<15><<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, b, L.x[c],
+                                                                  L.r, stop);
+    else if (L.st == 3)
+      k_mg_residual_st<3><<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, b, L.x[c],
+                                                                 L.r, stop);
+    else
+      k_mg_residual<<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, b, L.x[c], L.r,
+                                                          stop);
     ctx->launches++;
     MgLevel& Cc = lev[l + 1];
     k_mg_restrict<<<(unsigned)((Cc.m + kBlock - 1) / kBlock), kBlock, 0, s>>>(
@@ -316,6 +412,7 @@ int irk_mg_create(irk_ctx* ctx, int dim, int nlev, const int64_t* N_host,
   mg->nu = nu;
   mg->ncoarse = ncoarse;
   size_t total = 0;
+  std::vector<int64_t> pads;
   for (int l = 0; l < nlev; ++l) {
     const int64_t n1 = N_host[l] + 1;
     int64_t m = n1;
@@ -332,7 +429,16 @@ int irk_mg_create(irk_ctx* ctx, int dim, int nlev, const int64_t* N_host,
     L.A = make_view(A_levels[l], nullptr);
     L.mask = masks ? masks[l] : nullptr;
     mg->lev.push_back(L);
-    total += (size_t)(6 * m + 64);
+    // the iterate buffers carry a halo for the speculative stencil gathers
+    int64_t pad = 0;
+    if (L.A.sw == 3 || L.A.sw == 7 || L.A.sw == 15) {
+      for (int k = 0; k < L.A.sw; ++k) pad = std::max<int64_t>(pad, std::abs(L.A.sd[k]));
+      pad += 2 * kSlice;
+      L.st = L.A.sw;
+    }
+    mg->lev.back().st = L.st;
+    pads.push_back(pad);
+    total += (size_t)(6 * m + 4 * pad + 64);
   }
   cudaError_t e = cudaMalloc(&mg->mem, total * sizeof(double));
   if (e != cudaSuccess) {
@@ -342,11 +448,14 @@ int irk_mg_create(irk_ctx* ctx, int dim, int nlev, const int64_t* N_host,
   }
   IRK_CUDA(cudaMemsetAsync(mg->mem, 0, total * sizeof(double), ctx->stream));
   double* p = mg->mem;
-  for (auto& L : mg->lev) {
+  for (size_t l = 0; l < mg->lev.size(); ++l) {
+    MgLevel& L = mg->lev[l];
     double** v[6] = {&L.dinv, &L.b, &L.x[0], &L.x[1], &L.d, &L.r};
-    for (auto q : v) {
-      *q = p;
-      p += L.m;
+    for (int i = 0; i < 6; ++i) {
+      const int64_t pd = (i == 2 || i == 3) ? pads[l] : 0;
+      p += pd;
+      *v[i] = p;
+      p += L.m + pd;
     }
     p += 64;
   }

@@ -479,7 +479,8 @@ class BlockSolveSettings:
     (Jacobi-preconditioned CG) or "chebyshev" (Jacobi-Chebyshev,
     ``cheb_iters`` sweeps with Gershgorin/Lanczos-free bounds).
     mg_nu / mg_coarse_steps: Chebyshev smoothing steps per level and on the
-    coarsest level of the multigrid V-cycle.
+    coarsest level of the multigrid V-cycle; mg_coarse_ratio: coarsening stops
+    once beta / (alpha H^2) of a level is at most this (mass-dominated).
     raise_on_maxit: when False (preconditioner use) an unconverged block
     returns its last iterate, FGMRES being flexible."""
 
@@ -490,7 +491,8 @@ class BlockSolveSettings:
     raise_on_maxit: bool = False
     cheb_iters: int = 50
     mg_nu: int = 2
-    mg_coarse_steps: int = 8
+    mg_coarse_steps: int = 4
+    mg_coarse_ratio: float = 0.5
 
     def __post_init__(self):
         if self.method not in ("auto", "pcg", "mg", "chebyshev"):
@@ -504,8 +506,8 @@ class _MgHierarchy:
     (libirk irk_mg_*): level l re-assembles the operator with N/2^l cells per
     direction (nested P1 grids: the Galerkin operator), Dirichlet rows where
     the coincident fine node is constrained.  Coarsening stops at odd N, at
-    N < 4, or once the level is mass-dominated (beta/(alpha H^2) <= 1/2),
-    where a few Chebyshev steps solve it."""
+    N < 4, or once the level is mass-dominated (beta/(alpha H^2) <=
+    mg_coarse_ratio), where a few Chebyshev steps solve it well enough."""
 
     def __init__(self, handle, keep):
         self.handle = handle
@@ -539,7 +541,7 @@ class _MgHierarchy:
         Ns, mats, masks = [N], [B], [mask]
         while Ns[-1] % 2 == 0 and Ns[-1] // 2 >= 4 and len(Ns) < 12:
             H = 1.0 / Ns[-1]
-            if beta / (alpha * H * H) <= 0.5:
+            if beta / (alpha * H * H) <= settings.mg_coarse_ratio:
                 break
             Nc = Ns[-1] // 2
             hM, hK = C.c_void_p(), C.c_void_p()
