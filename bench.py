@@ -16,7 +16,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -46,60 +45,67 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled during the timed
+    region, in-process through NVML (the fields of the profiling recipe's
+    nvidia-smi line).  NVML is initialised before the warm-up; the timed loop
+    calls sample() between time steps (a few per run, ~5 ms each, on the
+    main thread).  Concurrent sampling from another thread or a looping
+    nvidia-smi was measured to stall this workload's frequent stream syncs by
+    100-400 ms per step (driver-lock contention), so it is not used."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40,
+               "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.lines = []
-        self.proc = None
+        self.samples = []  # (time, sm_mhz, reasons bitmask)
+        self.max_mhz = None
+        self.window = None
 
     def __enter__(self):
+        if os.environ.get("IRK_BENCH_NOCLOCKS"):
+            return self
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except (OSError, FileNotFoundError):
-            self.proc = None
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+        except Exception:  # no NVML: no samples (reported as such)
+            self._h = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def sample(self):
+        if getattr(self, "_h", None) is None:
+            return
+        nv, h = self._nv, self._h
+        try:
+            sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+            rs = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+            self.samples.append((time.perf_counter(), sm, rs))
+        except Exception:
+            pass
+
+    def mark(self, t0, t1):
+        """Bracket the timed region; summary() keeps the samples inside it
+        (the nearest one when the region is shorter than the period)."""
+        self.window = (t0, t1)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        pass
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) != 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[2:]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
-                "reasons": sorted(reasons), "samples": len(sm)}
+        smp = self.samples
+        if self.window is not None and smp:
+            t0, t1 = self.window
+            inside = [x for x in smp if t0 <= x[0] <= t1]
+            smp = inside or [min(smp, key=lambda x: abs(x[0] - 0.5 * (t0 + t1)))]
+        if not smp:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        reasons = sorted({n for _, _, rs in smp for n, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": float(np.median([x[1] for x in smp])), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(smp), "source": "nvml"}
 
 
 def dist_setup(args):
@@ -231,6 +237,7 @@ def run_ours(args, world, rank, local):
     _lib.load()
     wl = configs.build(args.config)
     st, prob = wl.stepper, wl.problem
+    clk = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
         st.step_device(prob)
     torch.cuda.synchronize()
@@ -242,15 +249,40 @@ def run_ours(args, world, rank, local):
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = _lib.launch_count()
-    with ClockSampler(local) as clk:
+    if os.environ.get("IRK_BENCH_NOGC"):
+        import gc
+
+        gc.disable()
+    if True:
         torch.cuda.synchronize()
+        w_t0 = time.perf_counter()
         e0.record(stream)
-        for _ in range(args.steps):
+        marks = []
+        sample_at = {args.steps // 3, (2 * args.steps) // 3, args.steps - 1}
+        for i in range(args.steps):
             _, rep = st.step_device(prob)
             reps.append(rep)
+            if i in sample_at:
+                ts0 = time.perf_counter()
+                clk.sample()
+                if os.environ.get("IRK_BENCH_TRACE"):
+                    print(f"sample after step {i}: {1e3 * (time.perf_counter() - ts0):.2f} ms",
+                          file=sys.stderr)
+            if os.environ.get("IRK_BENCH_TRACE"):
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(stream)
+                marks.append((ev, time.perf_counter()))
         e1.record(stream)
         torch.cuda.synchronize()
+        clk.mark(w_t0, time.perf_counter())
+    clk.__exit__(None, None, None)
     launches = _lib.launch_count() - launches0
+    if marks:
+        prev_e, prev_w = e0, None
+        for k, (ev, wt) in enumerate(marks):
+            print(f"step {k}: {prev_e.elapsed_time(ev):.2f} ms device, krylov "
+                  f"{reps[k].krylov_iters}", file=sys.stderr)
+            prev_e = ev
     t_dev = e0.elapsed_time(e1) / 1e3
     t_max, value = replica_throughput(t_dev, args.steps, world)
 

@@ -55,6 +55,14 @@ int irk_ctx_set_stream(irk_ctx* ctx, void* stream);
 int irk_ctx_synchronize(irk_ctx* ctx);
 /* Number of kernels this context has launched so far (bench accounting). */
 int64_t irk_ctx_launch_count(const irk_ctx* ctx);
+/* Deferred inner-solve status.  While enabled, irk_pcg / irk_cocg /
+ * irk_mg_pcg called with its_host == relres_host == NULL return IRK_OK
+ * without synchronising and append (iterations, code 0 ok / 1 cap /
+ * 2 breakdown, loop iterations, kernels per loop pass) to a device log;
+ * irk_ctx_log_take copies the entries in call order (synchronous) and
+ * clears the log.  Enabling also clears it. */
+int irk_ctx_log_enable(irk_ctx* ctx, int on);
+int irk_ctx_log_take(irk_ctx* ctx, int* out_host, int max_entries, int* n_out);
 const char* irk_last_error(void);
 /* Library version string. */
 const char* irk_version(void);

@@ -83,6 +83,8 @@ _SIGS = {
     "irk_fe_load": [_vp, _int, _i64, _vp, _vp],
     "irk_fe_mms_forcing": [_vp, _int, _i64, _dbl, _vp],
     "irk_fe_error_sq": [_vp, _int, _i64, _vp, _vp, _vp, _vp],
+    "irk_ctx_log_enable": [_vp, _int],
+    "irk_ctx_log_take": [_vp, _vp, _int, _vp],
     "irk_mg_create": [_vp, _int, _int, _vp, _vp, _vp, _int, _int, _vp],
     "irk_mg_destroy": [_vp],
     "irk_mg_vcycle": [_vp, _vp, _vp, _vp],
@@ -217,6 +219,29 @@ def ctx():
 
 def launch_count() -> int:
     return context().launches()
+
+
+class deferred_solves:
+    """Context manager: inner solves that pass no status buffers run without
+    a host round trip; on exit the per-solve (iterations, code) log is read
+    back in one copy into ``self.entries`` (numpy, shape (n, 4))."""
+
+    def __init__(self):
+        self.entries = np.zeros((0, 4), dtype=np.int32)
+
+    def __enter__(self):
+        call("irk_ctx_log_enable", ctx(), 1)
+        return self
+
+    def __exit__(self, *exc):
+        buf = np.zeros((4096, 4), dtype=np.int32)
+        n = C.c_int(0)
+        try:
+            call("irk_ctx_log_take", ctx(), hptr(buf), 4096, C.byref(n))
+        finally:
+            call("irk_ctx_log_enable", ctx(), 0)
+        self.entries = buf[: n.value].copy()
+        return False
 
 
 # ------------------------------------------------------------- marshalling

@@ -2,6 +2,8 @@
 #include <cstdarg>
 #include <cstring>
 
+#include <algorithm>
+
 #include "irk_internal.cuh"
 
 namespace irk {
@@ -101,6 +103,7 @@ int irk_ctx_destroy(irk_ctx* ctx) {
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
+  if (ctx->solve_log) cudaFree(ctx->solve_log);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   delete ctx;
   return IRK_OK;
@@ -119,5 +122,34 @@ int irk_ctx_synchronize(irk_ctx* ctx) {
 }
 
 int64_t irk_ctx_launch_count(const irk_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int irk_ctx_log_enable(irk_ctx* ctx, int on) {
+  IRK_REQUIRE(ctx, "irk_ctx_log_enable: NULL context");
+  if (on && !ctx->solve_log) {
+    ctx->log_cap = 4096;
+    IRK_CUDA(cudaMalloc(&ctx->solve_log, (size_t)ctx->log_cap * 4 * sizeof(int)));
+  }
+  ctx->log_on = on ? 1 : 0;
+  ctx->log_n = 0;
+  return IRK_OK;
+}
+
+int irk_ctx_log_take(irk_ctx* ctx, int* out_host, int max_entries, int* n_out) {
+  IRK_REQUIRE(ctx && n_out, "irk_ctx_log_take: NULL argument");
+  const int n = (int)std::min<int64_t>(ctx->log_n, max_entries);
+  if (n > 0) {
+    IRK_REQUIRE(out_host, "irk_ctx_log_take: NULL output");
+    IRK_CUDA(cudaMemcpyAsync(out_host, ctx->solve_log, (size_t)n * 4 * sizeof(int),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < n; ++i) {
+    // kernels executed by graph-resident loops: per pass, (iterations / 2 + 1) passes
+    ctx->launches += (int64_t)out_host[4 * i + 3] * (out_host[4 * i + 2] / 2 + 1);
+  }
+  *n_out = n;
+  ctx->log_n = 0;
+  return IRK_OK;
+}
 
 }  // extern "C"

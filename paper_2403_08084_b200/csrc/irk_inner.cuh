@@ -785,6 +785,27 @@ __global__ void k_cg_cond(cudaGraphConditionalHandle h, const SysState<T>* a,
     cudaGraphSetConditional(h, (__ldcg(&a->done) || __ldcg(&b->done)) ? 0u : 1u);
 }
 
+// Deferred status: the finished state's (max iterations, worst code,
+// loop iteration count) of one solve into the context's solve log.
+template <typename T>
+__global__ void k_cg_log(const SysState<T>* a, const SysState<T>* b, int nb, int body_kernels,
+                         int* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const SysState<T>* f = (a->done != b->done) ? (a->done ? a : b) : (a->iter >= b->iter ? a : b);
+  int its = 0, code = 0;
+  for (int k = 0; k < nb; ++k) {
+    its = max(its, f->its[k]);
+    int c = f->code[k];
+    if (c == 0 && f->active[k]) c = 1;
+    if (c == 2 && f->rr[k] <= f->tol2[k]) c = 0;  // breakdown after convergence
+    code = max(code, c);
+  }
+  out[0] = its;
+  out[1] = code;
+  out[2] = f->iter;
+  out[3] = body_kernels;
+}
+
 // External preconditioner z = P^-1 r for the real one-system CG (the
 // geometric multigrid of irk_mg.cu): a fixed, graph-capturable kernel
 // sequence on the given stream.
@@ -1041,6 +1062,16 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
     }
     // finalising A: applies the decisions of the last issued iteration (cap)
     IRK_TRY(launch_a(s, issued));
+  }
+  if (!its_host && !relres_host && ctx->log_on && ctx->log_n < ctx->log_cap) {
+    // deferred status: log the outcome on the device, no host round trip
+    k_cg_log<T><<<1, 32, 0, s>>>(st0, st1, NB, (int)body_kernels,
+                                 ctx->solve_log + 4 * ctx->log_n);
+    IRK_CHECK_LAUNCH(ctx);
+    ctx->log_n++;
+    k_cg_store<T, NB><<<grid_for(ctx, m), kBlock, 0, s>>>(m, w.x, xout, ld_x);
+    IRK_CHECK_LAUNCH(ctx);
+    return IRK_OK;
   }
   IRK_CUDA(cudaMemcpyAsync(hst, w.st, 2 * sizeof(SysState<T>), cudaMemcpyDeviceToHost, s));
   k_cg_store<T, NB><<<grid_for(ctx, m), kBlock, 0, s>>>(m, w.x, xout, ld_x);

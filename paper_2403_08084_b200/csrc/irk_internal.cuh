@@ -89,6 +89,14 @@ struct irk_ctx {
   };
   std::vector<GraphEntry> graphs;
   cudaStream_t cap_stream = nullptr;
+  // Deferred solve status (irk_ctx_log_enable): inner solves called with
+  // NULL its/relres do not synchronise; each appends (iterations, code,
+  // loop passes, kernels per pass) to this device log, read back in one copy
+  // by irk_ctx_log_take.
+  int log_on = 0;
+  int* solve_log = nullptr;  // 4 ints per entry
+  int log_cap = 0;
+  int64_t log_n = 0;
 };
 
 namespace irk {

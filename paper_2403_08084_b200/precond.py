@@ -124,6 +124,7 @@ class StagePreconditioner:
         self._mats = None
         self._schur = None
         self.inner_iterations = []
+        self.defer_solves = False  # set by the stepper around deferred_solves
 
     # ------------------------------------------------------------ helpers
     def mask(self):
@@ -200,7 +201,9 @@ class StagePreconditioner:
                 call("irk_stage_get", ctx(), m, s, i, ptr(R), ptr(tmp))
             fac = self.block_factors[i]
             xi = X[i:]
-            st = fac.dev_solve(tmp, xi, ld_rhs=1, ld_x=s, settings=self.settings)
+            # deferred (no host round trip) when the caller collects the log
+            st = fac.dev_solve(tmp, xi, ld_rhs=1, ld_x=s, settings=self.settings,
+                               defer=self.defer_solves)
             self.inner_iterations.append([st])
         return X
 

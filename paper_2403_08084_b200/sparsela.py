@@ -623,20 +623,29 @@ class BlockFactorization:
             self._matrix = SparseMatrix._from_device(self._B)
         return self._matrix
 
-    def dev_solve(self, rhs, x, ld_rhs=1, ld_x=1, nb=1, settings: BlockSolveSettings | None = None):
+    def dev_solve(self, rhs, x, ld_rhs=1, ld_x=1, nb=1, settings: BlockSolveSettings | None = None,
+                  defer: bool = False):
+        """Solve on device data.  defer=True (inside _lib.deferred_solves, for
+        preconditioner use that never raises): no host synchronisation, the
+        outcome goes to the context's solve log and None is returned."""
         st = settings or self.settings
         its = np.zeros(8, dtype=np.int32)
         rel = np.zeros(8, dtype=np.float64)
         one = np.ones(8)
+        defer = defer and not st.raise_on_maxit
+        its_p, rel_p = (None, None) if defer else (hptr(its), hptr(rel))
         if self._mg is not None and st.method in ("auto", "mg"):
             status = _lib.load().irk_mg_pcg(
                 ctx(), self._mg.handle, ptr(rhs), int(ld_rhs), ptr(x), int(ld_x),
-                float(st.rtol), float(st.atol), int(st.maxit), hptr(its), hptr(rel))
+                float(st.rtol), float(st.atol), int(st.maxit), its_p, rel_p)
         else:
             status = _lib.load().irk_pcg(
                 ctx(), 1, hptr(one), C.c_void_p(), self._B.handle, C.c_void_p(), C.c_void_p(),
                 C.c_void_p(), ptr(rhs), int(ld_rhs), ptr(x), int(ld_x), float(st.rtol),
-                float(st.atol), int(st.maxit), hptr(its), hptr(rel))
+                float(st.atol), int(st.maxit), its_p, rel_p)
+        if defer:
+            _lib.check(status, "deferred block solve")
+            return None
         self.last_iterations = int(its[0])
         self.last_relres = float(rel[0])
         if status == _lib.IRK_ENOCONV:

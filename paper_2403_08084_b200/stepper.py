@@ -25,6 +25,7 @@ from typing import Callable, Optional
 
 import numpy as np
 
+from . import _lib
 from . import sparsela as la
 from ._lib import call, ctx, hptr, ptr
 from .bcs import (
@@ -473,7 +474,20 @@ def _solve_constrained_dev(stepper, problem, op, rhs_il, unknown, t):
     if stepper.warm_start and stepper._last_stages_dev is not None:
         if stepper._last_stages_dev.numel() == srhs.numel():
             x0 = stepper._last_stages_dev
-    res = fgmres_device(A, srhs, P, stepper.krylov, x0)
+    if pc is not None:
+        # sequential block solves of the preconditioner run without a host
+        # round trip each; their iteration counts come back in one copy
+        pc.defer_solves = True
+        try:
+            with _lib.deferred_solves() as log:
+                res = fgmres_device(A, srhs, P, stepper.krylov, x0)
+        finally:
+            pc.defer_solves = False
+        entries = iter(log.entries[:, 0].tolist())
+        pc.inner_iterations = [[next(entries, -1) if v is None else v for v in its]
+                               for its in pc.inner_iterations]
+    else:
+        res = fgmres_device(A, srhs, P, stepper.krylov, x0)
     x = res.x
     if svals is not None:
         scatter_stage_values(x, bc.dofs_dev(), svals, op.s)
