@@ -351,12 +351,27 @@ def spmv(A: SparseMatrix, x):
     return _like_input(y, x)
 
 
+_MASKS: dict = {}
+
+
 def dof_mask(m: int, dofs):
-    """uint8 device mask with ones at ``dofs``."""
+    """uint8 device mask with ones at ``dofs`` (read-only; cached by content,
+    so every constrained operator of a problem shares one mask object and
+    the per-mask caches of eliminated matrices keep hitting -- a fresh mask
+    per step re-created, and freed with a device sync, both eliminated
+    stage matrices every step)."""
     torch = _torch()
-    idx = to_dev(np.asarray(dofs, dtype=np.int64), dtype=torch.int64)
+    d = np.ascontiguousarray(np.asarray(dofs, dtype=np.int64))
+    key = (int(m), d.size, hash(d.tobytes()), _lib.device_index())
+    hit = _MASKS.get(key)
+    if hit is not None and np.array_equal(hit[0], d):
+        return hit[1]
+    idx = to_dev(d, dtype=torch.int64)
     mask = torch.empty(int(m), dtype=torch.uint8, device=device())
     call("irk_bc_mask", ctx(), int(m), int(idx.numel()), ptr(idx), ptr(mask))
+    if len(_MASKS) >= 64:
+        _MASKS.pop(next(iter(_MASKS)))
+    _MASKS[key] = (d.copy(), mask)
     return mask
 
 
