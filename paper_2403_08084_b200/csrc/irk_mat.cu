@@ -193,9 +193,10 @@ int pattern_build_sell(irk_ctx* ctx, Pattern* p) {
     k_slice_sizes<<<(unsigned)((threads + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(
         p->nrows, ns, p->rowptr, sizes);
     IRK_CHECK_LAUNCH(ctx);
-    // Pad every slice to the widest one (ELL-32) when that costs <= 5%: the
-    // slice offsets become arithmetic (32 * W * s), so kernels need no
-    // dependent slice_ptr load before their first matrix load.
+    // Pad every slice to the widest one (ELL-32) when that costs <= 5% (or
+    // the matrix is small): the slice offsets become arithmetic (32 * W * s),
+    // so kernels need no dependent slice_ptr load before their first matrix
+    // load.
     {
       std::vector<int> hs(ns);
       IRK_CUDA(cudaMemcpyAsync(hs.data(), sizes, ns * sizeof(int), cudaMemcpyDeviceToHost,
@@ -209,7 +210,11 @@ int pattern_build_sell(irk_ctx* ctx, Pattern* p) {
       }
       const int64_t padded = ns * (int64_t)kSlice * wmax;
       p->ellw = 0;
-      if (wmax > 0 && padded <= tot + tot / 20 && padded < (int64_t)INT32_MAX / 2) {
+      // small matrices (the coarse multigrid levels): padding is cheap and
+      // the arithmetic slice offsets / stencil path save a dependent load
+      // in latency-bound kernels
+      const bool small = p->nrows <= (1 << 17) && padded <= 2 * tot;
+      if (wmax > 0 && (padded <= tot + tot / 20 || small) && padded < (int64_t)INT32_MAX / 2) {
         for (int64_t q = 0; q < ns; ++q) hs[q] = wmax * kSlice;
         IRK_CUDA(cudaMemcpyAsync(sizes, hs.data(), ns * sizeof(int), cudaMemcpyHostToDevice,
                                  ctx->stream));
