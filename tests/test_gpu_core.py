@@ -379,3 +379,51 @@ def test_mg_pcg_solves_block(cuda, irk, oracle, dim, n, beta):
                                                       raise_on_maxit=True))
     jac.solve(rhs)
     assert its_mg < jac.last_iterations / 3, (its_mg, jac.last_iterations)
+
+
+@pytest.mark.gpu
+def test_mg_pcg_cap_and_deferred_log(cuda, irk):
+    """Iteration cap inside the graph-resident loop raises / reports like the
+    host loop; deferred solves log (iterations, code) in call order."""
+    from paper_2403_08084_b200 import _lib
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd, fac = _p1_block(irk, 2, 32, 1.0, 5e-3)
+    rhs = la.to_dev(np.random.default_rng(2).standard_normal(M.nrows))
+    x = la.dev_empty(M.nrows)
+    capped = la.BlockSolveSettings(rtol=1e-14, maxit=2, raise_on_maxit=True)
+    with pytest.raises(la.NonConvergenceError):
+        fac.dev_solve(rhs, x, settings=capped)
+    assert fac.last_iterations == 2
+    soft = la.BlockSolveSettings(rtol=1e-6)
+    ref_its = fac.dev_solve(rhs, x, settings=soft)
+    capped_soft = la.BlockSolveSettings(rtol=1e-14, maxit=3)
+    with _lib.deferred_solves() as log:
+        assert fac.dev_solve(rhs, x, settings=soft, defer=True) is None
+        assert fac.dev_solve(rhs, x, settings=capped_soft, defer=True) is None
+    assert log.entries.shape == (2, 4)
+    assert log.entries[0, 0] == ref_its and log.entries[0, 1] == 0
+    assert log.entries[1, 0] == 3 and log.entries[1, 1] == 1
+
+
+@pytest.mark.gpu
+def test_mg_hierarchy_1d_and_masks(cuda, irk, oracle):
+    """1D P1 blocks get a hierarchy; a non-boundary Dirichlet set or a
+    missing grid tag falls back to Jacobi-PCG; the mask cache returns one
+    object per dof set."""
+    import scipy.sparse.linalg as spla
+
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd, fac = _p1_block(irk, 1, 256, 1.0, 1e-3)
+    assert fac._mg is not None and fac._mg.levels >= 3
+    rhs = np.random.default_rng(4).standard_normal(M.nrows)
+    Mo, Ko = oracle.p1_matrices(1, 256)
+    B = oracle.dirichlet_identity((Mo + 1e-3 * Ko).tocsr(), bd)
+    assert rel(fac.solve(rhs), spla.spsolve(B.tocsc(), rhs)) < 1e-9
+    inner = la.BlockFactorization(M, K, 1.0, 1e-3, np.array([5, 9]),
+                                  la.BlockSolveSettings(rtol=1e-12, raise_on_maxit=True))
+    assert inner._mg is None
+    untagged = la.SparseMatrix.from_scipy(Mo)
+    assert la.BlockFactorization(untagged, la.SparseMatrix.from_scipy(Ko), 1.0, 1e-3, bd)._mg is None
+    assert la.dof_mask(M.nrows, bd) is la.dof_mask(M.nrows, np.array(bd))
