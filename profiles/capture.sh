@@ -2,23 +2,24 @@
 # Round profiling capture (run on the GPU box from the repo root):
 #   /usr/local/graft/bin/gpurun --timeout 1500 -- 'bash profiles/capture.sh r01'
 # 1. bench.py must exit 0 without ncu first;
-# 2. ncu launch list of the bench command (cold-cache, serialised launches);
-# 3. one `ncu --set full` capture each of the stage apply (K2) and the two
-#    inner-PCG kernels (config 2), from which profiles/traffic.json is made.
+# 2. ncu launch list of the bench command (cold-cache, serialised launches).
+#    Kernels inside graphs with conditional (WHILE) nodes cannot be profiled
+#    by ncu, so the list is taken with IRK_NO_GRAPH=1 (same kernels, launched
+#    one by one);
+# 3. one `ncu --set full` capture each of the stage apply (K2), the fine-level
+#    multigrid smoother / residual and the CG kernels (config 2), from which
+#    profiles/traffic.json is made.
 set -u
 R=${1:-r01}
 OUT=gpurun_out/$R
 mkdir -p "$OUT"
-python bench.py --steps 2 --warmup 3 --no-cpu-baseline > "$OUT/bench_plain.json" 2> "$OUT/bench_plain.err" || exit 1
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+python bench.py --steps 3 --warmup 3 --no-cpu-baseline > "$OUT/bench_plain.json" 2> "$OUT/bench_plain.err" || exit 1
+IRK_NO_GRAPH=1 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
     --log-file "$OUT/launches.csv" python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
     > "$OUT/launches.log" 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_stage_apply_win -s 5 -c 1 \
     -o "$OUT/stage_apply" python profiles/micro_stage.py 2 > "$OUT/ncu_stage.log" 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_cg_ -s 40 -c 2 \
-    -o "$OUT/pcg" python profiles/micro_pcg.py 2 20 > "$OUT/ncu_pcg.log" 2>&1
-# steady-state (no cache flush) per-kernel DRAM traffic of the PCG kernels
-ncu --cache-control none --clock-control none -k regex:k_cg_ -s 400 -c 6 \
-    --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum \
-    --csv --log-file "$OUT/pcg_steady.csv" python profiles/micro_pcg.py 2 20 > /dev/null 2>&1
+IRK_NO_GRAPH=1 ncu --set full --clock-control none --import-source on \
+    -k regex:"k_mg_cheb_st|k_mg_residual_st|k_cg_spmv_st|k_cg_update" -s 200 -c 6 \
+    -o "$OUT/mg" python profiles/solve_probe.py 2 > "$OUT/ncu_mg.log" 2>&1
 echo done
