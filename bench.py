@@ -327,8 +327,9 @@ def run_ours(args, world, rank, local):
             "us_per_solve": t_in * 1e6,
             "us_per_iteration": t_in * 1e6 / max(meta_in["iterations_per_solve"], 1),
             "solves_per_step": float(np.mean(solves)) if solves else None,
-            "step_share_est": (float(np.mean(solves)) * t_in * args.steps / t_dev)
-            if solves else None, **meta_in}
+            "step_share_est": (float(np.mean(inner)) * t_in
+                               / max(meta_in["iterations_per_solve"], 1) * args.steps / t_dev)
+            if inner else None, **meta_in}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
