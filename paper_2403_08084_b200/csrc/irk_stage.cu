@@ -9,6 +9,7 @@
 //   step_linear update             stepper.py:352-361
 //   step_newton residual/stages    stepper.py:502-524
 #include <cstdlib>
+#include <vector>
 
 #include "irk_internal.cuh"
 
@@ -258,6 +259,142 @@ __global__ void __launch_bounds__(kBlock, MAXW <= 10 ? 3 : 2)
     }
     Out[r * S + i] = flagged ? Y[r * S + i] : o + dt * t;
   }
+}
+
+// Stencil variant of the windowed K2 for stencil-aligned ELL patterns: the
+// window layout of a plain stencil slice (every slot at the pattern's
+// stencil offset) is the same for all of them, so it is computed once on
+// the host and passed in (no per-slice shuffles / scans); a warp vote on
+// the slot headers selects it, other slices gather per entry.
+struct StLayout {
+  int nwin, total;
+  int wstart[16], wbase[16], wend[16];  // window w: rows [r0+wstart, ...), buffer rows [wbase, wend)
+  int srow[16];                         // buffer row of slot k for lane 0
+  int sd[16];                           // stencil offsets
+};
+
+template <int S, int W>
+__global__ void __launch_bounds__(kBlock, W <= 8 ? 3 : 2)
+    k_stage_apply_std(int64_t m, int64_t nslices, const StLayout SL,
+                      const int* __restrict__ sell_col, const int* __restrict__ colhdr,
+                      const double* __restrict__ mval, const double* __restrict__ kval,
+                      const Coef2 cf, double dt, const uint8_t* __restrict__ mask,
+                      const double* __restrict__ Y, double* __restrict__ Out) {
+  extern __shared__ double wsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t sl = (int64_t)blockIdx.x * (kBlock / 32) + warp;
+  if (sl >= nslices) return;
+  constexpr int SP = (S % 2 == 0) ? S + 1 : S;
+  double* buf = wsm + (size_t)warp * SL.total * SP;
+  const int64_t r0 = sl * kSlice, r = r0 + lane;
+  const int base = (int)(sl * kSlice * W);
+  const int q0 = (int)(sl * W);
+  const bool flagged = r < m && mask && mask[r];
+  double mv[W], kv[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    mv[k] = __ldg(mval + base + k * kSlice + lane);
+    kv[k] = __ldg(kval + base + k * kSlice + lane);
+  }
+  const int d = lane < W ? __ldg(colhdr + q0 + lane) : 0;
+  const bool std_slice = __all_sync(0xffffffffu, lane >= W || d == SL.sd[lane < W ? lane : 0]);
+  double a[S], b[S];
+#pragma unroll
+  for (int i = 0; i < S; ++i) a[i] = b[i] = 0.0;
+  if (std_slice) {
+    // copy the windows: buffer row br of window w is stage row r0 + wstart_w + br - wbase_w
+    const int64_t lim = m * S;
+    for (int g = 0; g < SL.total; g += 32 * kWinBatch) {
+      double v[kWinBatch][S];
+#pragma unroll
+      for (int c = 0; c < kWinBatch; ++c) {
+        const int br = g + c * 32 + lane;
+        int sh = 0;
+#pragma unroll
+        for (int w = 0; w < 16; ++w)
+          if (w < SL.nwin && br >= SL.wbase[w]) sh = SL.wstart[w] - SL.wbase[w];
+        const int64_t g0 = (r0 + br + sh) * S;
+        const bool in = br < SL.total && g0 >= 0 && g0 < lim;
+#pragma unroll
+        for (int i = 0; i < S; ++i) v[c][i] = in ? __ldg(Y + g0 + i) : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < kWinBatch; ++c) {
+        const int br = g + c * 32 + lane;
+        if (br < SL.total) {
+#pragma unroll
+          for (int i = 0; i < S; ++i) buf[br * SP + i] = v[c][i];
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const double* yr = buf + (SL.srow[k] + lane) * SP;
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        const double y = yr[i];
+        a[i] += mv[k] * y;
+        b[i] += kv[k] * y;
+      }
+    }
+  } else if (r < m) {
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const int c = sell_col_at(colhdr, sell_col, q0 + k, base + k * kSlice + lane, r);
+      const double* yc = Y + (int64_t)c * S;
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        const double y = __ldg(yc + i);
+        a[i] += mv[k] * y;
+        b[i] += kv[k] * y;
+      }
+    }
+  }
+  if (r >= m) return;
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    double o = 0.0, t = 0.0;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      o += cf.c1[i * S + j] * a[j];
+      t += cf.c2[i * S + j] * b[j];
+    }
+    Out[r * S + i] = flagged ? Y[r * S + i] : o + dt * t;
+  }
+}
+
+// host: window layout of a sorted stencil (the win_layout rule)
+static bool stencil_layout(const std::vector<int>& sd, StLayout& L) {
+  const int W = (int)sd.size();
+  if (W < 1 || W > 16) return false;
+  L = StLayout{};
+  int nw = 0, total = 0, start = 0;
+  std::vector<int> win(W);
+  for (int k = 0; k < W; ++k) {
+    if (k == 0 || sd[k] < sd[k - 1] || sd[k] - sd[k - 1] > kWinGap) {
+      if (k > 0) {
+        L.wend[nw - 1] = L.wbase[nw - 1] + (sd[k - 1] - L.wstart[nw - 1]) + kSlice;
+        total = L.wend[nw - 1];
+      }
+      if (nw == 16) return false;
+      L.wstart[nw] = sd[k];
+      L.wbase[nw] = total;
+      start = k;
+      ++nw;
+    }
+    win[k] = nw - 1;
+  }
+  (void)start;
+  L.wend[nw - 1] = L.wbase[nw - 1] + (sd[W - 1] - L.wstart[nw - 1]) + kSlice;
+  total = L.wend[nw - 1];
+  L.nwin = nw;
+  L.total = total;
+  for (int k = 0; k < W; ++k) {
+    L.srow[k] = L.wbase[win[k]] + sd[k] - L.wstart[win[k]];
+    L.sd[k] = sd[k];
+  }
+  return true;
 }
 
 // Semilinear per-stage Jacobian K_i = kscale K + M diag(D_i):
@@ -639,6 +776,46 @@ int irk_stage_apply(irk_ctx* ctx, int s, const double* C1_host, const double* C2
                           m, P->slice_ptr, P->sell_col, M->val, kp, cf, dt, rowmask_dev, \
                           Y_dev, Out_dev, P->ellw)))
   static const bool win_off = getenv("IRK_NO_WINDOW") != nullptr;
+  static const bool std_off = getenv("IRK_NO_STD_WINDOW") != nullptr;
+  // stencil patterns: precomputed window layout
+  if (!per && !win_off && !std_off && s <= 4 && P->ellw > 0 &&
+      (int)P->stencil.size() == P->ellw && (P->ellw == 7 || P->ellw == 15 || P->ellw == 3)) {
+    StLayout SL;
+    if (stencil_layout(P->stencil, SL)) {
+      const size_t smem = (size_t)(kBlock / 32) * SL.total * (s % 2 == 0 ? s + 1 : s) *
+                          sizeof(double);
+      if (smem <= 96 * 1024) {
+        const int64_t ns = P->nslices;
+        const unsigned gw = (unsigned)((ns + kBlock / 32 - 1) / (kBlock / 32));
+        static bool attr_done = false;
+        if (!attr_done) {
+          for (int ss = 1; ss <= 4; ++ss) {
+#define IRK_STD_ATTR(W)                                                                   \
+  IRK_STAGE_SWITCH4(ss, (cudaFuncSetAttribute(k_stage_apply_std<SS, W>,                   \
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                              96 * 1024)))
+            IRK_STD_ATTR(3) IRK_STD_ATTR(7) IRK_STD_ATTR(15)
+#undef IRK_STD_ATTR
+          }
+          attr_done = true;
+        }
+#define IRK_LAUNCH_STD(W)                                                                     \
+  IRK_STAGE_SWITCH4(s, (k_stage_apply_std<SS, W><<<gw, kBlock, smem, ctx->stream>>>(          \
+                          m, ns, SL, P->sell_col, P->colhdr, M->val, kp.k[0], cf, dt,         \
+                          rowmask_dev, Y_dev, Out_dev)))
+        if (P->ellw == 7) {
+          IRK_LAUNCH_STD(7)
+        } else if (P->ellw == 15) {
+          IRK_LAUNCH_STD(15)
+        } else {
+          IRK_LAUNCH_STD(3)
+        }
+#undef IRK_LAUNCH_STD
+        IRK_CHECK_LAUNCH(ctx);
+        return IRK_OK;
+      }
+    }
+  }
   const int wrows = P->win_rows;
   const size_t wsmem = (size_t)(kBlock / 32) * wrows * (s % 2 == 0 ? s + 1 : s) * sizeof(double);
   constexpr size_t kWinSmemMax = 96 * 1024;
