@@ -273,7 +273,7 @@ struct StLayout {
   int sd[16];                           // stencil offsets
 };
 
-template <int S, int W>
+template <int S, int W, int NW>
 __global__ void __launch_bounds__(kBlock, W <= 8 ? 3 : 2)
     k_stage_apply_std(int64_t m, int64_t nslices, const StLayout SL,
                       const int* __restrict__ sell_col, const int* __restrict__ colhdr,
@@ -311,8 +311,8 @@ __global__ void __launch_bounds__(kBlock, W <= 8 ? 3 : 2)
         const int br = g + c * 32 + lane;
         int sh = 0;
 #pragma unroll
-        for (int w = 0; w < 16; ++w)
-          if (w < SL.nwin && br >= SL.wbase[w]) sh = SL.wstart[w] - SL.wbase[w];
+        for (int w = 0; w < NW; ++w)
+          if (br >= SL.wbase[w]) sh = SL.wstart[w] - SL.wbase[w];
         const int64_t g0 = (r0 + br + sh) * S;
         const bool in = br < SL.total && g0 >= 0 && g0 < lim;
 #pragma unroll
@@ -790,25 +790,33 @@ int irk_stage_apply(irk_ctx* ctx, int s, const double* C1_host, const double* C2
         static bool attr_done = false;
         if (!attr_done) {
           for (int ss = 1; ss <= 4; ++ss) {
-#define IRK_STD_ATTR(W)                                                                   \
-  IRK_STAGE_SWITCH4(ss, (cudaFuncSetAttribute(k_stage_apply_std<SS, W>,                   \
+#define IRK_STD_ATTR(W, NW)                                                                 \
+  IRK_STAGE_SWITCH4(ss, (cudaFuncSetAttribute(k_stage_apply_std<SS, W, NW>,                 \
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                               96 * 1024)))
-            IRK_STD_ATTR(3) IRK_STD_ATTR(7) IRK_STD_ATTR(15)
+            IRK_STD_ATTR(3, 1) IRK_STD_ATTR(7, 3) IRK_STD_ATTR(15, 8)
 #undef IRK_STD_ATTR
           }
           attr_done = true;
         }
-#define IRK_LAUNCH_STD(W)                                                                     \
-  IRK_STAGE_SWITCH4(s, (k_stage_apply_std<SS, W><<<gw, kBlock, smem, ctx->stream>>>(          \
+#define IRK_LAUNCH_STD(W, NW)                                                                 \
+  IRK_STAGE_SWITCH4(s, (k_stage_apply_std<SS, W, NW><<<gw, kBlock, smem, ctx->stream>>>(      \
                           m, ns, SL, P->sell_col, P->colhdr, M->val, kp.k[0], cf, dt,         \
                           rowmask_dev, Y_dev, Out_dev)))
-        if (P->ellw == 7) {
-          IRK_LAUNCH_STD(7)
-        } else if (P->ellw == 15) {
-          IRK_LAUNCH_STD(15)
+        // window-lookup unrolled over NW >= SL.nwin windows (extra entries
+        // repeat the last window's base, so they never match first)
+        for (int w = SL.nwin; w < 16; ++w) {
+          SL.wbase[w] = 1 << 30;
+          SL.wstart[w] = 0;
+        }
+        if (P->ellw == 7 && SL.nwin <= 3) {
+          IRK_LAUNCH_STD(7, 3)
+        } else if (P->ellw == 15 && SL.nwin <= 8) {
+          IRK_LAUNCH_STD(15, 8)
+        } else if (P->ellw == 3 && SL.nwin <= 1) {
+          IRK_LAUNCH_STD(3, 1)
         } else {
-          IRK_LAUNCH_STD(3)
+          goto generic_window;
         }
 #undef IRK_LAUNCH_STD
         IRK_CHECK_LAUNCH(ctx);
@@ -816,6 +824,7 @@ int irk_stage_apply(irk_ctx* ctx, int s, const double* C1_host, const double* C2
       }
     }
   }
+generic_window:
   const int wrows = P->win_rows;
   const size_t wsmem = (size_t)(kBlock / 32) * wrows * (s % 2 == 0 ? s + 1 : s) * sizeof(double);
   constexpr size_t kWinSmemMax = 96 * 1024;
