@@ -189,7 +189,7 @@ def inner_solve_profile(wl, reps=20):
     st, prob = wl.stepper, wl.problem
     if st.formulation.name == "DIRK":
         fac = st._dirk_factor(st.tableau.A[0, 0], prob)
-        sett = st.dirk_solver if hasattr(st, "dirk_solver") else fac.settings
+        sett = getattr(st, "dirk_solver", None) or fac.settings
     else:
         pc = st._preconditioner(_SPLIT[st.formulation], prob)
         if pc is None or pc.kind.name == "SCHUR":
