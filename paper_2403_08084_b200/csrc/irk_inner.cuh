@@ -105,6 +105,7 @@ struct alignas(16) SysState {
   int done;
   int iter;
   int fresh;  // 1: written by the init kernel, no iteration decided yet
+  int skip;   // external preconditioner: this iteration's z is not needed
 };
 
 struct MatView {
@@ -742,7 +743,8 @@ __global__ void __launch_bounds__(kBlock)
 // (real, one system).  Same grid as the A/B kernels.
 static __global__ void __launch_bounds__(kBlock)
     k_cg_dot_rz(int64_t m, const double* __restrict__ r, const double* __restrict__ z,
-                double* red, int c) {
+                double* red, int c, const int* skip) {
+  if (skip && *skip) return;
   double v = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -773,6 +775,20 @@ static __global__ void __launch_bounds__(kBlock)
         st->done = 1;
       }
     }
+  }
+}
+
+// After the update kernel of an iteration with an external preconditioner:
+// decide from the ||r||^2 partials (same reduction order as the next A
+// kernel) whether that A kernel will end the solve (converged, cap,
+// non-finite); then the preconditioner application and r.z are skipped.
+static __global__ void __launch_bounds__(kBlock)
+    k_cg_skip(SysState<double>* st, const double* red, int G, int c, int maxit) {
+  __shared__ double srr[1];
+  reduce_partials<double, 1>(cg_part<double, 1>(const_cast<double*>(red), G, c).rr, G, srr);
+  if (threadIdx.x == 0) {
+    const double rr = srr[0];
+    st->skip = st->done || !st->active[0] || !(rr > st->tol2[0]) || st->its[0] + 1 >= maxit;
   }
 }
 
@@ -984,8 +1000,11 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
         IRK_CHECK_LAUNCH(ctx);
         double* rr_ = reinterpret_cast<double*>(w.r);
         double* zz_ = reinterpret_cast<double*>(w.z);
-        IRK_TRY(prec->apply(ctx, cs, rr_, zz_, &(c ? st1 : st0)->done));
-        k_cg_dot_rz<<<G, kBlock, 0, cs>>>(m, rr_, zz_, red, c);
+        SysState<double>* sc = reinterpret_cast<SysState<double>*>(c ? st1 : st0);
+        k_cg_skip<<<1, kBlock, 0, cs>>>(sc, red, G, c, maxit);
+        IRK_CHECK_LAUNCH(ctx);
+        IRK_TRY(prec->apply(ctx, cs, rr_, zz_, &sc->skip));
+        k_cg_dot_rz<<<G, kBlock, 0, cs>>>(m, rr_, zz_, red, c, &sc->skip);
         IRK_CHECK_LAUNCH(ctx);
         return IRK_OK;
       }
