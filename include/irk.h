@@ -334,6 +334,12 @@ int irk_mg_create(irk_ctx* ctx, int dim, int nlev, const int64_t* N_host,
 int irk_mg_destroy(irk_mg* mg);
 /* z = V(r): one V-cycle from a zero start (r != z). */
 int irk_mg_vcycle(irk_ctx* ctx, irk_mg* mg, const double* r_dev, double* z_dev);
+/* Structured 2D path (matrix-free stencil tile kernels, chosen at create
+ * time when every level is a verified 2D grid stencil with the full-boundary
+ * Dirichlet set and nu == 2; env IRK_MG_GENERIC disables it): switch it on
+ * (IRK_EINVAL when unavailable) or off, and query the hierarchy. */
+int irk_mg_set_structured(irk_mg* mg, int on);
+int irk_mg_info(const irk_mg* mg, int* nlev, int* structured);
 /* CG on the level-0 block preconditioned by one V-cycle per iteration;
  * strided rhs/x as irk_pcg; status as irk_pcg. */
 int irk_mg_pcg(irk_ctx* ctx, irk_mg* mg, const double* rhs_dev, int64_t ld_rhs, double* x_dev,

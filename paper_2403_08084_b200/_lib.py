@@ -88,6 +88,8 @@ _SIGS = {
     "irk_mg_create": [_vp, _int, _int, _vp, _vp, _vp, _int, _int, _vp],
     "irk_mg_destroy": [_vp],
     "irk_mg_vcycle": [_vp, _vp, _vp, _vp],
+    "irk_mg_set_structured": [_vp, _int],
+    "irk_mg_info": [_vp, _vp, _vp],
     "irk_mg_pcg": [_vp, _vp, _vp, _i64, _vp, _i64, _dbl, _dbl, _int, _vp, _vp],
 }
 _RESTYPES = {

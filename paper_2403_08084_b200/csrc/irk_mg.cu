@@ -273,6 +273,580 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Structured 2D path (P1/Q1 grid blocks with the full-boundary Dirichlet
+// set, nu = 2): every level operator is ONE 3x3 stencil on the interior
+// (boundary rows identity, boundary columns eliminated), read from the
+// assembled level matrix and verified against it at setup.  A V-cycle level
+// is then three matrix-free tile kernels with shared-memory halos instead of
+// seven gather kernels:
+//   k_mg2_pre      x2 = two Chebyshev steps from zero      (reads b,     writes x2)
+//   k_mg2_restrict b_c = P^T (b - A x2)                     (reads b, x2, writes b_c)
+//   k_mg2_post     z = two Chebyshev steps from x2 + P e_c  (reads b, x2, e_c, writes z)
+// (16-24 B per fine point each instead of ~244 B over the seven kernels),
+// and the coarsest level is one single-CTA kernel holding the grid in
+// shared memory.  Same arithmetic as the generic path up to summation order.
+struct Sten2 {
+  double c[3][3];  // c[dy + 1][dx + 1]: coefficient of the neighbour (x+dx, y+dy)
+  double dinv;     // 1 / c[1][1]
+};
+
+struct Cheb2 {
+  double cr0, cd1, cr1;  // the two steps of a 2-step Chebyshev smoother (cd0 = 0)
+};
+
+constexpr int kMaxCoarse = 64;
+struct ChebN {
+  int n;
+  double cd[kMaxCoarse], cr[kMaxCoarse];
+};
+
+// sum_{dx,dy} c[dy][dx] s[i + dy*W + dx] (zero coefficients skipped at
+// compile time for the P1 diagonal-edge layout: (1,-1) and (-1,1) are 0)
+template <bool F9>
+__device__ __forceinline__ double sten_apply(const Sten2& S, const double* s, int i, int W) {
+  double acc = S.c[1][1] * s[i];
+  acc += S.c[1][0] * s[i - 1] + S.c[1][2] * s[i + 1];
+  acc += S.c[0][1] * s[i - W] + S.c[2][1] * s[i + W];
+  acc += S.c[0][0] * s[i - W - 1] + S.c[2][2] * s[i + W + 1];
+  if (F9) acc += S.c[0][2] * s[i - W + 1] + S.c[2][0] * s[i + W - 1];
+  return acc;
+}
+
+__device__ __forceinline__ bool interior2(int gx, int gy, int N) {
+  return gx >= 1 && gx < N && gy >= 1 && gy < N;
+}
+
+// region [gx0, gx0 + W) x [gy0, gy0 + H) of a grid vector, zero outside the
+// interior (eliminated boundary columns / outside the grid): element
+// k = threadIdx.x + j * kBlock into v[j].  All loads are issued before any
+// use (memory-level parallelism: one round trip per region, not per element).
+template <int W, int H>
+struct Region {
+  static constexpr int kN = W * H;
+  static constexpr int kPer = (kN + kBlock - 1) / kBlock;
+  __device__ __forceinline__ static void load(double (&v)[kPer], const double* __restrict__ src,
+                                              int n1, int gx0, int gy0) {
+    const int N = n1 - 1;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int k = threadIdx.x + j * kBlock;
+      const int gx = gx0 + k % W, gy = gy0 + k / W;
+      v[j] = (k < kN && interior2(gx, gy, N)) ? src[(int64_t)gy * n1 + gx] : 0.0;
+    }
+  }
+  __device__ __forceinline__ static void store(double* dst, const double (&v)[kPer]) {
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int k = threadIdx.x + j * kBlock;
+      if (k < kN) dst[k] = v[j];
+    }
+  }
+};
+
+// Tiles cover the interior-anchored ranges [1 + T t, 1 + T (t+1)) in each
+// direction (clipped to [0, N]); the boundary lines x = 0 / y = 0 are written
+// by the first tile row/column.  f(gx, gy, lx, ly) for each owned grid point
+// (lx, ly: position in the tile, -1 on the boundary lines x = 0 / y = 0).
+template <int TX, int TY, typename F>
+__device__ __forceinline__ void for_tile_points(int N, F&& f) {
+  static_assert((TX * TY) % kBlock == 0, "tile must be a multiple of the block");
+  const int x0 = 1 + TX * blockIdx.x, y0 = 1 + TY * blockIdx.y;
+#pragma unroll
+  for (int j = 0; j < TX * TY / kBlock; ++j) {
+    const int k = threadIdx.x + j * kBlock;
+    const int lx = k % TX, ly = k / TX;
+    const int gx = x0 + lx, gy = y0 + ly;
+    if (gx <= N && gy <= N) f(gx, gy, lx, ly);
+  }
+  if (blockIdx.x == 0)
+    for (int j = threadIdx.x; j < TY; j += kBlock)
+      if (y0 + j <= N) f(0, y0 + j, -1, j);
+  if (blockIdx.y == 0)
+    for (int i = threadIdx.x; i < TX; i += kBlock)
+      if (x0 + i <= N) f(x0 + i, 0, i, -1);
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) f(0, 0, -1, -1);
+}
+
+// x2 = two Chebyshev steps from zero on b (boundary rows: x2 = b):
+//   x1 = cr0 D^-1 b,  x2 = (1 + cd1) x1 + cr1 D^-1 (b - A x1)
+template <int TX, int TY, bool F9>
+__global__ void __launch_bounds__(kBlock)
+    k_mg2_pre(int n1, Sten2 S, Cheb2 C, const double* __restrict__ b, double* __restrict__ x2,
+              const int* stop) {
+  if (stop && *stop) return;
+  constexpr int W = TX + 2, H = TY + 2;
+  using R = Region<W, H>;
+  __shared__ double sb[W * H];
+  const int N = n1 - 1;
+  const int gx0 = TX * blockIdx.x, gy0 = TY * blockIdx.y;  // region origin (halo 1)
+  {
+    double v[R::kPer];
+    R::load(v, b, n1, gx0, gy0);
+    R::store(sb, v);
+  }
+  __syncthreads();
+  const double s0 = C.cr0 * S.dinv;
+  for_tile_points<TX, TY>(N, [&](int gx, int gy, int lx, int ly) {
+    const int64_t g = (int64_t)gy * n1 + gx;
+    if (!interior2(gx, gy, N)) {
+      x2[g] = b[g];
+      return;
+    }
+    const int i = (ly + 1) * W + lx + 1;
+    const double bi = sb[i];
+    const double x1 = s0 * bi;
+    const double ax1 = s0 * sten_apply<F9>(S, sb, i, W);
+    x2[g] = (1.0 + C.cd1) * x1 + C.cr1 * S.dinv * (bi - ax1);
+  });
+}
+
+// b_c = P^T r on the coarse tile, r = b - A x2 on the fine interior (0 on the
+// boundary); coarse boundary rows 0.  Fine point f = 2c + p: P^T weights 1
+// (p = 0) and 1/2 for the six P1 edge neighbours 2c +- (1,0), (0,1), (1,1).
+template <int CX, int CY, bool F9>
+__global__ void __launch_bounds__(kBlock)
+    k_mg2_restrict(int n1f, int n1c, Sten2 S, const double* __restrict__ bf,
+                   const double* __restrict__ x2, double* __restrict__ bc, const int* stop) {
+  if (stop && *stop) return;
+  constexpr int RW = 2 * CX + 1, RH = 2 * CY + 1;  // residual region
+  constexpr int XW = RW + 2, XH = RH + 2;          // x2 region (halo 1)
+  using RX = Region<XW, XH>;
+  using RB = Region<RW, RH>;
+  __shared__ double sx[XW * XH];
+  __shared__ double sr[RW * RH];
+  const int Nc = n1c - 1;
+  const int cx0 = 1 + CX * blockIdx.x, cy0 = 1 + CY * blockIdx.y;
+  const int rx0 = 2 * cx0 - 1, ry0 = 2 * cy0 - 1;
+  double vb[RB::kPer];
+  {
+    double vx[RX::kPer];
+    RX::load(vx, x2, n1f, rx0 - 1, ry0 - 1);
+    RB::load(vb, bf, n1f, rx0, ry0);  // zero on the boundary: r = 0 there
+    RX::store(sx, vx);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < RB::kPer; ++j) {
+    const int k = threadIdx.x + j * kBlock;
+    if (k < RB::kN) {
+      const int lx = k % RW, ly = k / RW;
+      const bool in = interior2(rx0 + lx, ry0 + ly, n1f - 1);
+      sr[k] = in ? vb[j] - sten_apply<F9>(S, sx, (ly + 1) * XW + lx + 1, XW) : 0.0;
+    }
+  }
+  __syncthreads();
+  for_tile_points<CX, CY>(Nc, [&](int gx, int gy, int, int) {
+    double v = 0.0;
+    if (interior2(gx, gy, Nc)) {
+      const int i = (2 * gy - ry0) * RW + (2 * gx - rx0);
+      v = sr[i] + 0.5 * (sr[i - 1] + sr[i + 1] + sr[i - RW] + sr[i + RW] + sr[i - RW - 1] +
+                         sr[i + RW + 1]);
+    }
+    bc[(int64_t)gy * n1c + gx] = v;
+  });
+}
+
+// z = two Chebyshev steps from x_p = x2 + P e_c:
+//   x_a = x_p + cr0 D^-1 (b - A x_p),  z = x_a + cd1 (x_a - x_p) + cr1 D^-1 (b - A x_a)
+// boundary rows z = b.  x_p is formed on the tile + halo 2, x_a on halo 1.
+template <int TX, int TY, bool F9>
+__global__ void __launch_bounds__(kBlock)
+    k_mg2_post(int n1, int n1c, Sten2 S, Cheb2 C, const double* __restrict__ b,
+               const double* __restrict__ x2, const double* __restrict__ ec,
+               double* __restrict__ z, const int* stop) {
+  if (stop && *stop) return;
+  constexpr int PW = TX + 4, PH = TY + 4;  // x_p region
+  constexpr int AW = TX + 2, AH = TY + 2;  // x_a region
+  using RP = Region<PW, PH>;
+  using RA = Region<AW, AH>;
+  __shared__ double sp[PW * PH];
+  __shared__ double sa[AW * AH];
+  __shared__ double sb[AW * AH];
+  const int N = n1 - 1;
+  const int ax0 = TX * blockIdx.x, ay0 = TY * blockIdx.y;  // x_a region origin
+  const int px0 = ax0 - 1, py0 = ay0 - 1;
+  double vb[RA::kPer];
+  {
+    double vx[RP::kPer], e0[RP::kPer], e1[RP::kPer];
+    RA::load(vb, b, n1, ax0, ay0);
+#pragma unroll
+    for (int j = 0; j < RP::kPer; ++j) {
+      const int k = threadIdx.x + j * kBlock;
+      const int gx = px0 + k % PW, gy = py0 + k / PW;
+      vx[j] = e0[j] = e1[j] = 0.0;
+      if (k < RP::kN && interior2(gx, gy, N)) {
+        const int64_t c = (int64_t)(gy >> 1) * n1c + (gx >> 1);
+        vx[j] = x2[(int64_t)gy * n1 + gx];
+        e0[j] = ec[c];
+        e1[j] = ec[c + (int64_t)(gy & 1) * n1c + (gx & 1)];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < RP::kPer; ++j) {
+      const int k = threadIdx.x + j * kBlock;
+      const int gx = px0 + k % PW, gy = py0 + k / PW;
+      const bool odd = ((gx | gy) & 1) != 0;
+      if (k < RP::kN) sp[k] = vx[j] + (odd ? 0.5 * (e0[j] + e1[j]) : e0[j]);
+    }
+    RA::store(sb, vb);
+  }
+  __syncthreads();
+  const double s0 = C.cr0 * S.dinv;
+#pragma unroll
+  for (int j = 0; j < RA::kPer; ++j) {
+    const int k = threadIdx.x + j * kBlock;
+    if (k < RA::kN) {
+      const int lx = k % AW, ly = k / AW;
+      const int i = (ly + 1) * PW + lx + 1;
+      sa[k] = interior2(ax0 + lx, ay0 + ly, N)
+                  ? sp[i] + s0 * (vb[j] - sten_apply<F9>(S, sp, i, PW))
+                  : 0.0;
+    }
+  }
+  __syncthreads();
+  for_tile_points<TX, TY>(N, [&](int gx, int gy, int lx, int ly) {
+    const int64_t g = (int64_t)gy * n1 + gx;
+    if (!interior2(gx, gy, N)) {
+      z[g] = b[g];
+      return;
+    }
+    const int ia = (ly + 1) * AW + lx + 1;
+    const int ip = (ly + 2) * PW + lx + 2;
+    const double xa = sa[ia];
+    z[g] = xa + C.cd1 * (xa - sp[ip]) + C.cr1 * S.dinv * (sb[ia] - sten_apply<F9>(S, sa, ia, AW));
+  });
+}
+
+// Coarsest level: C.n Chebyshev steps from zero in ONE CTA (1024 threads,
+// up to PPT grid points per thread); the iterate lives in shared memory
+// (two zero-bordered n1 x n1 buffers), b / x / d of the owned points in
+// registers.
+template <int PPT, bool F9>
+__global__ void __launch_bounds__(1024, 1)
+    k_mg2_coarse(int n1, Sten2 S, ChebN C, const double* __restrict__ b, double* __restrict__ z,
+                 const int* stop) {
+  if (stop && *stop) return;
+  extern __shared__ double sm[];
+  const int N = n1 - 1, m = n1 * n1;
+  double* buf[2] = {sm, sm + m};
+  double bi[PPT], xi[PPT], di[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int g = threadIdx.x + p * 1024;
+    bi[p] = g < m ? b[g] : 0.0;
+    xi[p] = 0.0;
+    di[p] = 0.0;
+  }
+  for (int g = threadIdx.x; g < 2 * m; g += 1024) sm[g] = 0.0;
+  __syncthreads();
+  int cur = 0;
+  for (int k = 0; k < C.n; ++k) {
+    const double* xs = buf[cur];
+    double* xo = buf[cur ^ 1];
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) {
+      const int g = threadIdx.x + p * 1024;
+      if (g >= m) continue;
+      const int gx = g % n1, gy = g / n1;
+      if (!interior2(gx, gy, N)) {
+        xi[p] = bi[p];
+        continue;  // stays 0 in the shared iterate (eliminated column)
+      }
+      const double res = bi[p] - (k ? sten_apply<F9>(S, xs, g, n1) : 0.0);
+      const double dn = (k ? C.cd[k] * di[p] : 0.0) + C.cr[k] * S.dinv * res;
+      di[p] = dn;
+      xi[p] += dn;
+      xo[g] = xi[p];
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int g = threadIdx.x + p * 1024;
+    if (g < m) z[g] = xi[p];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Coarse-level tail: the levels from `lt` (<= ~70K points) down to the
+// coarsest run as ONE launch of one thread-block cluster (16 CTAs x 1024
+// threads when the GPU admits it, else 8); phases are separated by cluster
+// barriers (hardware, ~0.2 us, release/acquire at cluster scope) instead of
+// kernel boundaries (~3 us each in a graph).  Data stays in global memory
+// (L2-resident at these sizes); every level buffer is zero on the boundary
+// except where b itself is not (level lt == 0), so the neighbour loads test
+// interior2().  Phases per level: pre, residual, restriction, two post steps;
+// the coarsest level's Chebyshev steps ping-pong between two buffers.
+constexpr int kTailMax = 10;
+struct TailLevel {
+  int n1;
+  Sten2 S;
+  Cheb2 C;
+  const double* b;  // rhs (level lt: the caller's)
+  double* x2;       // pre-smoothed iterate; coarsest: ping buffer
+  double* r;        // residual; coarsest: pong buffer
+  double* xa;       // first post-smoothing step
+  double* z;        // result (level lt: the caller's output)
+};
+struct TailParams {
+  int nlev;  // levels in the tail (the last is the coarsest)
+  TailLevel L[kTailMax];
+  ChebN cn;
+};
+
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <bool F9>
+__device__ __forceinline__ double sten_global(const Sten2& S, const double* __restrict__ v, int n1,
+                                              int gx, int gy) {
+  const int N = n1 - 1;
+  auto at = [&](int dx, int dy) {
+    const int x = gx + dx, y = gy + dy;
+    return interior2(x, y, N) ? v[(int64_t)y * n1 + x] : 0.0;
+  };
+  double acc = S.c[1][1] * at(0, 0);
+  acc += S.c[1][0] * at(-1, 0) + S.c[1][2] * at(1, 0);
+  acc += S.c[0][1] * at(0, -1) + S.c[2][1] * at(0, 1);
+  acc += S.c[0][0] * at(-1, -1) + S.c[2][2] * at(1, 1);
+  if (F9) acc += S.c[0][2] * at(1, -1) + S.c[2][0] * at(-1, 1);
+  return acc;
+}
+
+// x_p = x2 + P e at an interior fine point (zero elsewhere)
+__device__ __forceinline__ double xp_at(const double* __restrict__ x2,
+                                        const double* __restrict__ ec, int n1, int n1c, int gx,
+                                        int gy) {
+  if (!interior2(gx, gy, n1 - 1)) return 0.0;
+  const int64_t c = (int64_t)(gy >> 1) * n1c + (gx >> 1);
+  const double e0 = ec[c];
+  const double e = ((gx | gy) & 1) ? 0.5 * (e0 + ec[c + (int64_t)(gy & 1) * n1c + (gx & 1)]) : e0;
+  return x2[(int64_t)gy * n1 + gx] + e;
+}
+
+template <bool F9>
+__global__ void __launch_bounds__(1024, 1)
+    k_mg2_tail(const __grid_constant__ TailParams P, const int* stop) {
+  if (stop && *stop) return;  // uniform over the cluster
+  const int T = gridDim.x * blockDim.x;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  // descend
+  for (int l = 0; l + 1 < P.nlev; ++l) {
+    const TailLevel& L = P.L[l];
+    const int n1 = L.n1, N = n1 - 1, m = n1 * n1;
+    const double s0 = L.C.cr0 * L.S.dinv;
+    for (int g = tid; g < m; g += T) {
+      const int gx = g % n1, gy = g / n1;
+      const double bi = L.b[g];
+      if (!interior2(gx, gy, N)) {
+        L.x2[g] = bi;
+        continue;
+      }
+      const double x1 = s0 * bi;
+      const double ax1 = s0 * sten_global<F9>(L.S, L.b, n1, gx, gy);
+      L.x2[g] = (1.0 + L.C.cd1) * x1 + L.C.cr1 * L.S.dinv * (bi - ax1);
+    }
+    cluster_barrier();
+    for (int g = tid; g < m; g += T) {
+      const int gx = g % n1, gy = g / n1;
+      L.r[g] = interior2(gx, gy, N) ? L.b[g] - sten_global<F9>(L.S, L.x2, n1, gx, gy) : 0.0;
+    }
+    cluster_barrier();
+    const TailLevel& Cc = P.L[l + 1];
+    const int n1c = Cc.n1, Nc = n1c - 1, mc = n1c * n1c;
+    double* bc = const_cast<double*>(Cc.b);
+    for (int g = tid; g < mc; g += T) {
+      const int cx = g % n1c, cy = g / n1c;
+      double v = 0.0;
+      if (interior2(cx, cy, Nc)) {
+        const double* r = L.r + (int64_t)(2 * cy) * n1 + 2 * cx;
+        v = r[0] + 0.5 * (r[-1] + r[1] + r[-n1] + r[n1] + r[-n1 - 1] + r[n1 + 1]);
+      }
+      bc[g] = v;
+    }
+    cluster_barrier();
+  }
+  // coarsest: x_{k+1} = x_k + cd_k (x_k - x_{k-1}) + cr_k D^-1 (b - A x_k)
+  {
+    const TailLevel& L = P.L[P.nlev - 1];
+    const int n1 = L.n1, N = n1 - 1, m = n1 * n1;
+    double* buf[2] = {L.x2, L.r};
+    for (int k = 0; k < P.cn.n; ++k) {
+      const double* xk = buf[(k + 1) & 1];  // x_k (unused at k = 0)
+      double* xo = buf[k & 1];              // holds x_{k-1}, receives x_{k+1}
+      for (int g = tid; g < m; g += T) {
+        const int gx = g % n1, gy = g / n1;
+        const double bi = L.b[g];
+        if (!interior2(gx, gy, N)) {
+          xo[g] = bi;
+          continue;
+        }
+        double xn;
+        if (k == 0) {
+          xn = P.cn.cr[0] * L.S.dinv * bi;
+        } else {
+          const double x = xk[g];
+          const double xm = k == 1 ? 0.0 : xo[g];
+          xn = x + P.cn.cd[k] * (x - xm) +
+               P.cn.cr[k] * L.S.dinv * (bi - sten_global<F9>(L.S, xk, n1, gx, gy));
+        }
+        xo[g] = xn;
+      }
+      cluster_barrier();
+    }
+    if (P.nlev == 1) {  // the tail is only the coarsest level: copy out
+      const double* res = buf[(P.cn.n - 1) & 1];
+      for (int g = tid; g < m; g += T) L.z[g] = res[g];
+      return;
+    }
+  }
+  // ascend
+  for (int l = P.nlev - 2; l >= 0; --l) {
+    const TailLevel& L = P.L[l];
+    const TailLevel& Cc = P.L[l + 1];
+    const int n1 = L.n1, N = n1 - 1, m = n1 * n1, n1c = Cc.n1;
+    const double* ec = (l + 2 == P.nlev) ? (((P.cn.n - 1) & 1) ? Cc.r : Cc.x2) : Cc.z;
+    const double s0 = L.C.cr0 * L.S.dinv;
+    for (int g = tid; g < m; g += T) {
+      const int gx = g % n1, gy = g / n1;
+      if (!interior2(gx, gy, N)) {
+        L.xa[g] = 0.0;
+        continue;
+      }
+      double ap = L.S.c[1][1] * xp_at(L.x2, ec, n1, n1c, gx, gy);
+      ap += L.S.c[1][0] * xp_at(L.x2, ec, n1, n1c, gx - 1, gy) +
+            L.S.c[1][2] * xp_at(L.x2, ec, n1, n1c, gx + 1, gy);
+      ap += L.S.c[0][1] * xp_at(L.x2, ec, n1, n1c, gx, gy - 1) +
+            L.S.c[2][1] * xp_at(L.x2, ec, n1, n1c, gx, gy + 1);
+      ap += L.S.c[0][0] * xp_at(L.x2, ec, n1, n1c, gx - 1, gy - 1) +
+            L.S.c[2][2] * xp_at(L.x2, ec, n1, n1c, gx + 1, gy + 1);
+      if (F9)
+        ap += L.S.c[0][2] * xp_at(L.x2, ec, n1, n1c, gx + 1, gy - 1) +
+              L.S.c[2][0] * xp_at(L.x2, ec, n1, n1c, gx - 1, gy + 1);
+      L.xa[g] = xp_at(L.x2, ec, n1, n1c, gx, gy) + s0 * (L.b[g] - ap);
+    }
+    cluster_barrier();
+    for (int g = tid; g < m; g += T) {
+      const int gx = g % n1, gy = g / n1;
+      const double bi = L.b[g];
+      if (!interior2(gx, gy, N)) {
+        L.z[g] = bi;
+        continue;
+      }
+      const double xa = L.xa[g];
+      L.z[g] = xa + L.C.cd1 * (xa - xp_at(L.x2, ec, n1, n1c, gx, gy)) +
+               L.C.cr1 * L.S.dinv * (bi - sten_global<F9>(L.S, L.xa, n1, gx, gy));
+    }
+    if (l > 0) cluster_barrier();
+  }
+}
+
+// Stencil of an interior row of a level matrix: out[(dy+1)*3 + dx+1] for the
+// entries of `row` at columns row + dx + n1 dy (|dx|, |dy| <= 1); err[0] = 1
+// when the row has any other column.
+__global__ void k_mg2_row_stencil(MatView A, int64_t row, int n1, double* out, int* err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int k = 0; k < 9; ++k) out[k] = 0.0;
+  const int64_t sl = row / kSlice;
+  const int lane = (int)(row % kSlice);
+  int base, width;
+  if (A.ellw) {
+    base = (int)(sl * kSlice * A.ellw);
+    width = A.ellw;
+  } else {
+    base = A.slice_ptr[sl];
+    width = (A.slice_ptr[sl + 1] - base) / kSlice;
+  }
+  const int q0 = base / kSlice;
+  for (int k = 0; k < width; ++k) {
+    const int pos = base + k * kSlice + lane;
+    const int c = sell_col_at(A.colhdr, A.sell_col, q0 + k, pos, row);
+    const double v = sell_val_at(A.ua, A.a, q0 + k, pos);
+    const int64_t d = (int64_t)c - row;
+    int hit = -1;
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx)
+        if (d == dx + (int64_t)dy * n1) hit = (dy + 1) * 3 + dx + 1;
+    if (hit >= 0)
+      out[hit] += v;
+    else if (v != 0.0)
+      err[0] = 1;
+  }
+}
+
+// max_i |(A v)_i - (S v)_i| and max_i |(A v)_i| over all rows for the
+// pseudo-random v_i = sin(0.37 i + 0.11) (block maxima into part[2 * block])
+__global__ void __launch_bounds__(kBlock)
+    k_mg2_verify(MatView A, int n1, Sten2 S, const uint8_t* __restrict__ mask, double* part) {
+  const int N = n1 - 1;
+  const int64_t m = (int64_t)n1 * n1;
+  double emax = 0.0, amax = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int gx = (int)(i % n1), gy = (int)(i / n1);
+    const bool in = interior2(gx, gy, N);
+    if (in == (mask[i] != 0)) {  // the mask must be exactly the boundary
+      emax = INFINITY;
+      continue;
+    }
+    // A v through the SELL arrays
+    const int64_t sl = i / kSlice;
+    const int lane = (int)(i % kSlice);
+    int base, width;
+    if (A.ellw) {
+      base = (int)(sl * kSlice * A.ellw);
+      width = A.ellw;
+    } else {
+      base = __ldg(A.slice_ptr + sl);
+      width = (__ldg(A.slice_ptr + sl + 1) - base) / kSlice;
+    }
+    const int q0 = base / kSlice;
+    double av = 0.0;
+    for (int k = 0; k < width; ++k) {
+      const int pos = base + k * kSlice + lane;
+      const int c = sell_col_at(A.colhdr, A.sell_col, q0 + k, pos, i);
+      av += sell_val_at(A.ua, A.a, q0 + k, pos) * sin(0.37 * c + 0.11);
+    }
+    double sv;
+    if (!in) {
+      sv = sin(0.37 * i + 0.11);  // identity row
+    } else {
+      sv = 0.0;
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int x = gx + dx, y = gy + dy;
+          if (interior2(x, y, N)) sv += S.c[dy + 1][dx + 1] * sin(0.37 * ((int64_t)y * n1 + x) + 0.11);
+        }
+    }
+    emax = fmax(emax, fabs(av - sv));
+    amax = fmax(amax, fabs(av));
+  }
+  __shared__ double re[kBlock / 32], ra[kBlock / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  }
+  if (lane == 0) {
+    re[warp] = emax;
+    ra[warp] = amax;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double e = 0.0, a = 0.0;
+    for (int w = 0; w < kBlock / 32; ++w) {
+      e = fmax(e, re[w]);
+      a = fmax(a, ra[w]);
+    }
+    part[2 * blockIdx.x] = e;
+    part[2 * blockIdx.x + 1] = a;
+  }
+}
+
 struct MgLevel {
   int64_t m = 0;
   GridIdx g{};
@@ -297,6 +871,16 @@ struct irk_mg : public irk::CgPrec {
   std::vector<irk::MgLevel> lev;
   std::vector<const irk_mat*> mats;
   double* mem = nullptr;
+  // structured 2D path (see k_mg2_*): available / in use
+  bool s2_ok = false, s2_on = false;
+  std::vector<irk::Sten2> sten;
+  std::vector<bool> f9;
+  std::vector<irk::Cheb2> c2;  // per level (lmax differs)
+  irk::ChebN cn{};
+  // cluster tail: levels >= tail_lev run in one k_mg2_tail launch of
+  // tail_cl CTAs (0: no tail, every level as tile kernels)
+  int tail_lev = -1, tail_cl = 0;
+  irk::TailParams tp{};
 
   // Chebyshev coefficients (cd_k, cr_k) of steps k = 0..n-1 on [lo, hi]
   static void cheb(double lo, double hi, int n, std::vector<double>& cd, std::vector<double>& cr) {
@@ -379,8 +963,221 @@ struct irk_mg : public irk::CgPrec {
     return smooth(ctx, s, l, b, c, nu, 0.25, out, stop);
   }
 
+  // structured 2D V-cycle: z_l = V_l(b_l) (see the k_mg2_* kernels)
+  int vcycle2(irk_ctx* ctx, cudaStream_t s, int l, const double* b, double* out,
+              const int* stop) {
+    using namespace irk;
+    const MgLevel& L = lev[l];
+    const int n1 = (int)L.g.n1, N = n1 - 1;
+    const Sten2& S = sten[l];
+    const Cheb2 C2 = l < (int)c2.size() ? c2[l] : Cheb2{};
+    const bool F = f9[l];
+    if (tail_cl > 0 && l == tail_lev) {
+      TailParams P = tp;
+      P.L[0].b = b;
+      P.L[0].z = out;
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(tail_cl);
+      cfg.blockDim = dim3(1024);
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = tail_cl;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const cudaError_t e = F ? cudaLaunchKernelEx(&cfg, k_mg2_tail<true>, P, stop)
+                              : cudaLaunchKernelEx(&cfg, k_mg2_tail<false>, P, stop);
+      ctx->launches++;
+      return e == cudaSuccess ? IRK_OK : IRK_ECUDA;
+    }
+    if (l == (int)lev.size() - 1) {
+      const int ppt = (int)((L.m + 1023) / 1024);
+      const size_t sh = 2 * (size_t)L.m * sizeof(double);
+#define IRK_CO(P)                                                                           \
+  (F ? k_mg2_coarse<P, true><<<1, 1024, sh, s>>>(n1, S, cn, b, out, stop)                  \
+     : k_mg2_coarse<P, false><<<1, 1024, sh, s>>>(n1, S, cn, b, out, stop))
+      if (ppt <= 1) IRK_CO(1);
+      else if (ppt <= 2) IRK_CO(2);
+      else if (ppt <= 4) IRK_CO(4);
+      else IRK_CO(8);
+#undef IRK_CO
+      ctx->launches++;
+      return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
+    }
+    const MgLevel& Cc = lev[l + 1];
+    const int n1c = (int)Cc.g.n1, Nc = n1c - 1;
+    double* x2 = L.x[0];
+    const bool big = N >= 512;
+    const dim3 gb((N + 63) / 64, (N + 15) / 16), gs((N + 31) / 32, (N + 7) / 8);
+    if (big) {
+      if (F) k_mg2_pre<64, 16, true><<<gb, kBlock, 0, s>>>(n1, S, C2, b, x2, stop);
+      else k_mg2_pre<64, 16, false><<<gb, kBlock, 0, s>>>(n1, S, C2, b, x2, stop);
+    } else {
+      if (F) k_mg2_pre<32, 8, true><<<gs, kBlock, 0, s>>>(n1, S, C2, b, x2, stop);
+      else k_mg2_pre<32, 8, false><<<gs, kBlock, 0, s>>>(n1, S, C2, b, x2, stop);
+    }
+    const dim3 gr((Nc + 31) / 32, (Nc + 7) / 8);
+    if (F) k_mg2_restrict<32, 8, true><<<gr, kBlock, 0, s>>>(n1, n1c, S, b, x2, Cc.b, stop);
+    else k_mg2_restrict<32, 8, false><<<gr, kBlock, 0, s>>>(n1, n1c, S, b, x2, Cc.b, stop);
+    ctx->launches += 2;
+    if (cudaPeekAtLastError() != cudaSuccess) return IRK_ECUDA;
+    IRK_TRY(vcycle2(ctx, s, l + 1, Cc.b, Cc.x[1], stop));
+    const double* ec = Cc.x[1];
+    if (big) {
+      if (F) k_mg2_post<64, 16, true><<<gb, kBlock, 0, s>>>(n1, n1c, S, C2, b, x2, ec, out, stop);
+      else k_mg2_post<64, 16, false><<<gb, kBlock, 0, s>>>(n1, n1c, S, C2, b, x2, ec, out, stop);
+    } else {
+      if (F) k_mg2_post<32, 8, true><<<gs, kBlock, 0, s>>>(n1, n1c, S, C2, b, x2, ec, out, stop);
+      else k_mg2_post<32, 8, false><<<gs, kBlock, 0, s>>>(n1, n1c, S, C2, b, x2, ec, out, stop);
+    }
+    ctx->launches++;
+    return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
+  }
+
+  // Enable the structured path when every level is a verified 2D stencil
+  // operator with the full-boundary Dirichlet set (else keep the generic one).
+  int setup_s2(irk_ctx* ctx) {
+    using namespace irk;
+    s2_ok = false;
+    const int nl = (int)lev.size();
+    if (dim != 2 || nu != 2 || ncoarse > kMaxCoarse) return IRK_OK;
+    if (lev.back().m > 8 * 1024) return IRK_OK;
+    for (const MgLevel& L : lev)
+      if (!L.mask || L.g.n1 - 1 < 4 || L.g.n1 > 46341) return IRK_OK;
+    IRK_TRY(ensure_red(ctx, 2 * (size_t)ctx->num_sms * 4 + 64));
+    sten.assign(nl, Sten2{});
+    f9.assign(nl, false);
+    for (int l = 0; l < nl; ++l) {
+      const MgLevel& L = lev[l];
+      const int n1 = (int)L.g.n1, N = n1 - 1;
+      int* err = (int*)ctx->counters + (kNumCounters - 2);
+      IRK_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
+      k_mg2_row_stencil<<<1, 32, 0, ctx->stream>>>(L.A, (int64_t)(N / 2) * n1 + N / 2, n1,
+                                                    ctx->red, err);
+      IRK_CHECK_LAUNCH(ctx);
+      double c[9];
+      int herr = 0;
+      IRK_CUDA(cudaMemcpyAsync(c, ctx->red, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+      IRK_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (herr || !(c[4] != 0.0) || !std::isfinite(c[4])) return IRK_OK;
+      Sten2& S = sten[l];
+      for (int k = 0; k < 9; ++k) S.c[k / 3][k % 3] = c[k];
+      S.dinv = 1.0 / c[4];
+      f9[l] = c[2] != 0.0 || c[6] != 0.0;
+      const int G = ctx->num_sms * 4;
+      k_mg2_verify<<<G, kBlock, 0, ctx->stream>>>(L.A, n1, S, L.mask, ctx->red);
+      IRK_CHECK_LAUNCH(ctx);
+      std::vector<double> part(2 * G);
+      IRK_CUDA(cudaMemcpyAsync(part.data(), ctx->red, part.size() * sizeof(double),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+      IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+      double e = 0.0, a = 0.0;
+      for (int b = 0; b < G; ++b) {
+        e = std::fmax(e, part[2 * b]);
+        a = std::fmax(a, part[2 * b + 1]);
+      }
+      if (!(e <= 1e-12 * a)) return IRK_OK;
+    }
+    // Chebyshev coefficients, as smooth(): [lmax/4, lmax] on the fine
+    // levels, [0.05 lmax, lmax] with ncoarse steps on the coarsest
+    c2.assign(nl, Cheb2{});
+    std::vector<double> cd, cr;
+    for (int l = 0; l + 1 < nl; ++l) {
+      cheb(0.25 * lev[l].lmax, lev[l].lmax, 2, cd, cr);
+      c2[l] = Cheb2{cr[0], cd[1], cr[1]};
+    }
+    cheb(0.05 * lev.back().lmax, lev.back().lmax, ncoarse, cd, cr);
+    cn.n = ncoarse;
+    for (int k = 0; k < ncoarse; ++k) {
+      cn.cd[k] = cd[k];
+      cn.cr[k] = cr[k];
+    }
+    s2_ok = true;
+    setup_tail();
+    return IRK_OK;
+  }
+
+  // The cluster tail covers the levels with at most kTailPts points (when
+  // there are at least two of them and the GPU schedules a 16- or 8-CTA
+  // cluster of 1024-thread CTAs).  Opt-in (env IRK_MG_TAIL): measured on
+  // B200 (config 2) the global-memory phases cost ~1.5 us each, so the tail
+  // (25 phases) is slower than the 10 tile kernels it replaces (V-cycle
+  // 87.6 vs 62.3 us).
+  void setup_tail() {
+    using namespace irk;
+    static const bool off = getenv("IRK_MG_TAIL") == nullptr;
+    constexpr int64_t kTailPts = 70000;
+    tail_cl = 0;
+    tail_lev = -1;
+    const int nl = (int)lev.size();
+    int lt = nl;
+    while (lt > 0 && lev[lt - 1].m <= kTailPts) --lt;
+    if (off || nl - lt < 2 || nl - lt > kTailMax) return;
+    bool any9 = false;
+    for (int l = lt; l < nl; ++l) any9 = any9 || f9[l];
+    for (int cl : {16, 8}) {
+      const void* fn = any9 ? (const void*)k_mg2_tail<true> : (const void*)k_mg2_tail<false>;
+      if (cl > 8 &&
+          cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+              cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(cl);
+      cfg.blockDim = dim3(1024);
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cl;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, fn, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        nc = 0;
+      }
+      if (nc >= 1) {
+        tail_cl = cl;
+        break;
+      }
+    }
+    if (!tail_cl) return;
+    tail_lev = lt;
+    tp = TailParams{};
+    tp.nlev = nl - lt;
+    for (int l = lt; l < nl; ++l) {
+      TailLevel& T = tp.L[l - lt];
+      const MgLevel& L = lev[l];
+      T.n1 = (int)L.g.n1;
+      T.S = sten[l];
+      T.C = c2[l];
+      T.b = L.b;
+      T.x2 = L.x[0];
+      T.r = L.r;
+      T.xa = L.d;
+      T.z = L.x[1];
+    }
+    tp.cn = cn;
+    // a mixed F9 tail uses the 9-point kernel everywhere (zero entries)
+    if (any9)
+      for (int l = lt; l < nl; ++l) f9[l] = true;
+  }
+
   int apply(irk_ctx* ctx, cudaStream_t s, const double* r, double* z,
             const int* stop) override {
+    if (s2_on) {
+      const int e = vcycle2(ctx, s, 0, r, z, stop);
+      if (e != IRK_OK || cudaGetLastError() != cudaSuccess) {
+        irk::set_error("irk_mg: structured V-cycle launch failed");
+        return IRK_ECUDA;
+      }
+      return IRK_OK;
+    }
     const int c = vcycle(ctx, s, 0, r, z, stop);
     if (c < 0 || cudaGetLastError() != cudaSuccess) {
       irk::set_error("irk_mg: V-cycle launch failed");
@@ -479,7 +1276,48 @@ int irk_mg_create(irk_ctx* ctx, int dim, int nlev, const int64_t* N_host,
     L.lmax = mx;
   }
   for (int l = 0; l < nlev; ++l) mg->mats.push_back(A_levels[l]);
+  {
+    const int e = mg->setup_s2(ctx);
+    if (e != IRK_OK) {
+      delete mg;
+      return e;
+    }
+    static const bool generic = getenv("IRK_MG_GENERIC") != nullptr;
+    mg->s2_on = mg->s2_ok && !generic;
+    if (mg->s2_ok) {
+      // dynamic shared memory of the single-CTA coarsest kernel (2 buffers)
+      const int sh4 = 2 * 4 * 1024 * (int)sizeof(double);
+      const int sh8 = 2 * 8 * 1024 * (int)sizeof(double);
+      IRK_CUDA(cudaFuncSetAttribute(k_mg2_coarse<4, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sh4));
+      IRK_CUDA(cudaFuncSetAttribute(k_mg2_coarse<4, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sh4));
+      IRK_CUDA(cudaFuncSetAttribute(k_mg2_coarse<8, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sh8));
+      IRK_CUDA(cudaFuncSetAttribute(k_mg2_coarse<8, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sh8));
+    }
+  }
   *out = mg;
+  return IRK_OK;
+}
+
+int irk_mg_set_structured(irk_mg* mg, int on) {
+  IRK_REQUIRE(mg, "irk_mg_set_structured: NULL argument");
+  IRK_REQUIRE(!on || mg->s2_ok,
+              "irk_mg_set_structured: no structured path for this hierarchy (needs 2D levels "
+              "with the full-boundary Dirichlet set, nu = 2, a coarsest level <= 8192 points)");
+  if ((on != 0) != mg->s2_on) {
+    mg->s2_on = on != 0;
+    mg->uid = g_mg_uid.fetch_add(1);  // cached graphs hold the other kernel sequence
+  }
+  return IRK_OK;
+}
+
+int irk_mg_info(const irk_mg* mg, int* nlev, int* structured) {
+  IRK_REQUIRE(mg, "irk_mg_info: NULL argument");
+  if (nlev) *nlev = (int)mg->lev.size();
+  if (structured) *structured = mg->s2_on ? 1 : 0;
   return IRK_OK;
 }
 

@@ -586,6 +586,17 @@ class _MgHierarchy:
     def levels(self):
         return len(self._keep[0])
 
+    @property
+    def structured(self) -> bool:
+        """True when the V-cycle runs the matrix-free 2D stencil kernels."""
+        on = C.c_int()
+        call("irk_mg_info", self.handle, None, C.byref(on))
+        return bool(on.value)
+
+    @structured.setter
+    def structured(self, on: bool):
+        call("irk_mg_set_structured", self.handle, int(bool(on)))
+
 
 class BlockFactorization:
     """Stage block alpha*M + dt*K with Dirichlet identity rows/columns,

@@ -359,6 +359,47 @@ def test_mg_vcycle_is_symmetric(cuda, irk):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n,beta", [(64, 2e-3), (128, 1e-3), (1024, 4e-4)])
+def test_mg_structured_vcycle_matches_generic(cuda, irk, n, beta):
+    """The matrix-free 2D stencil V-cycle (k_mg2_*) computes the generic
+    gather V-cycle (k_mg_*) up to summation order, stays symmetric, and the
+    MG-PCG solve converges in the same number of iterations."""
+    from paper_2403_08084_b200 import _lib
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd, fac = _p1_block(irk, 2, n, 1.0, beta)
+    mg = fac._mg
+    assert mg is not None and mg.structured
+    rng = np.random.default_rng(5)
+    a = la.to_dev(rng.standard_normal(M.nrows))
+    b = la.to_dev(rng.standard_normal(M.nrows))
+    lib = _lib.load()
+
+    def vc(v):
+        out = la.dev_empty(M.nrows)
+        assert lib.irk_mg_vcycle(_lib.ctx(), mg.handle, _lib.ptr(v), _lib.ptr(out)) == 0
+        return out
+
+    za, zb = vc(a), vc(b)
+    mg.structured = False
+    ga = vc(a)
+    rhs = rng.standard_normal(M.nrows)
+    x_gen = fac.solve(rhs)
+    its_gen = fac.last_iterations
+    mg.structured = True
+    x_st = fac.solve(rhs)
+    assert float(torch_norm(za - ga)) <= 1e-12 * float(torch_norm(ga))
+    x, y = float((za * b).sum()), float((a * zb).sum())
+    assert abs(x - y) <= 1e-12 * max(abs(x), 1.0)
+    assert rel(x_st, x_gen) < 1e-10
+    assert abs(fac.last_iterations - its_gen) <= 1
+
+
+def torch_norm(t):
+    return t.double().norm()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("dim,n,beta", [(2, 32, 5e-3), (2, 64, 1e-2), (3, 16, 5e-3)])
 def test_mg_pcg_solves_block(cuda, irk, oracle, dim, n, beta):
     import scipy.sparse.linalg as spla
