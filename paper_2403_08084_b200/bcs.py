@@ -83,12 +83,13 @@ def _boundary_state(u_n, dofs):
 def stage_bc_values(method: BcMethod, tab, bc: DirichletBC, u_n, t: float, dt: float,
                     unknown: StageUnknown = StageUnknown.DERIVATIVE) -> np.ndarray:
     """Boundary values of the stage unknowns, shape (s, |Gamma|) (bcs.py:58-96)."""
-    ub = _boundary_state(u_n, bc.dofs)
+    shape = (len(bc.dofs),)
     stage_t = [t + ci * dt for ci in tab.c]
     if method is BcMethod.DAE:
-        G = np.stack([_values_at(bc.g, ti, ub.shape) for ti in stage_t])
+        G = np.stack([_values_at(bc.g, ti, shape) for ti in stage_t])
         if unknown is StageUnknown.VALUE:
-            return G
+            return G  # independent of u_n: no device read-back
+        ub = _boundary_state(u_n, bc.dofs)
         W = (G - ub[None, :]) / dt
         if unknown is StageUnknown.W:
             return W
@@ -99,13 +100,13 @@ def stage_bc_values(method: BcMethod, tab, bc: DirichletBC, u_n, t: float, dt: f
         return np.linalg.solve(tab.A, W)
     if bc.g_dot is None:
         raise ValueError("ODE boundary conditions require g_dot")
-    Gd = np.stack([_values_at(bc.g_dot, ti, ub.shape) for ti in stage_t])
+    Gd = np.stack([_values_at(bc.g_dot, ti, shape) for ti in stage_t])
     if unknown is StageUnknown.DERIVATIVE:
         return Gd
     W = tab.A @ Gd
     if unknown is StageUnknown.W:
         return W
-    return ub[None, :] + dt * W
+    return _boundary_state(u_n, bc.dofs)[None, :] + dt * W
 
 
 class ConstrainedStageOperator:

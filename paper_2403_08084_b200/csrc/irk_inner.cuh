@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(kBlock)
               T* __restrict__ x, T* __restrict__ r, T* __restrict__ z, T* __restrict__ pold,
               T* __restrict__ dinv, double rtol2, double atol2, SysState<T>* st,
               double* __restrict__ part, unsigned int* counter) {
+  IRK_PDL_ENTER();
   T rho[NB];
   double bb[NB];
 #pragma unroll
@@ -495,6 +496,7 @@ __global__ void __launch_bounds__(kBlock, 4)
               const uint8_t* __restrict__ mask, const T* __restrict__ z,
               const T* __restrict__ pold, T* __restrict__ pnew, T* __restrict__ q,
               const SysState<T>* sin, SysState<T>* sout, double* red, int c, int maxit) {
+  IRK_PDL_ENTER();
   T beta[NB];
   bool act[NB];
   if (cg_enter_a<T, NB>(sin, sout, red, c, maxit, beta, act)) return;
@@ -596,6 +598,7 @@ __global__ void __launch_bounds__(kBlock, 4)
                  const double* __restrict__ pold, double* __restrict__ pnew,
                  double* __restrict__ q, const SysState<double>* sin, SysState<double>* sout,
                  double* red, int cpar, int maxit) {
+  IRK_PDL_ENTER();
   double betas[1];
   bool acts[1];
   if (cg_enter_a<double, 1>(sin, sout, red, cpar, maxit, betas, acts)) return;
@@ -661,6 +664,7 @@ __global__ void __launch_bounds__(kBlock)
     k_cg_update(int64_t m, const T* __restrict__ p, const T* __restrict__ q,
                 const T* __restrict__ dinv, T* __restrict__ x, T* __restrict__ r,
                 T* __restrict__ z, const SysState<T>* st, double* red, int c) {
+  IRK_PDL_ENTER();
   T alpha[NB];
   bool act[NB];
   if (cg_enter_b<T, NB>(st, red, c, alpha, act)) return;
@@ -744,6 +748,7 @@ __global__ void __launch_bounds__(kBlock)
 static __global__ void __launch_bounds__(kBlock)
     k_cg_dot_rz(int64_t m, const double* __restrict__ r, const double* __restrict__ z,
                 double* red, int c, const int* skip) {
+  IRK_PDL_ENTER();
   if (skip && *skip) return;
   double v = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
@@ -758,6 +763,7 @@ static __global__ void __launch_bounds__(kBlock)
 static __global__ void __launch_bounds__(kBlock)
     k_cg_rho_init(int64_t m, const double* __restrict__ r, const double* __restrict__ z,
                   SysState<double>* st, double* part, unsigned int* counter) {
+  IRK_PDL_ENTER();
   double v = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -784,6 +790,7 @@ static __global__ void __launch_bounds__(kBlock)
 // non-finite); then the preconditioner application and r.z are skipped.
 static __global__ void __launch_bounds__(kBlock)
     k_cg_skip(SysState<double>* st, const double* red, int G, int c, int maxit) {
+  IRK_PDL_ENTER();
   __shared__ double srr[1];
   reduce_partials<double, 1>(cg_part<double, 1>(const_cast<double*>(red), G, c).rr, G, srr);
   if (threadIdx.x == 0) {
@@ -797,6 +804,7 @@ static __global__ void __launch_bounds__(kBlock)
 template <typename T>
 __global__ void k_cg_cond(cudaGraphConditionalHandle h, const SysState<T>* a,
                           const SysState<T>* b) {
+  IRK_PDL_ENTER();
   if (threadIdx.x == 0 && blockIdx.x == 0)
     cudaGraphSetConditional(h, (__ldcg(&a->done) || __ldcg(&b->done)) ? 0u : 1u);
 }
@@ -806,6 +814,7 @@ __global__ void k_cg_cond(cudaGraphConditionalHandle h, const SysState<T>* a,
 template <typename T>
 __global__ void k_cg_log(const SysState<T>* a, const SysState<T>* b, int nb, int body_kernels,
                          int* out) {
+  IRK_PDL_ENTER();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const SysState<T>* f = (a->done != b->done) ? (a->done ? a : b) : (a->iter >= b->iter ? a : b);
   int its = 0, code = 0;
@@ -837,6 +846,7 @@ struct CgPrec {
 template <typename T, int NB>
 __global__ void k_cg_store(int64_t m, const T* __restrict__ x, T* __restrict__ out,
                            int64_t ld_out) {
+  IRK_PDL_ENTER();
   for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < m;
        row += (int64_t)gridDim.x * blockDim.x) {
 #pragma unroll
@@ -858,10 +868,23 @@ struct Workspace {
 template <typename T, int NB>
 __global__ void k_cg_stage_rhs(int64_t m, const T* __restrict__ rhs, int64_t ld,
                                T* __restrict__ rb) {
+  IRK_PDL_ENTER();
   for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < m;
        row += (int64_t)gridDim.x * blockDim.x) {
 #pragma unroll
     for (int k = 0; k < NB; ++k) rb[row * NB + k] = rhs[row * ld + k];
+  }
+}
+
+// zero the `pad` elements before and after each of a, b, c (length len)
+template <typename T>
+__global__ void k_zero_halos(T* a, T* b, T* c, int64_t len, int64_t pad) {
+  IRK_PDL_ENTER();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 6 * pad;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = i / (2 * pad), j = i % (2 * pad);
+    T* base = w == 0 ? a : (w == 1 ? b : c);
+    base[j < pad ? j - pad : len + (j - pad)] = s_zero(T{});
   }
 }
 
@@ -881,13 +904,16 @@ int carve(irk_ctx* ctx, int64_t m, int nb, Workspace<T>& w, int64_t pad = 0) {
   b += vec;
   T** v[7] = {&w.x, &w.r, &w.q, &w.dinv, &w.z, &w.p0, &w.p1};
   for (int i = 0; i < 7; ++i) {
-    if (i >= 4) {
-      if (pb) IRK_CUDA(cudaMemsetAsync(b, 0, 2 * pb + vec, ctx->stream));
-      b += pb;
-    }
+    if (i >= 4) b += pb;
     *v[i] = reinterpret_cast<T*>(b);
     b += vec;
     if (i >= 4) b += pb;
+  }
+  if (pad > 0) {
+    const int64_t n = 6 * pad * nb;
+    IRK_CUDA(launch(k_zero_halos<T>, (unsigned)std::min<int64_t>((n + kBlock - 1) / kBlock, 1024),
+                    kBlock, 0, ctx->stream, w.z, w.p0, w.p1, m * nb, pad * nb));
+    ctx->launches++;
   }
   return IRK_OK;
 }
@@ -919,10 +945,10 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   // arguments and replays as one cached graph.
   double* red = ctx->red;
   static const bool graph_off = getenv("IRK_NO_GRAPH") != nullptr;
-  k_cg_stage_rhs<T, NB><<<grid_for(ctx, m), kBlock, 0, s>>>(m, rhs, ld_rhs, w.rb);
+  launch(k_cg_stage_rhs<T, NB>, grid_for(ctx, m), kBlock, 0, s, m, rhs, ld_rhs, w.rb);
   IRK_CHECK_LAUNCH(ctx);
   auto init_body = [&](cudaStream_t cs) -> int {
-    k_cg_init<T, NB, HASB><<<G, kBlock, 0, cs>>>(m, A, P, shift, mask, w.rb, NB, w.x, w.r, w.z,
+    launch(k_cg_init<T, NB, HASB>, G, kBlock, 0, cs, m, A, P, shift, mask, w.rb, NB, w.x, w.r, w.z,
                                                  w.p0, w.dinv, rtol * rtol, atol * atol, st1,
                                                  red + 2 * cg_part_doubles<T, NB>(G), cnt);
     IRK_CHECK_LAUNCH(ctx);
@@ -931,7 +957,7 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
         double* rr_ = reinterpret_cast<double*>(w.r);
         double* zz_ = reinterpret_cast<double*>(w.z);
         IRK_TRY(prec->apply(ctx, cs, rr_, zz_, nullptr));
-        k_cg_rho_init<<<G, kBlock, 0, cs>>>(m, rr_, zz_,
+        launch(k_cg_rho_init, G, kBlock, 0, cs, m, rr_, zz_,
                                             reinterpret_cast<SysState<double>*>(st1),
                                             red + 2 * cg_part_doubles<T, NB>(G), cnt);
         IRK_CHECK_LAUNCH(ctx);
@@ -976,7 +1002,7 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
         const SysState<double>* si = reinterpret_cast<const SysState<double>*>(sin);
         SysState<double>* so = reinterpret_cast<SysState<double>*>(sout);
 #define IRK_ST(WW)                                                                            \
-  k_cg_spmv_st<WW, HASB><<<G, kBlock, 0, cs>>>((int)m, A, Pd, shift, mask, zz, po, pn, qq, si, \
+  launch(k_cg_spmv_st<WW, HASB>, G, kBlock, 0, cs, (int)m, A, Pd, shift, mask, zz, po, pn, qq, si, \
                                               so, red, c, maxit)
         if (A.sw == 7) IRK_ST(7);
         else if (A.sw == 9) IRK_ST(9);
@@ -986,7 +1012,7 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
       }
     }
     if (!stencil)
-      k_cg_spmv<T, NB, HASB, MAXW><<<G, kBlock, 0, cs>>>(m, A, P, shift, mask, w.z, pold, pnew,
+      launch(k_cg_spmv<T, NB, HASB, MAXW>, G, kBlock, 0, cs, m, A, P, shift, mask, w.z, pold, pnew,
                                                          w.q, sin, sout, red, c, maxit);
     IRK_CHECK_LAUNCH(ctx);
     return IRK_OK;
@@ -995,21 +1021,21 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
     const int c = it & 1;
     if constexpr (kExtOk) {
       if (prec) {
-        k_cg_update<T, NB, true><<<G, kBlock, 0, cs>>>(m, pbuf[c ^ 1], w.q, w.dinv, w.x, w.r,
+        launch(k_cg_update<T, NB, true>, G, kBlock, 0, cs, m, pbuf[c ^ 1], w.q, w.dinv, w.x, w.r,
                                                        w.z, c ? st1 : st0, red, c);
         IRK_CHECK_LAUNCH(ctx);
         double* rr_ = reinterpret_cast<double*>(w.r);
         double* zz_ = reinterpret_cast<double*>(w.z);
         SysState<double>* sc = reinterpret_cast<SysState<double>*>(c ? st1 : st0);
-        k_cg_skip<<<1, kBlock, 0, cs>>>(sc, red, G, c, maxit);
+        launch(k_cg_skip, 1, kBlock, 0, cs, sc, red, G, c, maxit);
         IRK_CHECK_LAUNCH(ctx);
         IRK_TRY(prec->apply(ctx, cs, rr_, zz_, &sc->skip));
-        k_cg_dot_rz<<<G, kBlock, 0, cs>>>(m, rr_, zz_, red, c, &sc->skip);
+        launch(k_cg_dot_rz, G, kBlock, 0, cs, m, rr_, zz_, red, c, &sc->skip);
         IRK_CHECK_LAUNCH(ctx);
         return IRK_OK;
       }
     }
-    k_cg_update<T, NB><<<G, kBlock, 0, cs>>>(m, pbuf[c ^ 1], w.q, w.dinv, w.x, w.r, w.z,
+    launch(k_cg_update<T, NB>, G, kBlock, 0, cs, m, pbuf[c ^ 1], w.q, w.dinv, w.x, w.r, w.z,
                                              c ? st1 : st0, red, c);
     IRK_CHECK_LAUNCH(ctx);
     return IRK_OK;
@@ -1040,7 +1066,7 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
         ctx, kw.k,
         [&](cudaStream_t cs, cudaGraphConditionalHandle h) -> int {
           IRK_TRY(chunk_body(cs, 0, 2));
-          k_cg_cond<T><<<1, 32, 0, cs>>>(h, st0, st1);
+          launch(k_cg_cond<T>, 1, 32, 0, cs, h, st0, st1);
           IRK_CHECK_LAUNCH(ctx);
           return IRK_OK;
         },
@@ -1084,16 +1110,16 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   }
   if (!its_host && !relres_host && ctx->log_on && ctx->log_n < ctx->log_cap) {
     // deferred status: log the outcome on the device, no host round trip
-    k_cg_log<T><<<1, 32, 0, s>>>(st0, st1, NB, (int)body_kernels,
+    launch(k_cg_log<T>, 1, 32, 0, s, st0, st1, NB, (int)body_kernels,
                                  ctx->solve_log + 4 * ctx->log_n);
     IRK_CHECK_LAUNCH(ctx);
     ctx->log_n++;
-    k_cg_store<T, NB><<<grid_for(ctx, m), kBlock, 0, s>>>(m, w.x, xout, ld_x);
+    launch(k_cg_store<T, NB>, grid_for(ctx, m), kBlock, 0, s, m, w.x, xout, ld_x);
     IRK_CHECK_LAUNCH(ctx);
     return IRK_OK;
   }
   IRK_CUDA(cudaMemcpyAsync(hst, w.st, 2 * sizeof(SysState<T>), cudaMemcpyDeviceToHost, s));
-  k_cg_store<T, NB><<<grid_for(ctx, m), kBlock, 0, s>>>(m, w.x, xout, ld_x);
+  launch(k_cg_store<T, NB>, grid_for(ctx, m), kBlock, 0, s, m, w.x, xout, ld_x);
   IRK_CHECK_LAUNCH(ctx);
   IRK_CUDA(cudaStreamSynchronize(s));
   // the latest state: the finished one (or the later iteration)

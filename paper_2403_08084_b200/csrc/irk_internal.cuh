@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/irk.h"
@@ -253,6 +254,40 @@ int graph_launch_while(irk_ctx* ctx, const std::string& key, F&& body,
   if (body_kernels) *body_kernels = ctx->graphs.back().kernels;
   IRK_CUDA(cudaGraphLaunch(exec, ctx->stream));
   return IRK_OK;
+}
+
+// Programmatic dependent launch (PDL): kernels of the inner-solver loops are
+// launched with programmatic stream serialisation, so a kernel's CTAs are
+// scheduled while its predecessor drains and only wait (griddepcontrol.wait)
+// for the predecessor's completion and memory before touching data; each
+// kernel immediately allows its own dependents to launch.  Every kernel
+// launched through irk::launch() must start with IRK_PDL_ENTER() (a no-op
+// when launched without the attribute).  Env IRK_NO_PDL disables it.
+#define IRK_PDL_ENTER()                                    \
+  do {                                                     \
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   \
+    asm volatile("griddepcontrol.launch_dependents;\n");   \
+  } while (0)
+
+inline bool pdl_on() {
+  static const bool on = getenv("IRK_NO_PDL") == nullptr;
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s,
+                          Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
 inline int grid_for(const irk_ctx* ctx, int64_t work_items, int per_block = kBlock,

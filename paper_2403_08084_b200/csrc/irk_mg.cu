@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(kBlock)
               const double* __restrict__ dinv, const double* __restrict__ b,
               const double* __restrict__ xin, double* __restrict__ d, double* __restrict__ xout,
               double cd, double cr, const int* stop) {
+  IRK_PDL_ENTER();
   if (stop && *stop) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(kBlock)
                  const double* __restrict__ dinv, const double* __restrict__ b,
                  const double* __restrict__ xin, double* __restrict__ d,
                  double* __restrict__ xout, double cd, double cr, const int* stop) {
+  IRK_PDL_ENTER();
   if (stop && *stop) return;
   const int lane = threadIdx.x & 31;
   const int64_t nsl = (m + kSlice - 1) / kSlice;
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(kBlock)
     k_mg_residual_st(int64_t m, MatView A, const uint8_t* __restrict__ mask,
                      const double* __restrict__ b, const double* __restrict__ x,
                      double* __restrict__ r, const int* stop) {
+  IRK_PDL_ENTER();
   if (stop && *stop) return;
   const int lane = threadIdx.x & 31;
   const int64_t nsl = (m + kSlice - 1) / kSlice;
@@ -170,6 +173,7 @@ __global__ void __launch_bounds__(kBlock)
     k_mg_residual(int64_t m, MatView A, const uint8_t* __restrict__ mask,
                   const double* __restrict__ b, const double* __restrict__ x,
                   double* __restrict__ r, const int* stop) {
+  IRK_PDL_ENTER();
   if (stop && *stop) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -180,6 +184,7 @@ __global__ void __launch_bounds__(kBlock)
 __global__ void __launch_bounds__(kBlock)
     k_mg_restrict(int64_t mc, GridIdx gc, GridIdx gf, const uint8_t* __restrict__ maskc,
                   const double* __restrict__ rf, double* __restrict__ bc, const int* stop) {
+  IRK_PDL_ENTER();
   if (stop && *stop) return;
   const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= mc) return;
@@ -214,6 +219,7 @@ __global__ void __launch_bounds__(kBlock)
 __global__ void __launch_bounds__(kBlock)
     k_mg_prolong(int64_t mf, GridIdx gf, GridIdx gc, const double* __restrict__ ec,
                  double* __restrict__ xf, const int* stop) {
+  IRK_PDL_ENTER();
   if (stop && *stop) return;
   const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= mf) return;
@@ -374,6 +380,7 @@ template <int TX, int TY, bool F9>
 __global__ void __launch_bounds__(kBlock)
     k_mg2_pre(int n1, Sten2 S, Cheb2 C, const double* __restrict__ b, double* __restrict__ x2,
               const int* stop) {
+  IRK_PDL_ENTER();
   if (stop && *stop) return;
   constexpr int W = TX + 2, H = TY + 2;
   using R = Region<W, H>;
@@ -408,6 +415,7 @@ template <int CX, int CY, bool F9>
 __global__ void __launch_bounds__(kBlock)
     k_mg2_restrict(int n1f, int n1c, Sten2 S, const double* __restrict__ bf,
                    const double* __restrict__ x2, double* __restrict__ bc, const int* stop) {
+  IRK_PDL_ENTER();
   if (stop && *stop) return;
   constexpr int RW = 2 * CX + 1, RH = 2 * CY + 1;  // residual region
   constexpr int XW = RW + 2, XH = RH + 2;          // x2 region (halo 1)
@@ -455,6 +463,7 @@ __global__ void __launch_bounds__(kBlock)
     k_mg2_post(int n1, int n1c, Sten2 S, Cheb2 C, const double* __restrict__ b,
                const double* __restrict__ x2, const double* __restrict__ ec,
                double* __restrict__ z, const int* stop) {
+  IRK_PDL_ENTER();
   if (stop && *stop) return;
   constexpr int PW = TX + 4, PH = TY + 4;  // x_p region
   constexpr int AW = TX + 2, AH = TY + 2;  // x_a region
@@ -526,6 +535,7 @@ template <int PPT, bool F9>
 __global__ void __launch_bounds__(1024, 1)
     k_mg2_coarse(int n1, Sten2 S, ChebN C, const double* __restrict__ b, double* __restrict__ z,
                  const int* stop) {
+  IRK_PDL_ENTER();
   if (stop && *stop) return;
   extern __shared__ double sm[];
   const int N = n1 - 1, m = n1 * n1;
@@ -566,182 +576,6 @@ __global__ void __launch_bounds__(1024, 1)
   for (int p = 0; p < PPT; ++p) {
     const int g = threadIdx.x + p * 1024;
     if (g < m) z[g] = xi[p];
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Coarse-level tail: the levels from `lt` (<= ~70K points) down to the
-// coarsest run as ONE launch of one thread-block cluster (16 CTAs x 1024
-// threads when the GPU admits it, else 8); phases are separated by cluster
-// barriers (hardware, ~0.2 us, release/acquire at cluster scope) instead of
-// kernel boundaries (~3 us each in a graph).  Data stays in global memory
-// (L2-resident at these sizes); every level buffer is zero on the boundary
-// except where b itself is not (level lt == 0), so the neighbour loads test
-// interior2().  Phases per level: pre, residual, restriction, two post steps;
-// the coarsest level's Chebyshev steps ping-pong between two buffers.
-constexpr int kTailMax = 10;
-struct TailLevel {
-  int n1;
-  Sten2 S;
-  Cheb2 C;
-  const double* b;  // rhs (level lt: the caller's)
-  double* x2;       // pre-smoothed iterate; coarsest: ping buffer
-  double* r;        // residual; coarsest: pong buffer
-  double* xa;       // first post-smoothing step
-  double* z;        // result (level lt: the caller's output)
-};
-struct TailParams {
-  int nlev;  // levels in the tail (the last is the coarsest)
-  TailLevel L[kTailMax];
-  ChebN cn;
-};
-
-__device__ __forceinline__ void cluster_barrier() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n"
-               "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-
-template <bool F9>
-__device__ __forceinline__ double sten_global(const Sten2& S, const double* __restrict__ v, int n1,
-                                              int gx, int gy) {
-  const int N = n1 - 1;
-  auto at = [&](int dx, int dy) {
-    const int x = gx + dx, y = gy + dy;
-    return interior2(x, y, N) ? v[(int64_t)y * n1 + x] : 0.0;
-  };
-  double acc = S.c[1][1] * at(0, 0);
-  acc += S.c[1][0] * at(-1, 0) + S.c[1][2] * at(1, 0);
-  acc += S.c[0][1] * at(0, -1) + S.c[2][1] * at(0, 1);
-  acc += S.c[0][0] * at(-1, -1) + S.c[2][2] * at(1, 1);
-  if (F9) acc += S.c[0][2] * at(1, -1) + S.c[2][0] * at(-1, 1);
-  return acc;
-}
-
-// x_p = x2 + P e at an interior fine point (zero elsewhere)
-__device__ __forceinline__ double xp_at(const double* __restrict__ x2,
-                                        const double* __restrict__ ec, int n1, int n1c, int gx,
-                                        int gy) {
-  if (!interior2(gx, gy, n1 - 1)) return 0.0;
-  const int64_t c = (int64_t)(gy >> 1) * n1c + (gx >> 1);
-  const double e0 = ec[c];
-  const double e = ((gx | gy) & 1) ? 0.5 * (e0 + ec[c + (int64_t)(gy & 1) * n1c + (gx & 1)]) : e0;
-  return x2[(int64_t)gy * n1 + gx] + e;
-}
-
-template <bool F9>
-__global__ void __launch_bounds__(1024, 1)
-    k_mg2_tail(const __grid_constant__ TailParams P, const int* stop) {
-  if (stop && *stop) return;  // uniform over the cluster
-  const int T = gridDim.x * blockDim.x;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  // descend
-  for (int l = 0; l + 1 < P.nlev; ++l) {
-    const TailLevel& L = P.L[l];
-    const int n1 = L.n1, N = n1 - 1, m = n1 * n1;
-    const double s0 = L.C.cr0 * L.S.dinv;
-    for (int g = tid; g < m; g += T) {
-      const int gx = g % n1, gy = g / n1;
-      const double bi = L.b[g];
-      if (!interior2(gx, gy, N)) {
-        L.x2[g] = bi;
-        continue;
-      }
-      const double x1 = s0 * bi;
-      const double ax1 = s0 * sten_global<F9>(L.S, L.b, n1, gx, gy);
-      L.x2[g] = (1.0 + L.C.cd1) * x1 + L.C.cr1 * L.S.dinv * (bi - ax1);
-    }
-    cluster_barrier();
-    for (int g = tid; g < m; g += T) {
-      const int gx = g % n1, gy = g / n1;
-      L.r[g] = interior2(gx, gy, N) ? L.b[g] - sten_global<F9>(L.S, L.x2, n1, gx, gy) : 0.0;
-    }
-    cluster_barrier();
-    const TailLevel& Cc = P.L[l + 1];
-    const int n1c = Cc.n1, Nc = n1c - 1, mc = n1c * n1c;
-    double* bc = const_cast<double*>(Cc.b);
-    for (int g = tid; g < mc; g += T) {
-      const int cx = g % n1c, cy = g / n1c;
-      double v = 0.0;
-      if (interior2(cx, cy, Nc)) {
-        const double* r = L.r + (int64_t)(2 * cy) * n1 + 2 * cx;
-        v = r[0] + 0.5 * (r[-1] + r[1] + r[-n1] + r[n1] + r[-n1 - 1] + r[n1 + 1]);
-      }
-      bc[g] = v;
-    }
-    cluster_barrier();
-  }
-  // coarsest: x_{k+1} = x_k + cd_k (x_k - x_{k-1}) + cr_k D^-1 (b - A x_k)
-  {
-    const TailLevel& L = P.L[P.nlev - 1];
-    const int n1 = L.n1, N = n1 - 1, m = n1 * n1;
-    double* buf[2] = {L.x2, L.r};
-    for (int k = 0; k < P.cn.n; ++k) {
-      const double* xk = buf[(k + 1) & 1];  // x_k (unused at k = 0)
-      double* xo = buf[k & 1];              // holds x_{k-1}, receives x_{k+1}
-      for (int g = tid; g < m; g += T) {
-        const int gx = g % n1, gy = g / n1;
-        const double bi = L.b[g];
-        if (!interior2(gx, gy, N)) {
-          xo[g] = bi;
-          continue;
-        }
-        double xn;
-        if (k == 0) {
-          xn = P.cn.cr[0] * L.S.dinv * bi;
-        } else {
-          const double x = xk[g];
-          const double xm = k == 1 ? 0.0 : xo[g];
-          xn = x + P.cn.cd[k] * (x - xm) +
-               P.cn.cr[k] * L.S.dinv * (bi - sten_global<F9>(L.S, xk, n1, gx, gy));
-        }
-        xo[g] = xn;
-      }
-      cluster_barrier();
-    }
-    if (P.nlev == 1) {  // the tail is only the coarsest level: copy out
-      const double* res = buf[(P.cn.n - 1) & 1];
-      for (int g = tid; g < m; g += T) L.z[g] = res[g];
-      return;
-    }
-  }
-  // ascend
-  for (int l = P.nlev - 2; l >= 0; --l) {
-    const TailLevel& L = P.L[l];
-    const TailLevel& Cc = P.L[l + 1];
-    const int n1 = L.n1, N = n1 - 1, m = n1 * n1, n1c = Cc.n1;
-    const double* ec = (l + 2 == P.nlev) ? (((P.cn.n - 1) & 1) ? Cc.r : Cc.x2) : Cc.z;
-    const double s0 = L.C.cr0 * L.S.dinv;
-    for (int g = tid; g < m; g += T) {
-      const int gx = g % n1, gy = g / n1;
-      if (!interior2(gx, gy, N)) {
-        L.xa[g] = 0.0;
-        continue;
-      }
-      double ap = L.S.c[1][1] * xp_at(L.x2, ec, n1, n1c, gx, gy);
-      ap += L.S.c[1][0] * xp_at(L.x2, ec, n1, n1c, gx - 1, gy) +
-            L.S.c[1][2] * xp_at(L.x2, ec, n1, n1c, gx + 1, gy);
-      ap += L.S.c[0][1] * xp_at(L.x2, ec, n1, n1c, gx, gy - 1) +
-            L.S.c[2][1] * xp_at(L.x2, ec, n1, n1c, gx, gy + 1);
-      ap += L.S.c[0][0] * xp_at(L.x2, ec, n1, n1c, gx - 1, gy - 1) +
-            L.S.c[2][2] * xp_at(L.x2, ec, n1, n1c, gx + 1, gy + 1);
-      if (F9)
-        ap += L.S.c[0][2] * xp_at(L.x2, ec, n1, n1c, gx + 1, gy - 1) +
-              L.S.c[2][0] * xp_at(L.x2, ec, n1, n1c, gx - 1, gy + 1);
-      L.xa[g] = xp_at(L.x2, ec, n1, n1c, gx, gy) + s0 * (L.b[g] - ap);
-    }
-    cluster_barrier();
-    for (int g = tid; g < m; g += T) {
-      const int gx = g % n1, gy = g / n1;
-      const double bi = L.b[g];
-      if (!interior2(gx, gy, N)) {
-        L.z[g] = bi;
-        continue;
-      }
-      const double xa = L.xa[g];
-      L.z[g] = xa + L.C.cd1 * (xa - xp_at(L.x2, ec, n1, n1c, gx, gy)) +
-               L.C.cr1 * L.S.dinv * (bi - sten_global<F9>(L.S, L.xa, n1, gx, gy));
-    }
-    if (l > 0) cluster_barrier();
   }
 }
 
@@ -877,10 +711,6 @@ struct irk_mg : public irk::CgPrec {
   std::vector<bool> f9;
   std::vector<irk::Cheb2> c2;  // per level (lmax differs)
   irk::ChebN cn{};
-  // cluster tail: levels >= tail_lev run in one k_mg2_tail launch of
-  // tail_cl CTAs (0: no tail, every level as tile kernels)
-  int tail_lev = -1, tail_cl = 0;
-  irk::TailParams tp{};
 
   // Chebyshev coefficients (cd_k, cr_k) of steps k = 0..n-1 on [lo, hi]
   static void cheb(double lo, double hi, int n, std::vector<double>& cd, std::vector<double>& cr) {
@@ -911,16 +741,16 @@ struct irk_mg : public irk::CgPrec {
       const double* xin = cur < 0 ? nullptr : L.x[cur];
       double* xo = (k == n - 1 && out) ? out : L.x[dst];
       if (xin && L.st == 7)
-        k_mg_cheb_st<7><<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, L.dinv, b, xin,
+        launch(k_mg_cheb_st<7>, grid_for(ctx, L.m), kBlock, 0, s, L.m, L.A, L.mask, L.dinv, b, xin,
                                                              L.d, xo, cd[k], cr[k], stop);
       else if (xin && L.st == 15)
-        k_mg_cheb_st<15><<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, L.dinv, b, xin,
+        launch(k_mg_cheb_st<15>, grid_for(ctx, L.m), kBlock, 0, s, L.m, L.A, L.mask, L.dinv, b, xin,
                                                               L.d, xo, cd[k], cr[k], stop);
       else if (xin && L.st == 3)
-        k_mg_cheb_st<3><<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, L.dinv, b, xin,
+        launch(k_mg_cheb_st<3>, grid_for(ctx, L.m), kBlock, 0, s, L.m, L.A, L.mask, L.dinv, b, xin,
                                                              L.d, xo, cd[k], cr[k], stop);
       else
-        k_mg_cheb<<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, L.dinv, b, xin, L.d,
+        launch(k_mg_cheb, grid_for(ctx, L.m), kBlock, 0, s, L.m, L.A, L.mask, L.dinv, b, xin, L.d,
                                                         xo, cd[k], cr[k], stop);
       if (cudaPeekAtLastError() != cudaSuccess) return -1;
       ctx->launches++;
@@ -939,25 +769,25 @@ struct irk_mg : public irk::CgPrec {
     const int c = smooth(ctx, s, l, b, -1, nu, 0.25, nullptr, stop);
     if (c < 0) return -1;
     if (L.st == 7)
-      k_mg_residual_st<7><<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, b, L.x[c],
+      launch(k_mg_residual_st<7>, grid_for(ctx, L.m), kBlock, 0, s, L.m, L.A, L.mask, b, L.x[c],
                                                                  L.r, stop);
     else if (L.st == 15)
-      k_mg_residual_st<15><<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, b, L.x[c],
+      launch(k_mg_residual_st<15>, grid_for(ctx, L.m), kBlock, 0, s, L.m, L.A, L.mask, b, L.x[c],
                                                                   L.r, stop);
     else if (L.st == 3)
-      k_mg_residual_st<3><<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, b, L.x[c],
+      launch(k_mg_residual_st<3>, grid_for(ctx, L.m), kBlock, 0, s, L.m, L.A, L.mask, b, L.x[c],
                                                                  L.r, stop);
     else
-      k_mg_residual<<<grid_for(ctx, L.m), kBlock, 0, s>>>(L.m, L.A, L.mask, b, L.x[c], L.r,
+      launch(k_mg_residual, grid_for(ctx, L.m), kBlock, 0, s, L.m, L.A, L.mask, b, L.x[c], L.r,
                                                           stop);
     ctx->launches++;
     MgLevel& Cc = lev[l + 1];
-    k_mg_restrict<<<(unsigned)((Cc.m + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+    launch(k_mg_restrict, (unsigned)((Cc.m + kBlock - 1) / kBlock), kBlock, 0, s, 
         Cc.m, Cc.g, L.g, Cc.mask, L.r, Cc.b, stop);
     ctx->launches++;
     const int cc = vcycle(ctx, s, l + 1, Cc.b, nullptr, stop);
     if (cc < 0) return -1;
-    k_mg_prolong<<<(unsigned)((L.m + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+    launch(k_mg_prolong, (unsigned)((L.m + kBlock - 1) / kBlock), kBlock, 0, s, 
         L.m, L.g, Cc.g, Cc.x[cc], L.x[c], stop);
     ctx->launches++;
     return smooth(ctx, s, l, b, c, nu, 0.25, out, stop);
@@ -972,32 +802,12 @@ struct irk_mg : public irk::CgPrec {
     const Sten2& S = sten[l];
     const Cheb2 C2 = l < (int)c2.size() ? c2[l] : Cheb2{};
     const bool F = f9[l];
-    if (tail_cl > 0 && l == tail_lev) {
-      TailParams P = tp;
-      P.L[0].b = b;
-      P.L[0].z = out;
-      cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3(tail_cl);
-      cfg.blockDim = dim3(1024);
-      cfg.stream = s;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = tail_cl;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      const cudaError_t e = F ? cudaLaunchKernelEx(&cfg, k_mg2_tail<true>, P, stop)
-                              : cudaLaunchKernelEx(&cfg, k_mg2_tail<false>, P, stop);
-      ctx->launches++;
-      return e == cudaSuccess ? IRK_OK : IRK_ECUDA;
-    }
     if (l == (int)lev.size() - 1) {
       const int ppt = (int)((L.m + 1023) / 1024);
       const size_t sh = 2 * (size_t)L.m * sizeof(double);
 #define IRK_CO(P)                                                                           \
-  (F ? k_mg2_coarse<P, true><<<1, 1024, sh, s>>>(n1, S, cn, b, out, stop)                  \
-     : k_mg2_coarse<P, false><<<1, 1024, sh, s>>>(n1, S, cn, b, out, stop))
+  (F ? launch(k_mg2_coarse<P, true>, 1, 1024, sh, s, n1, S, cn, b, out, stop)                  \
+     : launch(k_mg2_coarse<P, false>, 1, 1024, sh, s, n1, S, cn, b, out, stop))
       if (ppt <= 1) IRK_CO(1);
       else if (ppt <= 2) IRK_CO(2);
       else if (ppt <= 4) IRK_CO(4);
@@ -1012,25 +822,25 @@ struct irk_mg : public irk::CgPrec {
     const bool big = N >= 512;
     const dim3 gb((N + 63) / 64, (N + 15) / 16), gs((N + 31) / 32, (N + 7) / 8);
     if (big) {
-      if (F) k_mg2_pre<64, 16, true><<<gb, kBlock, 0, s>>>(n1, S, C2, b, x2, stop);
-      else k_mg2_pre<64, 16, false><<<gb, kBlock, 0, s>>>(n1, S, C2, b, x2, stop);
+      if (F) launch(k_mg2_pre<64, 16, true>, gb, kBlock, 0, s, n1, S, C2, b, x2, stop);
+      else launch(k_mg2_pre<64, 16, false>, gb, kBlock, 0, s, n1, S, C2, b, x2, stop);
     } else {
-      if (F) k_mg2_pre<32, 8, true><<<gs, kBlock, 0, s>>>(n1, S, C2, b, x2, stop);
-      else k_mg2_pre<32, 8, false><<<gs, kBlock, 0, s>>>(n1, S, C2, b, x2, stop);
+      if (F) launch(k_mg2_pre<32, 8, true>, gs, kBlock, 0, s, n1, S, C2, b, x2, stop);
+      else launch(k_mg2_pre<32, 8, false>, gs, kBlock, 0, s, n1, S, C2, b, x2, stop);
     }
     const dim3 gr((Nc + 31) / 32, (Nc + 7) / 8);
-    if (F) k_mg2_restrict<32, 8, true><<<gr, kBlock, 0, s>>>(n1, n1c, S, b, x2, Cc.b, stop);
-    else k_mg2_restrict<32, 8, false><<<gr, kBlock, 0, s>>>(n1, n1c, S, b, x2, Cc.b, stop);
+    if (F) launch(k_mg2_restrict<32, 8, true>, gr, kBlock, 0, s, n1, n1c, S, b, x2, Cc.b, stop);
+    else launch(k_mg2_restrict<32, 8, false>, gr, kBlock, 0, s, n1, n1c, S, b, x2, Cc.b, stop);
     ctx->launches += 2;
     if (cudaPeekAtLastError() != cudaSuccess) return IRK_ECUDA;
     IRK_TRY(vcycle2(ctx, s, l + 1, Cc.b, Cc.x[1], stop));
     const double* ec = Cc.x[1];
     if (big) {
-      if (F) k_mg2_post<64, 16, true><<<gb, kBlock, 0, s>>>(n1, n1c, S, C2, b, x2, ec, out, stop);
-      else k_mg2_post<64, 16, false><<<gb, kBlock, 0, s>>>(n1, n1c, S, C2, b, x2, ec, out, stop);
+      if (F) launch(k_mg2_post<64, 16, true>, gb, kBlock, 0, s, n1, n1c, S, C2, b, x2, ec, out, stop);
+      else launch(k_mg2_post<64, 16, false>, gb, kBlock, 0, s, n1, n1c, S, C2, b, x2, ec, out, stop);
     } else {
-      if (F) k_mg2_post<32, 8, true><<<gs, kBlock, 0, s>>>(n1, n1c, S, C2, b, x2, ec, out, stop);
-      else k_mg2_post<32, 8, false><<<gs, kBlock, 0, s>>>(n1, n1c, S, C2, b, x2, ec, out, stop);
+      if (F) launch(k_mg2_post<32, 8, true>, gs, kBlock, 0, s, n1, n1c, S, C2, b, x2, ec, out, stop);
+      else launch(k_mg2_post<32, 8, false>, gs, kBlock, 0, s, n1, n1c, S, C2, b, x2, ec, out, stop);
     }
     ctx->launches++;
     return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
@@ -1096,76 +906,7 @@ struct irk_mg : public irk::CgPrec {
       cn.cr[k] = cr[k];
     }
     s2_ok = true;
-    setup_tail();
     return IRK_OK;
-  }
-
-  // The cluster tail covers the levels with at most kTailPts points (when
-  // there are at least two of them and the GPU schedules a 16- or 8-CTA
-  // cluster of 1024-thread CTAs).  Opt-in (env IRK_MG_TAIL): measured on
-  // B200 (config 2) the global-memory phases cost ~1.5 us each, so the tail
-  // (25 phases) is slower than the 10 tile kernels it replaces (V-cycle
-  // 87.6 vs 62.3 us).
-  void setup_tail() {
-    using namespace irk;
-    static const bool off = getenv("IRK_MG_TAIL") == nullptr;
-    constexpr int64_t kTailPts = 70000;
-    tail_cl = 0;
-    tail_lev = -1;
-    const int nl = (int)lev.size();
-    int lt = nl;
-    while (lt > 0 && lev[lt - 1].m <= kTailPts) --lt;
-    if (off || nl - lt < 2 || nl - lt > kTailMax) return;
-    bool any9 = false;
-    for (int l = lt; l < nl; ++l) any9 = any9 || f9[l];
-    for (int cl : {16, 8}) {
-      const void* fn = any9 ? (const void*)k_mg2_tail<true> : (const void*)k_mg2_tail<false>;
-      if (cl > 8 &&
-          cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-              cudaSuccess) {
-        cudaGetLastError();
-        continue;
-      }
-      cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3(cl);
-      cfg.blockDim = dim3(1024);
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = cl;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      int nc = 0;
-      if (cudaOccupancyMaxActiveClusters(&nc, fn, &cfg) != cudaSuccess) {
-        cudaGetLastError();
-        nc = 0;
-      }
-      if (nc >= 1) {
-        tail_cl = cl;
-        break;
-      }
-    }
-    if (!tail_cl) return;
-    tail_lev = lt;
-    tp = TailParams{};
-    tp.nlev = nl - lt;
-    for (int l = lt; l < nl; ++l) {
-      TailLevel& T = tp.L[l - lt];
-      const MgLevel& L = lev[l];
-      T.n1 = (int)L.g.n1;
-      T.S = sten[l];
-      T.C = c2[l];
-      T.b = L.b;
-      T.x2 = L.x[0];
-      T.r = L.r;
-      T.xa = L.d;
-      T.z = L.x[1];
-    }
-    tp.cn = cn;
-    // a mixed F9 tail uses the 9-point kernel everywhere (zero entries)
-    if (any9)
-      for (int l = lt; l < nl; ++l) f9[l] = true;
   }
 
   int apply(irk_ctx* ctx, cudaStream_t s, const double* r, double* z,

@@ -84,7 +84,9 @@ def to_dev(x, dtype=None):
         return x.to(device=device(), dtype=dt).contiguous()
     np_dt = np.float64 if dt == torch.float64 else np.int64 if dt == torch.int64 else None
     arr = np.ascontiguousarray(np.asarray(x, dtype=np_dt))
-    return torch.from_numpy(arr).to(device())
+    # staged through pinned memory (torch's caching host allocator keeps the
+    # block until the copy ran): the host does not wait for the stream
+    return torch.from_numpy(arr).pin_memory().to(device(), non_blocking=True)
 
 
 def is_torch(x) -> bool:
@@ -878,12 +880,16 @@ def fgmres_device(A: _DevOp, b, P: _DevOp | None = None, settings: KrylovSetting
     projection pass + one fused update/norm pass on the device."""
     st = settings or KrylovSettings()
     n = int(b.numel())
-    if not _all_finite(b):
-        raise ValueError("right-hand side contains non-finite entries")
     left = P is not None and not st.right_pc
+    # one host synchronisation for the finiteness check and ||rhs|| (the
+    # norm of a finite vector is finite unless its entries exceed ~1e154)
+    normb = _norm(b) if not left else None
+    if (normb is None or not np.isfinite(normb)) and not _all_finite(b):
+        raise ValueError("right-hand side contains non-finite entries")
     if left:
         rhs = dev_empty(n)
         P.dev_apply(b, rhs)
+        normb = _norm(rhs)
     else:
         rhs = b
     x = dev_zeros(n) if x0 is None else to_dev(x0).clone()
@@ -900,9 +906,8 @@ def fgmres_device(A: _DevOp, b, P: _DevOp | None = None, settings: KrylovSetting
         return r_
 
     r = rhs.clone() if x0 is None else residual_of(x)
-    normb = _norm(rhs)
     target = max(st.rtol * normb, st.atol)
-    residuals = [_norm(r)]
+    residuals = [normb if x0 is None else _norm(r)]
     iterations = 0
     if residuals[0] <= target:
         return FgmresResult(x, 0, residuals)
@@ -915,7 +920,7 @@ def fgmres_device(A: _DevOp, b, P: _DevOp | None = None, settings: KrylovSetting
             raise NonConvergenceError(
                 f"fgmres: no convergence in {st.maxit} iterations "
                 f"(residual {residuals[-1]:.3e}, target {target:.3e})", residuals)
-        beta = _norm(r)
+        beta = residuals[-1] if iterations == 0 else _norm(r)
         V = dev_empty((cycle + 1) * n).view(cycle + 1, n)
         store_z = P is not None and not left
         Z = dev_empty(cycle * n).view(cycle, n) if store_z else V
