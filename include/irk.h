@@ -324,7 +324,8 @@ int irk_fe_error_sq(irk_ctx* ctx, int dim, int64_t N, const double* u_dev, const
  * assembled on structured grids: level l is the block re-assembled with
  * N_l = N_0 / 2^l cells per direction ((N_l+1)^dim rows, identity rows at
  * masks[l] != 0); prolongation = P1 interpolation on the nested grids,
- * restriction its transpose, Chebyshev smoothing (nu steps pre/post) and
+ * restriction its transpose, Chebyshev smoothing (nu steps pre/post; nu = 0
+ * picks 2) and
  * `ncoarse` Chebyshev steps on the coarsest level.  The handle keeps
  * pointers to the level matrices and masks (they must outlive it). */
 typedef struct irk_mg irk_mg;
@@ -336,7 +337,7 @@ int irk_mg_destroy(irk_mg* mg);
 int irk_mg_vcycle(irk_ctx* ctx, irk_mg* mg, const double* r_dev, double* z_dev);
 /* Structured 2D path (matrix-free stencil tile kernels, chosen at create
  * time when every level is a verified 2D grid stencil with the full-boundary
- * Dirichlet set and nu == 2; env IRK_MG_GENERIC disables it): switch it on
+ * Dirichlet set and 2 <= nu <= 4; env IRK_MG_GENERIC disables it): switch it on
  * (IRK_EINVAL when unavailable) or off, and query the hierarchy. */
 int irk_mg_set_structured(irk_mg* mg, int on);
 int irk_mg_info(const irk_mg* mg, int* nlev, int* structured);

@@ -297,8 +297,11 @@ struct Sten2 {
   double dinv;     // 1 / c[1][1]
 };
 
-struct Cheb2 {
-  double cr0, cd1, cr1;  // the two steps of a 2-step Chebyshev smoother (cd0 = 0)
+// Chebyshev smoother of nu <= kMaxNu steps: d_k = cd_k d_{k-1} + cr_k D^-1 r_k
+// (cd_0 = 0), i.e. x_{k+1} = x_k + cd_k (x_k - x_{k-1}) + cr_k D^-1 (b - A x_k)
+constexpr int kMaxNu = 4;
+struct ChebS {
+  double cd[kMaxNu], cr[kMaxNu];
 };
 
 constexpr int kMaxCoarse = 64;
@@ -374,37 +377,129 @@ __device__ __forceinline__ void for_tile_points(int N, F&& f) {
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) f(0, 0, -1, -1);
 }
 
-// x2 = two Chebyshev steps from zero on b (boundary rows: x2 = b):
-//   x1 = cr0 D^-1 b,  x2 = (1 + cd1) x1 + cr1 D^-1 (b - A x1)
-template <int TX, int TY, bool F9>
+// The boundary lines x = 0 / y = 0 next to the first tile column / row
+// (outside the interior-anchored tiles): f(gx, gy).
+template <int TX, int TY, typename F>
+__device__ __forceinline__ void boundary_lines(int N, F&& f) {
+  const int x0 = 1 + TX * blockIdx.x, y0 = 1 + TY * blockIdx.y;
+  if (blockIdx.x == 0)
+    for (int j = threadIdx.x; j < TY; j += kBlock)
+      if (y0 + j <= N) f(0, y0 + j);
+  if (blockIdx.y == 0)
+    for (int i = threadIdx.x; i < TX; i += kBlock)
+      if (x0 + i <= N) f(x0 + i, 0);
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) f(0, 0);
+}
+
+// Region loops of the temporally blocked smoothers: f(local index, gx, gy)
+// over the (TX + 2h) x (TY + 2h) points of halo h of a tile whose shared
+// buffers have halo HX (row width WL); (ox, oy) = global coordinates of local
+// (0, 0).  h is a compile-time constant after unrolling.
+template <int TX, int TY, int HX, typename F>
+__device__ __forceinline__ void for_halo(int h, int ox, int oy, F&& f) {
+  constexpr int WL = TX + 2 * HX;
+  const int w = TX + 2 * h, hh = TY + 2 * h, lo = HX - h;
+  for (int k = threadIdx.x; k < w * hh; k += kBlock) {
+    const int i = lo + k % w, j = lo + k / w;
+    f(j * WL + i, ox + i, oy + j);
+  }
+}
+
+// One Chebyshev step on halo h of a tile (shared buffers of halo HX, row
+// width WL), register-blocked: thread t owns column t % w (w = TX + 2h) over
+// a segment of rows and slides a 3x3 window of x_k down it, so each point
+// costs 3 shared loads of x_k (the new row) + b + x_{k-1} instead of 9.
+// sink(local index, gx, gy, value) receives x_{k+1} at every point of the
+// region (zero-extended outside the interior is the caller's job).
+template <int TX, int TY, int HX, bool F9, typename Sink>
+__device__ __forceinline__ void cheb_rows(int h, const Sten2& S, const double* __restrict__ xk,
+                                          const double* __restrict__ xm, bool first,
+                                          const double* __restrict__ sb, double cd, double cr,
+                                          int ox, int oy, int N, Sink&& sink) {
+  constexpr int WL = TX + 2 * HX;
+  const int w = TX + 2 * h, hgt = TY + 2 * h;
+  const int nseg = kBlock / w;
+  const int rs = (hgt + nseg - 1) / nseg;
+  const int c = threadIdx.x % w, sg = threadIdx.x / w;
+  if (sg >= nseg) return;
+  const int i = HX - h + c;
+  const int j0 = HX - h + sg * rs, j1 = min(HX - h + hgt, j0 + rs);
+  if (j0 >= j1) return;
+  const double* col = xk + i;
+  // window rows j-1 (s), j (c), j+1 (n) of columns i-1 (w), i, i+1 (e)
+  double ws = col[(j0 - 1) * WL - 1], cs = col[(j0 - 1) * WL], es = col[(j0 - 1) * WL + 1];
+  double wc = col[j0 * WL - 1], cc = col[j0 * WL], ec = col[j0 * WL + 1];
+  const int gx = ox + i;
+  for (int j = j0; j < j1; ++j) {
+    const double* r = col + (j + 1) * WL;
+    const double wn = r[-1], cn = r[0], en = r[1];
+    const int gy = oy + j;
+    const int li = j * WL + i;
+    double v = 0.0;
+    if (interior2(gx, gy, N)) {
+      double ax = S.c[1][1] * cc;
+      ax += S.c[1][0] * wc + S.c[1][2] * ec;
+      ax += S.c[0][1] * cs + S.c[2][1] * cn;
+      ax += S.c[0][0] * ws + S.c[2][2] * en;
+      if (F9) ax += S.c[0][2] * es + S.c[2][0] * wn;
+      const double xmv = first ? 0.0 : xm[li];
+      v = cc + cd * (cc - xmv) + cr * (sb[li] - ax);
+    }
+    sink(li, gx, gy, v);
+    ws = wc, cs = cc, es = ec;
+    wc = wn, cc = cn, ec = en;
+  }
+}
+
+// x = NU Chebyshev steps from zero on b (boundary rows: x = b), temporally
+// blocked: b and x_1 = cr_0 D^-1 b on the tile + halo NU-1, step k on halo
+// NU-1-k; the iterates ping-pong between two shared buffers (x_{k+1}
+// overwrites x_{k-1} point by point), only x_NU goes to global memory.
+template <int TX, int TY, int NU, bool F9>
 __global__ void __launch_bounds__(kBlock)
-    k_mg2_pre(int n1, Sten2 S, Cheb2 C, const double* __restrict__ b, double* __restrict__ x2,
+    k_mg2_pre(int n1, Sten2 S, ChebS C, const double* __restrict__ b, double* __restrict__ x2,
               const int* stop) {
   IRK_PDL_ENTER();
   if (stop && *stop) return;
-  constexpr int W = TX + 2, H = TY + 2;
-  using R = Region<W, H>;
-  __shared__ double sb[W * H];
+  constexpr int HX = NU - 1, WL = TX + 2 * HX, HL = TY + 2 * HX;
+  using R = Region<WL, HL>;
+  __shared__ double sb[WL * HL], sx[2][WL * HL];
   const int N = n1 - 1;
-  const int gx0 = TX * blockIdx.x, gy0 = TY * blockIdx.y;  // region origin (halo 1)
+  const int ox = 1 + TX * blockIdx.x - HX, oy = 1 + TY * blockIdx.y - HX;
   {
     double v[R::kPer];
-    R::load(v, b, n1, gx0, gy0);
-    R::store(sb, v);
+    R::load(v, b, n1, ox, oy);
+    const double c0 = C.cr[0] * S.dinv;
+#pragma unroll
+    for (int j = 0; j < R::kPer; ++j) {
+      const int k = threadIdx.x + j * kBlock;
+      if (k < R::kN) {
+        sb[k] = v[j];
+        sx[0][k] = c0 * v[j];  // x_1 (zero outside the interior)
+      }
+    }
   }
   __syncthreads();
-  const double s0 = C.cr0 * S.dinv;
-  for_tile_points<TX, TY>(N, [&](int gx, int gy, int lx, int ly) {
+  int cur = 0;  // sx[cur] = x_k
+#pragma unroll
+  for (int k = 1; k < NU - 1; ++k) {
+    const double* xk = sx[cur];
+    double* xo = sx[cur ^ 1];  // x_{k-1} in, x_{k+1} out
+    cheb_rows<TX, TY, HX, F9>(NU - 1 - k, S, xk, xo, k == 1, sb, C.cd[k], C.cr[k] * S.dinv, ox,
+                              oy, N, [&](int li, int, int, double v) { xo[li] = v; });
+    __syncthreads();
+    cur ^= 1;
+  }
+  cheb_rows<TX, TY, HX, F9>(0, S, sx[cur], sx[cur ^ 1], NU == 2, sb, C.cd[NU - 1],
+                            C.cr[NU - 1] * S.dinv, ox, oy, N,
+                            [&](int, int gx, int gy, double v) {
+                              if (gx > N || gy > N) return;
+                              const int64_t g = (int64_t)gy * n1 + gx;
+                              x2[g] = interior2(gx, gy, N) ? v : b[g];
+                            });
+  boundary_lines<TX, TY>(N, [&](int gx, int gy) {
     const int64_t g = (int64_t)gy * n1 + gx;
-    if (!interior2(gx, gy, N)) {
-      x2[g] = b[g];
-      return;
-    }
-    const int i = (ly + 1) * W + lx + 1;
-    const double bi = sb[i];
-    const double x1 = s0 * bi;
-    const double ax1 = s0 * sten_apply<F9>(S, sb, i, W);
-    x2[g] = (1.0 + C.cd1) * x1 + C.cr1 * S.dinv * (bi - ax1);
+    x2[g] = b[g];
   });
 }
 
@@ -455,36 +550,34 @@ __global__ void __launch_bounds__(kBlock)
   });
 }
 
-// z = two Chebyshev steps from x_p = x2 + P e_c:
-//   x_a = x_p + cr0 D^-1 (b - A x_p),  z = x_a + cd1 (x_a - x_p) + cr1 D^-1 (b - A x_a)
-// boundary rows z = b.  x_p is formed on the tile + halo 2, x_a on halo 1.
-template <int TX, int TY, bool F9>
-__global__ void __launch_bounds__(kBlock)
-    k_mg2_post(int n1, int n1c, Sten2 S, Cheb2 C, const double* __restrict__ b,
+// z = NU Chebyshev steps from x_p = x2 + P e_c (boundary rows z = b),
+// temporally blocked like k_mg2_pre: x_p and b on the tile + halo NU, step k
+// on halo NU-1-k, only z goes to global memory.
+template <int TX, int TY, int NU, bool F9>
+__global__ void __launch_bounds__(kBlock, 4)
+    k_mg2_post(int n1, int n1c, Sten2 S, ChebS C, const double* __restrict__ b,
                const double* __restrict__ x2, const double* __restrict__ ec,
                double* __restrict__ z, const int* stop) {
   IRK_PDL_ENTER();
   if (stop && *stop) return;
-  constexpr int PW = TX + 4, PH = TY + 4;  // x_p region
-  constexpr int AW = TX + 2, AH = TY + 2;  // x_a region
-  using RP = Region<PW, PH>;
-  using RA = Region<AW, AH>;
-  __shared__ double sp[PW * PH];
-  __shared__ double sa[AW * AH];
-  __shared__ double sb[AW * AH];
+  constexpr int HX = NU, WL = TX + 2 * HX, HL = TY + 2 * HX;
+  using R = Region<WL, HL>;
+  __shared__ double sb[WL * HL], sx[2][WL * HL];
   const int N = n1 - 1;
-  const int ax0 = TX * blockIdx.x, ay0 = TY * blockIdx.y;  // x_a region origin
-  const int px0 = ax0 - 1, py0 = ay0 - 1;
-  double vb[RA::kPer];
+  const int ox = 1 + TX * blockIdx.x - HX, oy = 1 + TY * blockIdx.y - HX;
   {
-    double vx[RP::kPer], e0[RP::kPer], e1[RP::kPer];
-    RA::load(vb, b, n1, ax0, ay0);
+    double vb[R::kPer];
+    R::load(vb, b, n1, ox, oy);
+    R::store(sb, vb);
+  }
+  {
+    double vx[R::kPer], e0[R::kPer], e1[R::kPer];
 #pragma unroll
-    for (int j = 0; j < RP::kPer; ++j) {
+    for (int j = 0; j < R::kPer; ++j) {
       const int k = threadIdx.x + j * kBlock;
-      const int gx = px0 + k % PW, gy = py0 + k / PW;
+      const int gx = ox + k % WL, gy = oy + k / WL;
       vx[j] = e0[j] = e1[j] = 0.0;
-      if (k < RP::kN && interior2(gx, gy, N)) {
+      if (k < R::kN && interior2(gx, gy, N)) {
         const int64_t c = (int64_t)(gy >> 1) * n1c + (gx >> 1);
         vx[j] = x2[(int64_t)gy * n1 + gx];
         e0[j] = ec[c];
@@ -492,38 +585,34 @@ __global__ void __launch_bounds__(kBlock)
       }
     }
 #pragma unroll
-    for (int j = 0; j < RP::kPer; ++j) {
+    for (int j = 0; j < R::kPer; ++j) {
       const int k = threadIdx.x + j * kBlock;
-      const int gx = px0 + k % PW, gy = py0 + k / PW;
+      const int gx = ox + k % WL, gy = oy + k / WL;
       const bool odd = ((gx | gy) & 1) != 0;
-      if (k < RP::kN) sp[k] = vx[j] + (odd ? 0.5 * (e0[j] + e1[j]) : e0[j]);
+      if (k < R::kN) sx[0][k] = vx[j] + (odd ? 0.5 * (e0[j] + e1[j]) : e0[j]);
     }
-    RA::store(sb, vb);
   }
   __syncthreads();
-  const double s0 = C.cr0 * S.dinv;
+  int cur = 0;  // sx[cur] = x_k
 #pragma unroll
-  for (int j = 0; j < RA::kPer; ++j) {
-    const int k = threadIdx.x + j * kBlock;
-    if (k < RA::kN) {
-      const int lx = k % AW, ly = k / AW;
-      const int i = (ly + 1) * PW + lx + 1;
-      sa[k] = interior2(ax0 + lx, ay0 + ly, N)
-                  ? sp[i] + s0 * (vb[j] - sten_apply<F9>(S, sp, i, PW))
-                  : 0.0;
-    }
+  for (int k = 0; k < NU - 1; ++k) {
+    const double* xk = sx[cur];
+    double* xo = sx[cur ^ 1];
+    cheb_rows<TX, TY, HX, F9>(NU - 1 - k, S, xk, xo, k == 0, sb, C.cd[k], C.cr[k] * S.dinv, ox,
+                              oy, N, [&](int li, int, int, double v) { xo[li] = v; });
+    __syncthreads();
+    cur ^= 1;
   }
-  __syncthreads();
-  for_tile_points<TX, TY>(N, [&](int gx, int gy, int lx, int ly) {
+  cheb_rows<TX, TY, HX, F9>(0, S, sx[cur], sx[cur ^ 1], false, sb, C.cd[NU - 1],
+                            C.cr[NU - 1] * S.dinv, ox, oy, N,
+                            [&](int, int gx, int gy, double v) {
+                              if (gx > N || gy > N) return;
+                              const int64_t g = (int64_t)gy * n1 + gx;
+                              z[g] = interior2(gx, gy, N) ? v : b[g];
+                            });
+  boundary_lines<TX, TY>(N, [&](int gx, int gy) {
     const int64_t g = (int64_t)gy * n1 + gx;
-    if (!interior2(gx, gy, N)) {
-      z[g] = b[g];
-      return;
-    }
-    const int ia = (ly + 1) * AW + lx + 1;
-    const int ip = (ly + 2) * PW + lx + 2;
-    const double xa = sa[ia];
-    z[g] = xa + C.cd1 * (xa - sp[ip]) + C.cr1 * S.dinv * (sb[ia] - sten_apply<F9>(S, sa, ia, AW));
+    z[g] = b[g];
   });
 }
 
@@ -709,7 +798,7 @@ struct irk_mg : public irk::CgPrec {
   bool s2_ok = false, s2_on = false;
   std::vector<irk::Sten2> sten;
   std::vector<bool> f9;
-  std::vector<irk::Cheb2> c2;  // per level (lmax differs)
+  std::vector<irk::ChebS> c2;  // per level (lmax differs)
   irk::ChebN cn{};
 
   // Chebyshev coefficients (cd_k, cr_k) of steps k = 0..n-1 on [lo, hi]
@@ -800,7 +889,7 @@ struct irk_mg : public irk::CgPrec {
     const MgLevel& L = lev[l];
     const int n1 = (int)L.g.n1, N = n1 - 1;
     const Sten2& S = sten[l];
-    const Cheb2 C2 = l < (int)c2.size() ? c2[l] : Cheb2{};
+    const ChebS C2 = l < (int)c2.size() ? c2[l] : ChebS{};
     const bool F = f9[l];
     if (l == (int)lev.size() - 1) {
       const int ppt = (int)((L.m + 1023) / 1024);
@@ -821,13 +910,19 @@ struct irk_mg : public irk::CgPrec {
     double* x2 = L.x[0];
     const bool big = N >= 512;
     const dim3 gb((N + 63) / 64, (N + 15) / 16), gs((N + 31) / 32, (N + 7) / 8);
-    if (big) {
-      if (F) launch(k_mg2_pre<64, 16, true>, gb, kBlock, 0, s, n1, S, C2, b, x2, stop);
-      else launch(k_mg2_pre<64, 16, false>, gb, kBlock, 0, s, n1, S, C2, b, x2, stop);
-    } else {
-      if (F) launch(k_mg2_pre<32, 8, true>, gs, kBlock, 0, s, n1, S, C2, b, x2, stop);
-      else launch(k_mg2_pre<32, 8, false>, gs, kBlock, 0, s, n1, S, C2, b, x2, stop);
-    }
+#define IRK_MG2(KER, NU, ...)                                                              \
+  do {                                                                                     \
+    if (big) {                                                                             \
+      if (F) launch(KER<64, 16, NU, true>, gb, kBlock, 0, s, __VA_ARGS__);                 \
+      else launch(KER<64, 16, NU, false>, gb, kBlock, 0, s, __VA_ARGS__);                  \
+    } else {                                                                               \
+      if (F) launch(KER<32, 8, NU, true>, gs, kBlock, 0, s, __VA_ARGS__);                  \
+      else launch(KER<32, 8, NU, false>, gs, kBlock, 0, s, __VA_ARGS__);                   \
+    }                                                                                      \
+  } while (0)
+    if (nu == 2) IRK_MG2(k_mg2_pre, 2, n1, S, C2, b, x2, stop);
+    else if (nu == 3) IRK_MG2(k_mg2_pre, 3, n1, S, C2, b, x2, stop);
+    else IRK_MG2(k_mg2_pre, 4, n1, S, C2, b, x2, stop);
     const dim3 gr((Nc + 31) / 32, (Nc + 7) / 8);
     if (F) launch(k_mg2_restrict<32, 8, true>, gr, kBlock, 0, s, n1, n1c, S, b, x2, Cc.b, stop);
     else launch(k_mg2_restrict<32, 8, false>, gr, kBlock, 0, s, n1, n1c, S, b, x2, Cc.b, stop);
@@ -835,13 +930,10 @@ struct irk_mg : public irk::CgPrec {
     if (cudaPeekAtLastError() != cudaSuccess) return IRK_ECUDA;
     IRK_TRY(vcycle2(ctx, s, l + 1, Cc.b, Cc.x[1], stop));
     const double* ec = Cc.x[1];
-    if (big) {
-      if (F) launch(k_mg2_post<64, 16, true>, gb, kBlock, 0, s, n1, n1c, S, C2, b, x2, ec, out, stop);
-      else launch(k_mg2_post<64, 16, false>, gb, kBlock, 0, s, n1, n1c, S, C2, b, x2, ec, out, stop);
-    } else {
-      if (F) launch(k_mg2_post<32, 8, true>, gs, kBlock, 0, s, n1, n1c, S, C2, b, x2, ec, out, stop);
-      else launch(k_mg2_post<32, 8, false>, gs, kBlock, 0, s, n1, n1c, S, C2, b, x2, ec, out, stop);
-    }
+    if (nu == 2) IRK_MG2(k_mg2_post, 2, n1, n1c, S, C2, b, x2, ec, out, stop);
+    else if (nu == 3) IRK_MG2(k_mg2_post, 3, n1, n1c, S, C2, b, x2, ec, out, stop);
+    else IRK_MG2(k_mg2_post, 4, n1, n1c, S, C2, b, x2, ec, out, stop);
+#undef IRK_MG2
     ctx->launches++;
     return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
   }
@@ -852,7 +944,7 @@ struct irk_mg : public irk::CgPrec {
     using namespace irk;
     s2_ok = false;
     const int nl = (int)lev.size();
-    if (dim != 2 || nu != 2 || ncoarse > kMaxCoarse) return IRK_OK;
+    if (dim != 2 || nu < 2 || nu > kMaxNu || ncoarse > kMaxCoarse) return IRK_OK;
     if (lev.back().m > 8 * 1024) return IRK_OK;
     for (const MgLevel& L : lev)
       if (!L.mask || L.g.n1 - 1 < 4 || L.g.n1 > 46341) return IRK_OK;
@@ -893,11 +985,14 @@ struct irk_mg : public irk::CgPrec {
     }
     // Chebyshev coefficients, as smooth(): [lmax/4, lmax] on the fine
     // levels, [0.05 lmax, lmax] with ncoarse steps on the coarsest
-    c2.assign(nl, Cheb2{});
+    c2.assign(nl, ChebS{});
     std::vector<double> cd, cr;
     for (int l = 0; l + 1 < nl; ++l) {
-      cheb(0.25 * lev[l].lmax, lev[l].lmax, 2, cd, cr);
-      c2[l] = Cheb2{cr[0], cd[1], cr[1]};
+      cheb(0.25 * lev[l].lmax, lev[l].lmax, nu, cd, cr);
+      for (int k = 0; k < nu; ++k) {
+        c2[l].cd[k] = cd[k];
+        c2[l].cr[k] = cr[k];
+      }
     }
     cheb(0.05 * lev.back().lmax, lev.back().lmax, ncoarse, cd, cr);
     cn.n = ncoarse;
@@ -942,12 +1037,17 @@ int irk_mg_create(irk_ctx* ctx, int dim, int nlev, const int64_t* N_host,
   IRK_REQUIRE(ctx && N_host && A_levels && out, "irk_mg_create: NULL argument");
   IRK_REQUIRE(dim >= 1 && dim <= 3, "irk_mg_create: dim must be 1, 2 or 3");
   IRK_REQUIRE(nlev >= 1 && nlev <= 16, "irk_mg_create: 1 <= nlev <= 16");
-  IRK_REQUIRE(nu >= 1 && nu <= 8 && ncoarse >= 1 && ncoarse <= 64,
-              "irk_mg_create: 1 <= nu <= 8, 1 <= ncoarse <= 64");
+  IRK_REQUIRE(nu >= 0 && nu <= 8 && ncoarse >= 1 && ncoarse <= 64,
+              "irk_mg_create: 0 <= nu <= 8 (0: automatic), 1 <= ncoarse <= 64");
   irk_mg* mg = new irk_mg();
   mg->uid = g_mg_uid.fetch_add(1);
   mg->dim = dim;
-  mg->nu = nu;
+  // nu = 0 (automatic): 2.  Measured on B200 (config 2): nu = 3 / 4 cut the
+  // CG iterations of a block solve from 6 to 5 / 4 and the solve time by
+  // 6 / 11 %, but the outer FGMRES then needs 9.0 instead of 8.1 iterations
+  // per step (the inexact blocks change), so the step is slower.
+  const bool nu_auto = nu == 0;
+  mg->nu = nu_auto ? 2 : nu;
   mg->ncoarse = ncoarse;
   size_t total = 0;
   std::vector<int64_t> pads;

@@ -137,6 +137,17 @@ class StagePreconditioner:
             self._mats = la.shared_pattern([self.M.device()] + [K.device() for K in self.Ks])
         return self._mats
 
+    def _mg_blocks(self) -> bool:
+        """Blocks are solved one by one with multigrid-PCG when they are P1
+        grid operators (no diagonal shift): ~5 instead of O(100) iterations."""
+        if self._shift is not None or self.settings.method not in ("auto", "mg"):
+            return False
+        if getattr(self.M, "_p1_grid", None) is None:
+            return False
+        if getattr(self.Ks[0], "_p1_grid", None) != self.M._p1_grid:
+            return False
+        return all(getattr(f, "_mg", None) is not None for f in self.block_factors)
+
     def _block_coefs(self):
         s = self.s
         if self.form is Splitting.IA:
@@ -176,7 +187,9 @@ class StagePreconditioner:
         mk = self.mask()
         mats = [d.eliminated(mk) for d in self._device_mats()]
         Md, Ks = mats[0], mats[1:]
-        if kind is PreconditionerKind.BLOCK_DIAGONAL and len(Ks) == 1:
+        if kind is PreconditionerKind.BLOCK_DIAGONAL and len(Ks) == 1 and not self._mg_blocks():
+            # independent blocks without a multigrid hierarchy: one batched
+            # Jacobi-PCG advances all s systems per pass
             a, b = self._block_coefs()
             self._pcg(s, a, b, Md, Ks[0], self._shift, R, s, X, s)
             return X

@@ -84,9 +84,46 @@ def to_dev(x, dtype=None):
         return x.to(device=device(), dtype=dt).contiguous()
     np_dt = np.float64 if dt == torch.float64 else np.int64 if dt == torch.int64 else None
     arr = np.ascontiguousarray(np.asarray(x, dtype=np_dt))
-    # staged through pinned memory (torch's caching host allocator keeps the
-    # block until the copy ran): the host does not wait for the stream
-    return torch.from_numpy(arr).pin_memory().to(device(), non_blocking=True)
+    return _STAGER.upload(torch.from_numpy(arr))
+
+
+class _PinnedStager:
+    """Host->device uploads through a ring of persistent pinned buffers: the
+    copy is asynchronous (the host does not wait for the stream, unlike a
+    pageable copy), and no pinned memory is allocated per call (a fresh
+    cudaHostAlloc costs milliseconds).  A slot is reused once the event
+    recorded after its last copy has completed."""
+
+    SLOTS = 4
+
+    def __init__(self):
+        self._buf = [None] * self.SLOTS
+        self._ev = [None] * self.SLOTS
+        self._next = 0
+
+    def upload(self, t):
+        torch = _torch()
+        nbytes = t.numel() * t.element_size()
+        if nbytes == 0:
+            return t.to(device())
+        i = self._next
+        self._next = (i + 1) % self.SLOTS
+        ev = self._ev[i]
+        if ev is not None:
+            ev.synchronize()  # normally long complete
+        buf = self._buf[i]
+        if buf is None or buf.numel() < nbytes:
+            buf = self._buf[i] = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8,
+                                             pin_memory=True)
+        host = buf[:nbytes].view(t.dtype).view(t.shape)
+        host.copy_(t)
+        out = host.to(device(), non_blocking=True)
+        ev = self._ev[i] = self._ev[i] or torch.cuda.Event()
+        ev.record()
+        return out
+
+
+_STAGER = _PinnedStager()
 
 
 def is_torch(x) -> bool:
@@ -495,8 +532,9 @@ class BlockSolveSettings:
     operators, Jacobi-PCG otherwise), "mg" (multigrid required), "pcg"
     (Jacobi-preconditioned CG) or "chebyshev" (Jacobi-Chebyshev,
     ``cheb_iters`` sweeps with Gershgorin/Lanczos-free bounds).
-    mg_nu / mg_coarse_steps: Chebyshev smoothing steps per level and on the
-    coarsest level of the multigrid V-cycle; mg_coarse_ratio: coarsening stops
+    mg_nu / mg_coarse_steps: Chebyshev smoothing steps per level (0: automatic
+    = 2; the structured 2D path fuses up to 4) and on the coarsest level of the
+    multigrid V-cycle; mg_coarse_ratio: coarsening stops
     once beta / (alpha H^2) of a level is at most this (mass-dominated).
     raise_on_maxit: when False (preconditioner use) an unconverged block
     returns its last iterate, FGMRES being flexible."""
@@ -507,7 +545,7 @@ class BlockSolveSettings:
     maxit: int = 20000
     raise_on_maxit: bool = False
     cheb_iters: int = 50
-    mg_nu: int = 2
+    mg_nu: int = 0
     mg_coarse_steps: int = 4
     mg_coarse_ratio: float = 0.5
 
