@@ -81,6 +81,12 @@ def to_dev(x, dtype=None):
     if isinstance(x, torch.Tensor):
         if x.device.type == "cuda" and x.dtype == dt and x.is_contiguous():
             return x
+        if x.device.type == "cpu" and x.is_pinned() and x.dtype == dt and x.is_contiguous():
+            # direct DMA from the caller's pinned buffer; synchronised so the
+            # caller may reuse the buffer as soon as this returns
+            out = x.to(device=device(), non_blocking=True)
+            torch.cuda.current_stream(out.device).synchronize()
+            return out
         return x.to(device=device(), dtype=dt).contiguous()
     np_dt = np.float64 if dt == torch.float64 else np.int64 if dt == torch.int64 else None
     arr = np.ascontiguousarray(np.asarray(x, dtype=np_dt))
@@ -135,7 +141,15 @@ def is_torch(x) -> bool:
 
 
 def to_host(t) -> np.ndarray:
-    return t.detach().cpu().numpy()
+    """Device tensor -> fresh numpy array.  Large device reads land in pinned
+    memory (torch's caching host allocator recycles the block once the array
+    is dropped): a direct DMA instead of the driver's pageable bounce."""
+    t = t.detach()
+    if t.device.type == "cuda" and t.numel() * t.element_size() >= (1 << 20):
+        out = _torch().empty(t.shape, dtype=t.dtype, pin_memory=True)
+        out.copy_(t)
+        return out.numpy()
+    return t.cpu().numpy()
 
 
 def _like_input(dev_result, like):

@@ -265,7 +265,8 @@ class TimeStepper:
 
     @u.setter
     def u(self, value):
-        self._u_dev = la.to_dev(value).clone()
+        d = la.to_dev(value)
+        self._u_dev = d.clone() if (la.is_torch(value) and d.data_ptr() == value.data_ptr()) else d
         self._u_host = None
 
     @property
@@ -372,7 +373,7 @@ class TimeStepper:
     def step(self, problem: SemidiscreteProblem | None = None):
         """One step (stepper.py:262-268); returns (u_next numpy, StepReport)."""
         _, rep = self.step_device(problem)
-        return self.u.copy(), rep
+        return la.to_host(self._u_dev), rep  # fresh array, owned by the caller
 
 
 # ------------------------------------------------------------ stage data
