@@ -616,6 +616,166 @@ __global__ void __launch_bounds__(kBlock, 4)
   });
 }
 
+// Restriction of level l fused with the pre-smoothing of level l+1 (one
+// kernel per descent step instead of two): the CTA owns a coarse tile,
+// forms the fine residual r = b - A x2 over the fine region under the
+// coarse tile + halo NU-1 (fine x2 with one more halo), restricts it to
+// b_c on that coarse region, then runs the NU pre-smoothing steps of level
+// l+1 in shared memory.  Writes b_c and x2_c of the tile (both are read
+// again by the level's post-smoother and the next descent step).  The
+// coarse buffers alias the fine x2 buffer once the residual is formed.
+template <int CX, int CY, int NU, bool F9>
+__global__ void __launch_bounds__(kBlock)
+    k_mg2_rp(int n1f, int n1c, Sten2 Sf, Sten2 Sc, ChebS C, const double* __restrict__ bf,
+             const double* __restrict__ x2f, double* __restrict__ bc, double* __restrict__ x2c,
+             const int* stop) {
+  IRK_PDL_ENTER();
+  if (stop && *stop) return;
+  constexpr int HX = NU - 1, WL = CX + 2 * HX, HL = CY + 2 * HX;  // coarse region
+  constexpr int RW = 2 * WL + 1, RH = 2 * HL + 1;                  // fine residual region
+  constexpr int XW = RW + 2, XH = RH + 2;                          // fine x2 region
+  static_assert(3 * WL * HL <= XW * XH, "coarse buffers alias the fine x2 buffer");
+  using RX = Region<XW, XH>;
+  using RB = Region<RW, RH>;
+  __shared__ double sxf[XW * XH];
+  __shared__ double srf[RW * RH];
+  double* sb = sxf;
+  double* sx[2] = {sxf + WL * HL, sxf + 2 * WL * HL};
+  const int Nf = n1f - 1, Nc = n1c - 1;
+  const int ox = 1 + CX * blockIdx.x - HX, oy = 1 + CY * blockIdx.y - HX;
+  const int rx0 = 2 * ox - 1, ry0 = 2 * oy - 1;
+  {
+    double vb[RB::kPer];
+    {
+      double vx[RX::kPer];
+      RX::load(vx, x2f, n1f, rx0 - 1, ry0 - 1);
+      RB::load(vb, bf, n1f, rx0, ry0);
+      RX::store(sxf, vx);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < RB::kPer; ++j) {
+      const int k = threadIdx.x + j * kBlock;
+      if (k < RB::kN) {
+        const int lx = k % RW, ly = k / RW;
+        srf[k] = interior2(rx0 + lx, ry0 + ly, Nf)
+                     ? vb[j] - sten_apply<F9>(Sf, sxf, (ly + 1) * XW + lx + 1, XW)
+                     : 0.0;
+      }
+    }
+  }
+  __syncthreads();  // sxf is free from here on
+  const double c0 = C.cr[0] * Sc.dinv;
+  for (int k = threadIdx.x; k < WL * HL; k += kBlock) {
+    const int cx = ox + k % WL, cy = oy + k / WL;
+    double v = 0.0;
+    if (interior2(cx, cy, Nc)) {
+      const int i = (2 * cy - ry0) * RW + (2 * cx - rx0);
+      v = srf[i] + 0.5 * (srf[i - 1] + srf[i + 1] + srf[i - RW] + srf[i + RW] +
+                          srf[i - RW - 1] + srf[i + RW + 1]);
+    }
+    sb[k] = v;
+    sx[0][k] = c0 * v;  // x_1
+  }
+  __syncthreads();
+  int cur = 0;
+#pragma unroll
+  for (int k = 1; k < NU - 1; ++k) {
+    const double* xk = sx[cur];
+    double* xo = sx[cur ^ 1];
+    cheb_rows<CX, CY, HX, F9>(NU - 1 - k, Sc, xk, xo, k == 1, sb, C.cd[k], C.cr[k] * Sc.dinv, ox,
+                              oy, Nc, [&](int li, int, int, double v) { xo[li] = v; });
+    __syncthreads();
+    cur ^= 1;
+  }
+  cheb_rows<CX, CY, HX, F9>(0, Sc, sx[cur], sx[cur ^ 1], NU == 2, sb, C.cd[NU - 1],
+                            C.cr[NU - 1] * Sc.dinv, ox, oy, Nc,
+                            [&](int li, int gx, int gy, double v) {
+                              if (gx > Nc || gy > Nc) return;
+                              const int64_t g = (int64_t)gy * n1c + gx;
+                              const bool in = interior2(gx, gy, Nc);
+                              bc[g] = in ? sb[li] : 0.0;
+                              x2c[g] = in ? v : 0.0;
+                            });
+  boundary_lines<CX, CY>(Nc, [&](int gx, int gy) {
+    const int64_t g = (int64_t)gy * n1c + gx;
+    bc[g] = 0.0;
+    x2c[g] = 0.0;
+  });
+}
+
+// Restriction of level L-2 fused with the coarsest solve (one CTA): the
+// whole fine level (x2 zero-extended, then the residual in place of it) and
+// the coarse iterate live in shared memory; b_c of the owned coarse points
+// goes to registers, then C.n Chebyshev steps as in k_mg2_coarse.
+template <int PPT, bool F9>
+__global__ void __launch_bounds__(1024, 1)
+    k_mg2_rc(int n1f, int n1, Sten2 Sf, Sten2 S, ChebN C, const double* __restrict__ bf,
+             const double* __restrict__ x2f, double* __restrict__ z, const int* stop) {
+  IRK_PDL_ENTER();
+  if (stop && *stop) return;
+  extern __shared__ double sm[];
+  const int Nf = n1f - 1, mf = n1f * n1f;
+  const int N = n1 - 1, m = n1 * n1;
+  double* fx = sm;       // fine x2 (zero outside the interior)
+  double* fr = sm + mf;  // fine residual
+  double* buf[2] = {sm + 2 * mf, sm + 2 * mf + m};
+  for (int g = threadIdx.x; g < mf; g += 1024) {
+    const int gx = g % n1f, gy = g / n1f;
+    const bool in = interior2(gx, gy, Nf);
+    fx[g] = in ? x2f[g] : 0.0;
+    fr[g] = in ? bf[g] : 0.0;
+  }
+  for (int g = threadIdx.x; g < 2 * m; g += 1024) buf[0][g] = 0.0;
+  __syncthreads();
+  for (int g = threadIdx.x; g < mf; g += 1024) {
+    const int gx = g % n1f, gy = g / n1f;
+    if (interior2(gx, gy, Nf)) fr[g] -= sten_apply<F9>(Sf, fx, g, n1f);
+  }
+  __syncthreads();
+  double bi[PPT], xi[PPT], di[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int g = threadIdx.x + p * 1024;
+    double v = 0.0;
+    if (g < m) {
+      const int cx = g % n1, cy = g / n1;
+      if (interior2(cx, cy, N)) {
+        const int i = 2 * cy * n1f + 2 * cx;
+        v = fr[i] + 0.5 * (fr[i - 1] + fr[i + 1] + fr[i - n1f] + fr[i + n1f] + fr[i - n1f - 1] +
+                           fr[i + n1f + 1]);
+      }
+    }
+    bi[p] = v;
+    xi[p] = 0.0;
+    di[p] = 0.0;
+  }
+  int cur = 0;
+  for (int k = 0; k < C.n; ++k) {
+    const double* xs = buf[cur];
+    double* xo = buf[cur ^ 1];
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) {
+      const int g = threadIdx.x + p * 1024;
+      if (g >= m) continue;
+      const int gx = g % n1, gy = g / n1;
+      if (!interior2(gx, gy, N)) continue;  // b_c = 0 there: x stays 0
+      const double res = bi[p] - (k ? sten_apply<F9>(S, xs, g, n1) : 0.0);
+      const double dn = (k ? C.cd[k] * di[p] : 0.0) + C.cr[k] * S.dinv * res;
+      di[p] = dn;
+      xi[p] += dn;
+      xo[g] = xi[p];
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int g = threadIdx.x + p * 1024;
+    if (g < m) z[g] = xi[p];
+  }
+}
+
 // Coarsest level: C.n Chebyshev steps from zero in ONE CTA (1024 threads,
 // up to PPT grid points per thread); the iterate lives in shared memory
 // (two zero-bordered n1 x n1 buffers), b / x / d of the owned points in
@@ -882,59 +1042,123 @@ struct irk_mg : public irk::CgPrec {
     return smooth(ctx, s, l, b, c, nu, 0.25, out, stop);
   }
 
-  // structured 2D V-cycle: z_l = V_l(b_l) (see the k_mg2_* kernels)
-  int vcycle2(irk_ctx* ctx, cudaStream_t s, int l, const double* b, double* out,
-              const int* stop) {
+  // structured 2D V-cycle: z_l = V_l(b_l) (see the k_mg2_* kernels).  The
+  // descent fuses each restriction with the next level's pre-smoothing
+  // (k_mg2_rp) and the last one with the coarsest solve (k_mg2_rc): 11
+  // kernels instead of 16 on 6 levels.  Env IRK_MG_NOFUSE: separate kernels.
+  int coarse2(irk_ctx* ctx, cudaStream_t s, const double* b, double* out, const int* stop) {
     using namespace irk;
+    const int l = (int)lev.size() - 1;
     const MgLevel& L = lev[l];
-    const int n1 = (int)L.g.n1, N = n1 - 1;
+    const int n1 = (int)L.g.n1;
     const Sten2& S = sten[l];
-    const ChebS C2 = l < (int)c2.size() ? c2[l] : ChebS{};
     const bool F = f9[l];
-    if (l == (int)lev.size() - 1) {
-      const int ppt = (int)((L.m + 1023) / 1024);
-      const size_t sh = 2 * (size_t)L.m * sizeof(double);
+    const int ppt = (int)((L.m + 1023) / 1024);
+    const size_t sh = 2 * (size_t)L.m * sizeof(double);
 #define IRK_CO(P)                                                                           \
   (F ? launch(k_mg2_coarse<P, true>, 1, 1024, sh, s, n1, S, cn, b, out, stop)                  \
      : launch(k_mg2_coarse<P, false>, 1, 1024, sh, s, n1, S, cn, b, out, stop))
-      if (ppt <= 1) IRK_CO(1);
-      else if (ppt <= 2) IRK_CO(2);
-      else if (ppt <= 4) IRK_CO(4);
-      else IRK_CO(8);
+    if (ppt <= 1) IRK_CO(1);
+    else if (ppt <= 2) IRK_CO(2);
+    else if (ppt <= 4) IRK_CO(4);
+    else IRK_CO(8);
 #undef IRK_CO
-      ctx->launches++;
-      return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
-    }
+    ctx->launches++;
+    return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
+  }
+
+  bool fuse_ok() const {
+    static const bool off = getenv("IRK_MG_NOFUSE") != nullptr;
+    return !off && nu <= 4;
+  }
+  // k_mg2_rc: the fine level and the coarsest fit one CTA's shared memory
+  bool rc_ok() const {
+    const int64_t mf = lev[lev.size() - 2].m, mc = lev.back().m;
+    return fuse_ok() && mc <= 2048 && (2 * mf + 2 * mc) * (int64_t)sizeof(double) <= kRcSmem;
+  }
+  static constexpr int kRcSmem = 200 * 1024;
+
+  int vcycle2(irk_ctx* ctx, cudaStream_t s, int l, const double* b, double* out,
+              const int* stop) {
+    using namespace irk;
+    if (l == (int)lev.size() - 1) return coarse2(ctx, s, b, out, stop);
+    const MgLevel& L = lev[l];
+    const int n1 = (int)L.g.n1, N = n1 - 1;
+    const Sten2& S = sten[l];
+    const ChebS C2 = c2[l];
+    const bool F = f9[l];
+    double* x2 = L.x[0];
+#define IRK_MG2(N_, KER, NU, ...)                                                          \
+  do {                                                                                     \
+    if ((N_) >= 512) {                                                                     \
+      const dim3 g_(((N_) + 63) / 64, ((N_) + 15) / 16);                                   \
+      if (F) launch(KER<64, 16, NU, true>, g_, kBlock, 0, s, __VA_ARGS__);                 \
+      else launch(KER<64, 16, NU, false>, g_, kBlock, 0, s, __VA_ARGS__);                  \
+    } else {                                                                               \
+      const dim3 g_(((N_) + 31) / 32, ((N_) + 7) / 8);                                     \
+      if (F) launch(KER<32, 8, NU, true>, g_, kBlock, 0, s, __VA_ARGS__);                  \
+      else launch(KER<32, 8, NU, false>, g_, kBlock, 0, s, __VA_ARGS__);                   \
+    }                                                                                      \
+    ctx->launches++;                                                                       \
+  } while (0)
+#define IRK_NU(N_, KER, ...)                            \
+  do {                                                  \
+    if (nu == 2) IRK_MG2(N_, KER, 2, __VA_ARGS__);      \
+    else if (nu == 3) IRK_MG2(N_, KER, 3, __VA_ARGS__); \
+    else IRK_MG2(N_, KER, 4, __VA_ARGS__);              \
+  } while (0)
+    if (l == 0) IRK_NU(N, k_mg2_pre, n1, S, C2, b, x2, stop);  // the top level's pre
     const MgLevel& Cc = lev[l + 1];
     const int n1c = (int)Cc.g.n1, Nc = n1c - 1;
-    double* x2 = L.x[0];
-    const bool big = N >= 512;
-    const dim3 gb((N + 63) / 64, (N + 15) / 16), gs((N + 31) / 32, (N + 7) / 8);
-#define IRK_MG2(KER, NU, ...)                                                              \
-  do {                                                                                     \
-    if (big) {                                                                             \
-      if (F) launch(KER<64, 16, NU, true>, gb, kBlock, 0, s, __VA_ARGS__);                 \
-      else launch(KER<64, 16, NU, false>, gb, kBlock, 0, s, __VA_ARGS__);                  \
-    } else {                                                                               \
-      if (F) launch(KER<32, 8, NU, true>, gs, kBlock, 0, s, __VA_ARGS__);                  \
-      else launch(KER<32, 8, NU, false>, gs, kBlock, 0, s, __VA_ARGS__);                   \
-    }                                                                                      \
-  } while (0)
-    if (nu == 2) IRK_MG2(k_mg2_pre, 2, n1, S, C2, b, x2, stop);
-    else if (nu == 3) IRK_MG2(k_mg2_pre, 3, n1, S, C2, b, x2, stop);
-    else IRK_MG2(k_mg2_pre, 4, n1, S, C2, b, x2, stop);
+    const bool last = l + 2 == (int)lev.size();
     const dim3 gr((Nc + 31) / 32, (Nc + 7) / 8);
-    if (F) launch(k_mg2_restrict<32, 8, true>, gr, kBlock, 0, s, n1, n1c, S, b, x2, Cc.b, stop);
-    else launch(k_mg2_restrict<32, 8, false>, gr, kBlock, 0, s, n1, n1c, S, b, x2, Cc.b, stop);
-    ctx->launches += 2;
+    if (last && rc_ok()) {
+      const int ppt = (int)((Cc.m + 1023) / 1024);
+      const size_t sh = (2 * (size_t)L.m + 2 * (size_t)Cc.m) * sizeof(double);
+      if (ppt <= 1) {
+        if (F) launch(k_mg2_rc<1, true>, 1, 1024, sh, s, n1, n1c, S, sten[l + 1], cn, b, x2, Cc.x[1], stop);
+        else launch(k_mg2_rc<1, false>, 1, 1024, sh, s, n1, n1c, S, sten[l + 1], cn, b, x2, Cc.x[1], stop);
+      } else {
+        if (F) launch(k_mg2_rc<2, true>, 1, 1024, sh, s, n1, n1c, S, sten[l + 1], cn, b, x2, Cc.x[1], stop);
+        else launch(k_mg2_rc<2, false>, 1, 1024, sh, s, n1, n1c, S, sten[l + 1], cn, b, x2, Cc.x[1], stop);
+      }
+      ctx->launches++;
+    } else if (!last && fuse_ok()) {
+      // restriction + the next level's pre-smoothing (32 x 8 coarse tiles)
+      const ChebS Cn = c2[l + 1];
+      const bool F1 = F || f9[l + 1];
+#define IRK_RP(NU)                                                                              \
+  (F1 ? launch(k_mg2_rp<32, 8, NU, true>, gr, kBlock, 0, s, n1, n1c, S, sten[l + 1], Cn, b, x2, \
+               Cc.b, Cc.x[0], stop)                                                              \
+      : launch(k_mg2_rp<32, 8, NU, false>, gr, kBlock, 0, s, n1, n1c, S, sten[l + 1], Cn, b, x2, \
+               Cc.b, Cc.x[0], stop))
+      if (nu == 2) IRK_RP(2);
+      else if (nu == 3) IRK_RP(3);
+      else IRK_RP(4);
+#undef IRK_RP
+      ctx->launches++;
+    } else {
+      if (F) launch(k_mg2_restrict<32, 8, true>, gr, kBlock, 0, s, n1, n1c, S, b, x2, Cc.b, stop);
+      else launch(k_mg2_restrict<32, 8, false>, gr, kBlock, 0, s, n1, n1c, S, b, x2, Cc.b, stop);
+      ctx->launches++;
+      if (last) {
+        IRK_TRY(coarse2(ctx, s, Cc.b, Cc.x[1], stop));
+      } else {
+        const ChebS Cn = c2[l + 1];
+        const bool Fs = F;
+        {
+          const bool F = Fs || f9[l + 1];
+          const Sten2& S1 = sten[l + 1];
+          IRK_NU(Nc, k_mg2_pre, n1c, S1, Cn, Cc.b, Cc.x[0], stop);
+        }
+      }
+    }
     if (cudaPeekAtLastError() != cudaSuccess) return IRK_ECUDA;
-    IRK_TRY(vcycle2(ctx, s, l + 1, Cc.b, Cc.x[1], stop));
+    if (!last) IRK_TRY(vcycle2(ctx, s, l + 1, Cc.b, Cc.x[1], stop));
     const double* ec = Cc.x[1];
-    if (nu == 2) IRK_MG2(k_mg2_post, 2, n1, n1c, S, C2, b, x2, ec, out, stop);
-    else if (nu == 3) IRK_MG2(k_mg2_post, 3, n1, n1c, S, C2, b, x2, ec, out, stop);
-    else IRK_MG2(k_mg2_post, 4, n1, n1c, S, C2, b, x2, ec, out, stop);
+    IRK_NU(N, k_mg2_post, n1, n1c, S, C2, b, x2, ec, out, stop);
+#undef IRK_NU
 #undef IRK_MG2
-    ctx->launches++;
     return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
   }
 
@@ -1137,6 +1361,10 @@ int irk_mg_create(irk_ctx* ctx, int dim, int nlev, const int64_t* N_host,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, sh8));
       IRK_CUDA(cudaFuncSetAttribute(k_mg2_coarse<8, true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, sh8));
+      for (const void* fn : {(const void*)k_mg2_rc<1, false>, (const void*)k_mg2_rc<1, true>,
+                             (const void*)k_mg2_rc<2, false>, (const void*)k_mg2_rc<2, true>})
+        IRK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      irk_mg::kRcSmem));
     }
   }
   *out = mg;

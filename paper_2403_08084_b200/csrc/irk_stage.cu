@@ -470,12 +470,32 @@ __global__ void k_stage_mix(int64_t m, int so, int si, const Mat8 Q, const doubl
   }
 }
 
-// out[r*ld] = R[r*s+i] - sum_c C[r,c] sum_j coef[j] X[c*s+j]  (masked)
+// Slot-uniform SELL row access (colhdr/uval headers: one broadcast load per
+// slot instead of the 12 B per entry of sell_col + val)
+struct SellRow {
+  int q0, base, width, lane;
+  __device__ __forceinline__ SellRow(const int* __restrict__ slice_ptr, int ellw, int64_t r) {
+    const int64_t sl = r / kSlice;
+    lane = (int)(r % kSlice);
+    if (ellw) {
+      base = (int)(sl * kSlice * ellw);
+      width = ellw;
+    } else {
+      base = __ldg(slice_ptr + sl);
+      width = (__ldg(slice_ptr + sl + 1) - base) / kSlice;
+    }
+    q0 = base / kSlice;
+  }
+};
+
+// out[r*ld] = R[r*s+i] - sum_c C[r,c] sum_{j in J} coef[j] X[c*s+j]  (masked);
+// J = the stages with a nonzero coefficient (jmask), gathered only those
 template <int S>
 __global__ void __launch_bounds__(kBlock)
-    k_stage_couple(int64_t m, int i, const int* __restrict__ slice_ptr,
-                   const int* __restrict__ sell_col, const double* __restrict__ cval,
-                   const Mat8 coef, const uint8_t* __restrict__ mask,
+    k_stage_couple(int64_t m, int i, const int* __restrict__ slice_ptr, int ellw,
+                   const int* __restrict__ colhdr, const int* __restrict__ sell_col,
+                   const double* __restrict__ uval, const double* __restrict__ cval,
+                   const Mat8 coef, unsigned jmask, const uint8_t* __restrict__ mask,
                    const double* __restrict__ R, const double* __restrict__ X,
                    double* __restrict__ out, int64_t ld_out) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -485,17 +505,16 @@ __global__ void __launch_bounds__(kBlock)
     out[r * ld_out] = rv;
     return;
   }
-  int64_t s = r / kSlice;
-  int lane = (int)(r % kSlice);
-  int base = __ldg(slice_ptr + s), width = (__ldg(slice_ptr + s + 1) - base) / kSlice;
+  const SellRow sr(slice_ptr, ellw, r);
   double acc = 0.0;
-  for (int k = 0; k < width; ++k) {
-    int pos = base + k * kSlice + lane;
-    int c = __ldg(sell_col + pos);
+  for (int k = 0; k < sr.width; ++k) {
+    const int pos = sr.base + k * kSlice + sr.lane;
+    const int c = sell_col_at(colhdr, sell_col, sr.q0 + k, pos, r);
     double w = 0.0;
 #pragma unroll
-    for (int j = 0; j < S; ++j) w += coef.q[j] * __ldg(X + (int64_t)c * S + j);
-    acc += __ldg(cval + pos) * w;
+    for (int j = 0; j < S; ++j)
+      if (jmask & (1u << j)) w += coef.q[j] * __ldg(X + (int64_t)c * S + j);
+    acc += sell_val_at(uval, cval, sr.q0 + k, pos) * w;
   }
   out[r * ld_out] = rv - acc;
 }
@@ -503,19 +522,20 @@ __global__ void __launch_bounds__(kBlock)
 // Out_r,i = a (B u)_r + sum_j G_ij F_r,j
 template <int S>
 __global__ void __launch_bounds__(kBlock)
-    k_stage_rhs(int64_t m, const int* __restrict__ slice_ptr, const int* __restrict__ sell_col,
-                const double* __restrict__ bval, double a, const double* __restrict__ u,
-                const Mat8 G, const double* __restrict__ F, double* __restrict__ Out) {
+    k_stage_rhs(int64_t m, const int* __restrict__ slice_ptr, int ellw,
+                const int* __restrict__ colhdr, const int* __restrict__ sell_col,
+                const double* __restrict__ ubval, const double* __restrict__ bval, double a,
+                const double* __restrict__ u, const Mat8 G, const double* __restrict__ F,
+                double* __restrict__ Out) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
   double bu = 0.0;
   if (bval) {
-    int64_t s = r / kSlice;
-    int lane = (int)(r % kSlice);
-    int base = __ldg(slice_ptr + s), width = (__ldg(slice_ptr + s + 1) - base) / kSlice;
-    for (int k = 0; k < width; ++k) {
-      int pos = base + k * kSlice + lane;
-      bu += __ldg(bval + pos) * __ldg(u + __ldg(sell_col + pos));
+    const SellRow sr(slice_ptr, ellw, r);
+    for (int k = 0; k < sr.width; ++k) {
+      const int pos = sr.base + k * kSlice + sr.lane;
+      bu += sell_val_at(ubval, bval, sr.q0 + k, pos) *
+            __ldg(u + sell_col_at(colhdr, sell_col, sr.q0 + k, pos, r));
     }
     bu *= a;
   } else if (u) {
@@ -926,11 +946,14 @@ int irk_stage_couple(irk_ctx* ctx, int s, int i, const double* coef_host, const 
   Mat8 cf;
   for (int q = 0; q < kMaxStages * kMaxStages; ++q) cf.q[q] = 0.0;
   for (int j = 0; j < s; ++j) cf.q[j] = coef_host[j];
+  unsigned jm = 0;
+  for (int j = 0; j < s; ++j)
+    if (coef_host[j] != 0.0) jm |= 1u << j;
   const Pattern* P = C->pat;
   unsigned g = (unsigned)((m + kBlock - 1) / kBlock);
   IRK_STAGE_SWITCH(s, (k_stage_couple<SS><<<g, kBlock, 0, ctx->stream>>>(
-                          m, i, P->slice_ptr, P->sell_col, C->val, cf, rowmask_dev, R_dev, X_dev,
-                          out_dev, ld_out)))
+                          m, i, P->slice_ptr, P->ellw, P->colhdr, P->sell_col, C->uval, C->val,
+                          cf, jm, rowmask_dev, R_dev, X_dev, out_dev, ld_out)))
   IRK_CHECK_LAUNCH(ctx);
   return IRK_OK;
 }
@@ -948,9 +971,12 @@ int irk_stage_rhs(irk_ctx* ctx, int64_t m, int s, double a, const irk_mat* B, co
   unsigned g = (unsigned)((m + kBlock - 1) / kBlock);
   const int* sp = B ? B->pat->slice_ptr : nullptr;
   const int* sc = B ? B->pat->sell_col : nullptr;
+  const int* ch = B ? B->pat->colhdr : nullptr;
+  const int ew = B ? B->pat->ellw : 0;
   const double* bv = B ? B->val : nullptr;
-  IRK_STAGE_SWITCH(s, (k_stage_rhs<SS><<<g, kBlock, 0, ctx->stream>>>(m, sp, sc, bv, a, u_dev, G,
-                                                                      F_dev, Out_dev)))
+  const double* ub = B ? B->uval : nullptr;
+  IRK_STAGE_SWITCH(s, (k_stage_rhs<SS><<<g, kBlock, 0, ctx->stream>>>(m, sp, ew, ch, sc, ub, bv, a,
+                                                                      u_dev, G, F_dev, Out_dev)))
   IRK_CHECK_LAUNCH(ctx);
   return IRK_OK;
 }
