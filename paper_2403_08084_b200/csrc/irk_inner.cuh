@@ -965,17 +965,6 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
     }
     return IRK_OK;
   };
-  {
-    GraphKey ki;
-    ki.add((const void*)&k_cg_init<T, NB, HASB>).add(m).add(G).add(A).add(P).add(shift);
-    ki.add(mask).add(w).add(red).add(cnt).add(rtol).add(atol);
-    ki.add(prec ? prec->uid : (uint64_t)0);
-    if (graph_off) {
-      IRK_TRY(init_body(s));
-    } else {
-      IRK_TRY(graph_launch(ctx, ki.k, init_body));
-    }
-  }
   // pinned mirrors: two polls in flight, each of both states
   SysState<T>* hst = reinterpret_cast<SysState<T>*>(ctx->pinned);
   const int chunk = m < 65536 ? 8 : 16;
@@ -1048,6 +1037,30 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
     }
     return IRK_OK;
   };
+  // iterations issued with the init sequence (external preconditioner and
+  // graph-resident loop only; even, so the loop keeps its parities)
+  static const int prefix_env =
+      getenv("IRK_CG_PREFIX") ? std::max(0, atoi(getenv("IRK_CG_PREFIX")) & ~1) : 4;
+  static const bool while_off = getenv("IRK_NO_WHILE") != nullptr;  // A/B: chunked graphs
+  const int prefix = (prec && maxit > 0 && !graph_off && !while_off) ? prefix_env : 0;
+  {
+    GraphKey ki;
+    ki.add((const void*)&k_cg_init<T, NB, HASB>).add(m).add(G).add(A).add(P).add(shift);
+    ki.add(mask).add(w).add(red).add(cnt).add(rtol).add(atol);
+    ki.add(prec ? prec->uid : (uint64_t)0).add(prefix).add(stencil).add(maxit);
+    if (graph_off) {
+      IRK_TRY(init_body(s));
+    } else {
+      // the first `prefix` iterations ride in the init graph (straight-line
+      // graphs run the V-cycle-preconditioned iteration ~20 us faster than
+      // the body of the conditional WHILE node); later ones are no-ops once
+      // the state is finished
+      IRK_TRY(graph_launch(ctx, ki.k, [&](cudaStream_t cs) -> int {
+        IRK_TRY(init_body(cs));
+        return chunk_body(cs, 0, prefix);
+      }));
+    }
+  }
   // The key holds every launch argument of the loop kernels.
   GraphKey key;
   key.add((const void*)&k_cg_spmv<T, NB, HASB, MAXW>).add((const void*)&k_cg_update<T, NB>);
@@ -1055,7 +1068,7 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   key.add(m).add(G).add(A).add(P).add(shift).add(mask).add(w).add(red);
   key.add(maxit).add(prec ? prec->uid : (uint64_t)0);
   int64_t body_kernels = 0;  // kernels per pass of the graph-resident loop
-  if (maxit > 0 && !graph_off) {
+  if (maxit > 0 && !graph_off && !while_off) {
     // The whole iteration loop is ONE graph: a conditional WHILE node whose
     // body runs two iterations (both parities) and then sets the loop
     // condition from the device state; termination never returns to the
@@ -1065,7 +1078,8 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
     IRK_TRY(graph_launch_while(
         ctx, kw.k,
         [&](cudaStream_t cs, cudaGraphConditionalHandle h) -> int {
-          IRK_TRY(chunk_body(cs, 0, 2));
+          static const int body_its = getenv("IRK_WHILE_BODY") ? atoi(getenv("IRK_WHILE_BODY")) : 2;
+          IRK_TRY(chunk_body(cs, 0, body_its));
           launch(k_cg_cond<T>, 1, 32, 0, cs, h, st0, st1);
           IRK_CHECK_LAUNCH(ctx);
           return IRK_OK;
@@ -1127,7 +1141,8 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
                           : (hst[0].iter >= hst[1].iter ? hst[0] : hst[1]);
   // body passes executed by the graph-resident loop: iterations in pairs,
   // plus the pass in which the finished state was observed
-  if (body_kernels) ctx->launches += body_kernels * ((int64_t)fs.iter / 2 + 1);
+  if (body_kernels)
+    ctx->launches += body_kernels * ((int64_t)std::max(fs.iter - prefix, 0) / 2 + 1);
   int status = IRK_OK;
   for (int k = 0; k < NB; ++k) {
     if (its_host) its_host[k] = fs.its[k];
