@@ -655,6 +655,96 @@ __global__ void __launch_bounds__(kBlock, 4)
   block_reduce_store<double, 1>(mus, cg_part<double, 1>(red, gridDim.x, cpar).mu);
 }
 
+__device__ __forceinline__ double ldv(const double* p) { return __ldg(p); }
+__device__ __forceinline__ cplx ldv(const cplx* p) {
+  const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+  return {v.x, v.y};
+}
+
+// Stencil variant of k_cg_spmv for NB batched systems and complex
+// scalars (the block-Jacobi surrogate blocks, the Schur-pair COCG): one warp
+// per SELL slice; the slot headers are loaded once per slice (lane k holds
+// slot k) and checked with one warp vote while the gathers at the stencil
+// offsets are already in flight (z and p_old carry a readable halo of `pad`
+// rows); a plain stencil slice then forms each system's coefficient from
+// the broadcast headers.  Other slices take the SELL row path.
+template <typename T, int NB, int W, bool HASB>
+__global__ void __launch_bounds__(kBlock, 2)
+    k_cg_spmv_stn(int m, MatView A, const SysParams<T> P, const double* __restrict__ shift,
+                  const uint8_t* __restrict__ mask, const T* __restrict__ z,
+                  const T* __restrict__ pold, T* __restrict__ pnew, T* __restrict__ q,
+                  const SysState<T>* sin, SysState<T>* sout, double* red, int cpar, int maxit) {
+  IRK_PDL_ENTER();
+  T beta[NB];
+  bool act[NB];
+  if (cg_enter_a<T, NB>(sin, sout, red, cpar, maxit, beta, act)) return;
+  const int lane = threadIdx.x & 31;
+  const int nsl = (m + kSlice - 1) / kSlice;
+  const int wstride = gridDim.x * (blockDim.x / 32);
+  T mu[NB];
+#pragma unroll
+  for (int k = 0; k < NB; ++k) mu[k] = s_zero(T{});
+  for (int sl = (blockIdx.x * blockDim.x + threadIdx.x) / 32; sl < nsl; sl += wstride) {
+    const int row = sl * kSlice + lane;
+    const bool valid = row < m;
+    const int q0 = sl * W;
+    const bool hl = lane < W;
+    const int hd = hl ? __ldg(A.colhdr + q0 + lane) : 0;
+    const double ha = hl ? __ldg(A.ua + q0 + lane) : 0.0;
+    const double hb = (HASB && hl) ? __ldg(A.ub + q0 + lane) : 0.0;
+    T pr[NB], acc[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      const int64_t qi = (int64_t)row * NB + k;
+      pr[k] = s_add(ldv(z + qi), s_mul(beta[k], ldv(pold + qi)));
+      acc[k] = s_zero(T{});
+    }
+    const bool ok = __all_sync(0xffffffffu, !hl || (hd == A.sd[lane < W ? lane : 0] &&
+                                                    !isnan(ha) && !(HASB && isnan(hb))));
+    if (ok) {
+#pragma unroll
+      for (int kk = 0; kk < W; ++kk) {
+        const double a = __shfl_sync(0xffffffffu, ha, kk);
+        const double b = HASB ? __shfl_sync(0xffffffffu, hb, kk) : 0.0;
+        const int64_t qc = (int64_t)(row + A.sd[kk]) * NB;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          const T pc = s_add(ldv(z + qc + k), s_mul(beta[k], ldv(pold + qc + k)));
+          acc[k] = s_add(acc[k], s_mul(s_coef(P.alpha[k], P.beta[k], a, b), pc));
+        }
+      }
+    } else if (valid) {
+      const int base = sl * kSlice * W;
+#pragma unroll
+      for (int kk = 0; kk < W; ++kk) {
+        const int pos = base + kk * kSlice + lane;
+        const int c = sell_col_at(A.colhdr, A.sell_col, q0 + kk, pos, row);
+        const double av = sell_val_at(A.ua, A.a, q0 + kk, pos);
+        const double bv = HASB ? sell_val_at(A.ub, A.b, q0 + kk, pos) : 0.0;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          const int64_t qc = (int64_t)c * NB + k;
+          const T pc = s_add(ldv(z + qc), s_mul(beta[k], ldv(pold + qc)));
+          acc[k] = s_add(acc[k], s_mul(s_coef(P.alpha[k], P.beta[k], av, bv), pc));
+        }
+      }
+    }
+    if (!valid) continue;
+    const bool flagged = mask && mask[row];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      if (shift) acc[k] = s_add(acc[k], s_mul(s_real<T>(shift[(int64_t)row * NB + k]), pr[k]));
+      if (flagged) acc[k] = pr[k];
+      if (!act[k]) continue;
+      const int64_t qi = (int64_t)row * NB + k;
+      pnew[qi] = pr[k];
+      q[qi] = acc[k];
+      mu[k] = s_add(mu[k], s_mul(pr[k], acc[k]));
+    }
+  }
+  block_reduce_store<T, NB>(mu, cg_part<T, NB>(red, gridDim.x, cpar).mu);
+}
+
 // x += alpha p, r -= alpha q, z = D^-1 r; partials of rho' = r^T z and
 // rr = ||r||^2 (the next A kernel decides convergence / cap / beta).
 // EXTZ: an external preconditioner forms z (and the r.z partials) after
@@ -926,7 +1016,7 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   IRK_REQUIRE(!prec || kExtOk, "run_cg: external preconditioner needs one real system");
   Workspace<T> w;
   int64_t pad = 0;
-  if (NB == 1 && sizeof(T) == 8 && A.sw > 0) {
+  if (A.sw > 0) {
     for (int k = 0; k < A.sw; ++k) pad = std::max<int64_t>(pad, std::abs(A.sd[k]));
     pad += kSlice;
   }
@@ -972,6 +1062,10 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   static const bool stencil_off = getenv("IRK_NO_STENCIL") != nullptr;
   const bool stencil = kStencil && !stencil_off && w.pad > 0 && m < INT_MAX / 2 &&
                        (A.sw == 3 || A.sw == 5 || A.sw == 7 || A.sw == 9);
+  // batched / complex systems on the P1 grid stencils (7-point 2D, 15-point 3D)
+  constexpr bool kStencilN = !kStencil && MAXW > 0 && NB <= 4;
+  constexpr int kWN = MAXW == 8 ? 7 : 15;
+  const bool stencil_n = kStencilN && !stencil_off && w.pad > 0 && m < INT_MAX / 2 && A.sw == kWN;
   T* pbuf[2] = {w.p0, w.p1};
   // kernel A of iteration `it` (parity it & 1; the state says whether it
   // is the first one after the init)
@@ -998,6 +1092,14 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
         else if (A.sw == 5) IRK_ST(5);
         else IRK_ST(3);
 #undef IRK_ST
+      }
+    }
+    if constexpr (kStencilN) {
+      if (stencil_n) {
+        launch(k_cg_spmv_stn<T, NB, kWN, HASB>, G, kBlock, 0, cs, (int)m, A, P, shift, mask, w.z,
+               pold, pnew, w.q, sin, sout, red, c, maxit);
+        IRK_CHECK_LAUNCH(ctx);
+        return IRK_OK;
       }
     }
     if (!stencil)
@@ -1064,7 +1166,7 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   // The key holds every launch argument of the loop kernels.
   GraphKey key;
   key.add((const void*)&k_cg_spmv<T, NB, HASB, MAXW>).add((const void*)&k_cg_update<T, NB>);
-  key.add(stencil);
+  key.add(stencil).add(stencil_n);
   key.add(m).add(G).add(A).add(P).add(shift).add(mask).add(w).add(red);
   key.add(maxit).add(prec ? prec->uid : (uint64_t)0);
   int64_t body_kernels = 0;  // kernels per pass of the graph-resident loop
