@@ -271,6 +271,7 @@ def run_ours(args, world, rank, local):
     if True:
         torch.cuda.synchronize()
         w_t0 = time.perf_counter()
+        torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/
         e0.record(stream)
         marks = []
         sample_at = {args.steps // 3, (2 * args.steps) // 3, args.steps - 1}
@@ -288,6 +289,7 @@ def run_ours(args, world, rank, local):
                 ev.record(stream)
                 marks.append((ev, time.perf_counter()))
         e1.record(stream)
+        torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
         clk.mark(w_t0, time.perf_counter())
     clk.__exit__(None, None, None)
