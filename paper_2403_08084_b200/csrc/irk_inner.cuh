@@ -391,10 +391,33 @@ __device__ __forceinline__ void state_copy(SysState<T>* dst, const SysState<T>* 
 }
 
 // Prologue of A_k: returns true when the solve is finished (all threads).
+// Sum of n partials (any n) in a fixed order, all blocks alike.
+__device__ __forceinline__ double reduce_partials_n(const double* part, int n) {
+  __shared__ double pr[kBlock / 32];
+  __shared__ double res;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double v = 0.0;
+  for (int b = threadIdx.x; b < n; b += kBlock) v += __ldcg(part + b);
+  v = warp_sum(v);
+  if (lane == 0) pr[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kBlock / 32; ++w) t += pr[w];
+    res = t;
+  }
+  __syncthreads();
+  return res;
+}
+
+// ext_rz / n_ext: r.z partials written by a fused external preconditioner
+// (its last kernel, n_ext blocks) replace the rz partials; the fresh state
+// then takes rho from them (no separate rho kernel after the init).
 template <typename T, int NB>
 __device__ __forceinline__ bool cg_enter_a(const SysState<T>* sin, SysState<T>* sout,
                                            double* red, int c, int maxit,
-                                           T (&beta)[NB], bool (&act)[NB]) {
+                                           T (&beta)[NB], bool (&act)[NB],
+                                           const double* ext_rz = nullptr, int n_ext = 0) {
   __shared__ SysState<T> S;
   __shared__ T smu[NB], srz[NB];
   __shared__ double srr[NB];
@@ -405,6 +428,24 @@ __device__ __forceinline__ bool cg_enter_a(const SysState<T>* sin, SysState<T>* 
     // from the init kernel); reduce_partials3 synchronises
     const CgPart<T, NB> pin = cg_part<T, NB>(red, G, c ^ 1);
     reduce_partials3<T, NB>(pin.mu, pin.rz, pin.rr, G, smu, srz, srr);
+  }
+  if constexpr (NB == 1 && sizeof(T) == 8) {
+    if (ext_rz) {
+      const double v = reduce_partials_n(ext_rz, n_ext);
+      if (threadIdx.x == 0) {
+        reinterpret_cast<double*>(srz)[0] = v;
+        if (S.fresh && !S.done && S.active[0]) {
+          if (!isfinite(v) || v == 0.0) {  // as k_cg_rho_init
+            S.active[0] = 0;
+            S.code[0] = 2;
+            S.done = 1;
+          } else {
+            reinterpret_cast<double*>(S.rho)[0] = v;
+          }
+        }
+      }
+      __syncthreads();
+    }
   }
   const bool first = S.fresh != 0;
   if (S.done) {
@@ -495,11 +536,12 @@ __global__ void __launch_bounds__(kBlock, 4)
     k_cg_spmv(int64_t m, MatView A, const SysParams<T> P, const double* __restrict__ shift,
               const uint8_t* __restrict__ mask, const T* __restrict__ z,
               const T* __restrict__ pold, T* __restrict__ pnew, T* __restrict__ q,
-              const SysState<T>* sin, SysState<T>* sout, double* red, int c, int maxit) {
+              const SysState<T>* sin, SysState<T>* sout, double* red, int c, int maxit,
+              const double* ext_rz, int n_ext) {
   IRK_PDL_ENTER();
   T beta[NB];
   bool act[NB];
-  if (cg_enter_a<T, NB>(sin, sout, red, c, maxit, beta, act)) return;
+  if (cg_enter_a<T, NB>(sin, sout, red, c, maxit, beta, act, ext_rz, n_ext)) return;
   T mu[NB];
 #pragma unroll
   for (int k = 0; k < NB; ++k) mu[k] = s_zero(T{});
@@ -597,11 +639,11 @@ __global__ void __launch_bounds__(kBlock, 4)
                  const uint8_t* __restrict__ mask, const double* __restrict__ z,
                  const double* __restrict__ pold, double* __restrict__ pnew,
                  double* __restrict__ q, const SysState<double>* sin, SysState<double>* sout,
-                 double* red, int cpar, int maxit) {
+                 double* red, int cpar, int maxit, const double* ext_rz, int n_ext) {
   IRK_PDL_ENTER();
   double betas[1];
   bool acts[1];
-  if (cg_enter_a<double, 1>(sin, sout, red, cpar, maxit, betas, acts)) return;
+  if (cg_enter_a<double, 1>(sin, sout, red, cpar, maxit, betas, acts, ext_rz, n_ext)) return;
   const double beta = betas[0];
   const bool act = acts[0];
   const int lane = threadIdx.x & 31;
@@ -874,6 +916,13 @@ static __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// The skip predicate (shared by k_cg_skip and the fused preconditioners):
+// the next A kernel will end the solve (converged, cap, finished).
+__device__ __forceinline__ bool cg_skip_pred(const SysState<double>* st, double rr, int maxit) {
+  return __ldcg(&st->done) || !__ldcg(&st->active[0]) || !(rr > __ldcg(&st->tol2[0])) ||
+         __ldcg(&st->its[0]) + 1 >= maxit;
+}
+
 // After the update kernel of an iteration with an external preconditioner:
 // decide from the ||r||^2 partials (same reduction order as the next A
 // kernel) whether that A kernel will end the solve (converged, cap,
@@ -883,10 +932,7 @@ static __global__ void __launch_bounds__(kBlock)
   IRK_PDL_ENTER();
   __shared__ double srr[1];
   reduce_partials<double, 1>(cg_part<double, 1>(const_cast<double*>(red), G, c).rr, G, srr);
-  if (threadIdx.x == 0) {
-    const double rr = srr[0];
-    st->skip = st->done || !st->active[0] || !(rr > st->tol2[0]) || st->its[0] + 1 >= maxit;
-  }
+  if (threadIdx.x == 0) st->skip = cg_skip_pred(st, srr[0], maxit);
 }
 
 // Loop condition of the graph-resident CG loop: continue while neither
@@ -924,14 +970,31 @@ __global__ void k_cg_log(const SysState<T>* a, const SysState<T>* b, int nb, int
 // External preconditioner z = P^-1 r for the real one-system CG (the
 // geometric multigrid of irk_mg.cu): a fixed, graph-capturable kernel
 // sequence on the given stream.
+// Skip decision of a fused preconditioner application (what k_cg_skip
+// decides): st == nullptr -> always apply (the init application).
+struct SkipCtl {
+  SysState<double>* st = nullptr;
+  const double* rr = nullptr;  // ||r||^2 partials of the update kernel (G of them)
+  int G = 0, maxit = 0;
+};
+
 struct CgPrec {
   uint64_t uid = 0;  // unique per instance (graph-cache key; addresses get reused)
   // stop: device flag; when nonzero at run time the kernels do nothing (the
   // solve finished inside a graph-resident loop)
   virtual int apply(irk_ctx* ctx, cudaStream_t s, const double* r, double* z,
                     const int* stop) = 0;
+  // Fused variant (0 partials: not supported): the first kernel takes the
+  // skip decision itself and publishes it in st->skip for the others; the
+  // last kernel writes fused_rz_count() partials of r.z to rz_part.
+  virtual int fused_rz_count() { return 0; }
+  virtual int apply_fused(irk_ctx* ctx, cudaStream_t s, const double* r, double* z,
+                          const SkipCtl& sk, double* rz_part) {
+    return IRK_EINVAL;
+  }
   virtual ~CgPrec() {}
 };
+
 
 template <typename T, int NB>
 __global__ void k_cg_store(int64_t m, const T* __restrict__ x, T* __restrict__ out,
@@ -1022,7 +1085,11 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   }
   IRK_TRY(carve<T>(ctx, m, NB, w, pad));
   const int G = grid_for(ctx, m, kBlock, 4);
-  IRK_TRY(ensure_red(ctx, 2 * cg_part_doubles<T, NB>(G) + (size_t)G * NB * 4 + 64));
+  // a fused preconditioner writes its r.z partials (two parities) past the
+  // loop and init partials
+  const int n_ext = (prec && NB == 1 && sizeof(T) == 8) ? prec->fused_rz_count() : 0;
+  const size_t red_base = 2 * cg_part_doubles<T, NB>(G) + (size_t)G * NB * 4 + 64;
+  IRK_TRY(ensure_red(ctx, red_base + 2 * (size_t)n_ext));
   IRK_TRY(ensure_pinned(ctx, 4 * sizeof(SysState<T>) + 64));
   cudaStream_t s = ctx->stream;
   unsigned int* cnt = ctx->counters + 4;
@@ -1043,7 +1110,13 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
                                                  red + 2 * cg_part_doubles<T, NB>(G), cnt);
     IRK_CHECK_LAUNCH(ctx);
     if constexpr (kExtOk) {
-      if (prec) {
+      if (prec && n_ext) {
+        // rho comes from the preconditioner's r.z partials (parity 1, read
+        // by A_0), taken by the first A kernel
+        IRK_TRY(prec->apply_fused(ctx, cs, reinterpret_cast<double*>(w.r),
+                                  reinterpret_cast<double*>(w.z), SkipCtl{},
+                                  red + red_base + n_ext));
+      } else if (prec) {
         double* rr_ = reinterpret_cast<double*>(w.r);
         double* zz_ = reinterpret_cast<double*>(w.z);
         IRK_TRY(prec->apply(ctx, cs, rr_, zz_, nullptr));
@@ -1084,9 +1157,10 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
         const SysParams<double>& Pd = reinterpret_cast<const SysParams<double>&>(P);
         const SysState<double>* si = reinterpret_cast<const SysState<double>*>(sin);
         SysState<double>* so = reinterpret_cast<SysState<double>*>(sout);
+        const double* ext = n_ext ? red + red_base + (size_t)(c ^ 1) * n_ext : nullptr;
 #define IRK_ST(WW)                                                                            \
   launch(k_cg_spmv_st<WW, HASB>, G, kBlock, 0, cs, (int)m, A, Pd, shift, mask, zz, po, pn, qq, si, \
-                                              so, red, c, maxit)
+                                              so, red, c, maxit, ext, n_ext)
         if (A.sw == 7) IRK_ST(7);
         else if (A.sw == 9) IRK_ST(9);
         else if (A.sw == 5) IRK_ST(5);
@@ -1104,7 +1178,8 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
     }
     if (!stencil)
       launch(k_cg_spmv<T, NB, HASB, MAXW>, G, kBlock, 0, cs, m, A, P, shift, mask, w.z, pold, pnew,
-                                                         w.q, sin, sout, red, c, maxit);
+             w.q, sin, sout, red, c, maxit,
+             n_ext ? red + red_base + (size_t)(c ^ 1) * n_ext : (const double*)nullptr, n_ext);
     IRK_CHECK_LAUNCH(ctx);
     return IRK_OK;
   };
@@ -1118,6 +1193,15 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
         double* rr_ = reinterpret_cast<double*>(w.r);
         double* zz_ = reinterpret_cast<double*>(w.z);
         SysState<double>* sc = reinterpret_cast<SysState<double>*>(c ? st1 : st0);
+        if (n_ext) {
+          // the preconditioner decides the skip and writes r.z partials
+          SkipCtl sk;
+          sk.st = sc;
+          sk.rr = cg_part<double, 1>(red, G, c).rr;
+          sk.G = G;
+          sk.maxit = maxit;
+          return prec->apply_fused(ctx, cs, rr_, zz_, sk, red + red_base + (size_t)c * n_ext);
+        }
         launch(k_cg_skip, 1, kBlock, 0, cs, sc, red, G, c, maxit);
         IRK_CHECK_LAUNCH(ctx);
         IRK_TRY(prec->apply(ctx, cs, rr_, zz_, &sc->skip));
@@ -1149,7 +1233,7 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
     GraphKey ki;
     ki.add((const void*)&k_cg_init<T, NB, HASB>).add(m).add(G).add(A).add(P).add(shift);
     ki.add(mask).add(w).add(red).add(cnt).add(rtol).add(atol);
-    ki.add(prec ? prec->uid : (uint64_t)0).add(prefix).add(stencil).add(maxit);
+    ki.add(prec ? prec->uid : (uint64_t)0).add(prefix).add(stencil).add(maxit).add(n_ext);
     if (graph_off) {
       IRK_TRY(init_body(s));
     } else {
@@ -1166,7 +1250,7 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   // The key holds every launch argument of the loop kernels.
   GraphKey key;
   key.add((const void*)&k_cg_spmv<T, NB, HASB, MAXW>).add((const void*)&k_cg_update<T, NB>);
-  key.add(stencil).add(stencil_n);
+  key.add(stencil).add(stencil_n).add(n_ext);
   key.add(m).add(G).add(A).add(P).add(shift).add(mask).add(w).add(red);
   key.add(maxit).add(prec ? prec->uid : (uint64_t)0);
   int64_t body_kernels = 0;  // kernels per pass of the graph-resident loop

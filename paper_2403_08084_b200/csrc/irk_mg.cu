@@ -458,9 +458,20 @@ __device__ __forceinline__ void cheb_rows(int h, const Sten2& S, const double* _
 template <int TX, int TY, int NU, bool F9>
 __global__ void __launch_bounds__(kBlock)
     k_mg2_pre(int n1, Sten2 S, ChebS C, const double* __restrict__ b, double* __restrict__ x2,
-              const int* stop) {
+              const int* stop, SkipCtl sk) {
   IRK_PDL_ENTER();
-  if (stop && *stop) return;
+  if (sk.st) {
+    // fused CG: the skip decision of k_cg_skip, taken by every CTA from the
+    // update kernel's partials (same order) and published for the rest of
+    // the V-cycle
+    __shared__ double srr[1];
+    reduce_partials<double, 1>(sk.rr, sk.G, srr);
+    const bool skip = cg_skip_pred(sk.st, srr[0], sk.maxit);
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) sk.st->skip = skip ? 1 : 0;
+    if (skip) return;
+  } else if (stop && *stop) {
+    return;
+  }
   constexpr int HX = NU - 1, WL = TX + 2 * HX, HL = TY + 2 * HX;
   using R = Region<WL, HL>;
   __shared__ double sb[WL * HL], sx[2][WL * HL];
@@ -557,7 +568,7 @@ template <int TX, int TY, int NU, bool F9>
 __global__ void __launch_bounds__(kBlock, 4)
     k_mg2_post(int n1, int n1c, Sten2 S, ChebS C, const double* __restrict__ b,
                const double* __restrict__ x2, const double* __restrict__ ec,
-               double* __restrict__ z, const int* stop) {
+               double* __restrict__ z, const int* stop, double* __restrict__ rz_part) {
   IRK_PDL_ENTER();
   if (stop && *stop) return;
   constexpr int HX = NU, WL = TX + 2 * HX, HL = TY + 2 * HX;
@@ -603,17 +614,37 @@ __global__ void __launch_bounds__(kBlock, 4)
     __syncthreads();
     cur ^= 1;
   }
+  double rz = 0.0;  // r.z of the written points (fused CG: rz_part)
   cheb_rows<TX, TY, HX, F9>(0, S, sx[cur], sx[cur ^ 1], false, sb, C.cd[NU - 1],
                             C.cr[NU - 1] * S.dinv, ox, oy, N,
-                            [&](int, int gx, int gy, double v) {
+                            [&](int li, int gx, int gy, double v) {
                               if (gx > N || gy > N) return;
                               const int64_t g = (int64_t)gy * n1 + gx;
-                              z[g] = interior2(gx, gy, N) ? v : b[g];
+                              const bool in = interior2(gx, gy, N);
+                              const double bi = in ? sb[li] : b[g];
+                              const double zi = in ? v : bi;
+                              z[g] = zi;
+                              rz += bi * zi;
                             });
   boundary_lines<TX, TY>(N, [&](int gx, int gy) {
     const int64_t g = (int64_t)gy * n1 + gx;
-    z[g] = b[g];
+    const double bi = b[g];
+    z[g] = bi;
+    rz += bi * bi;
   });
+  if (rz_part) {
+    double v[1] = {rz};
+    __shared__ double red[kBlock / 32][1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v[0] = warp_sum(v[0]);
+    if (lane == 0) red[warp][0] = v[0];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kBlock / 32; ++w) t += red[w][0];
+      rz_part[blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+  }
 }
 
 // Restriction of level l fused with the pre-smoothing of level l+1 (one
@@ -1078,8 +1109,11 @@ struct irk_mg : public irk::CgPrec {
   }
   static constexpr int kRcSmem = 200 * 1024;
 
+  // sk / rz_part (fused CG, top level only): the top pre-smoother takes the
+  // skip decision, the top post-smoother writes the r.z partials
   int vcycle2(irk_ctx* ctx, cudaStream_t s, int l, const double* b, double* out,
-              const int* stop) {
+              const int* stop, const irk::SkipCtl& sk = irk::SkipCtl{},
+              double* rz_part = nullptr) {
     using namespace irk;
     if (l == (int)lev.size() - 1) return coarse2(ctx, s, b, out, stop);
     const MgLevel& L = lev[l];
@@ -1107,7 +1141,7 @@ struct irk_mg : public irk::CgPrec {
     else if (nu == 3) IRK_MG2(N_, KER, 3, __VA_ARGS__); \
     else IRK_MG2(N_, KER, 4, __VA_ARGS__);              \
   } while (0)
-    if (l == 0) IRK_NU(N, k_mg2_pre, n1, S, C2, b, x2, stop);  // the top level's pre
+    if (l == 0) IRK_NU(N, k_mg2_pre, n1, S, C2, b, x2, sk.st ? nullptr : stop, sk);  // top pre
     const MgLevel& Cc = lev[l + 1];
     const int n1c = (int)Cc.g.n1, Nc = n1c - 1;
     const bool last = l + 2 == (int)lev.size();
@@ -1149,14 +1183,14 @@ struct irk_mg : public irk::CgPrec {
         {
           const bool F = Fs || f9[l + 1];
           const Sten2& S1 = sten[l + 1];
-          IRK_NU(Nc, k_mg2_pre, n1c, S1, Cn, Cc.b, Cc.x[0], stop);
+          IRK_NU(Nc, k_mg2_pre, n1c, S1, Cn, Cc.b, Cc.x[0], stop, SkipCtl{});
         }
       }
     }
     if (cudaPeekAtLastError() != cudaSuccess) return IRK_ECUDA;
     if (!last) IRK_TRY(vcycle2(ctx, s, l + 1, Cc.b, Cc.x[1], stop));
     const double* ec = Cc.x[1];
-    IRK_NU(N, k_mg2_post, n1, n1c, S, C2, b, x2, ec, out, stop);
+    IRK_NU(N, k_mg2_post, n1, n1c, S, C2, b, x2, ec, out, stop, l == 0 ? rz_part : nullptr);
 #undef IRK_NU
 #undef IRK_MG2
     return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
@@ -1225,6 +1259,26 @@ struct irk_mg : public irk::CgPrec {
       cn.cr[k] = cr[k];
     }
     s2_ok = true;
+    return IRK_OK;
+  }
+
+  // fused CG support (structured path with at least two levels): the
+  // top-level post-smoother's CTAs write the r.z partials
+  int fused_rz_count() override {
+    static const bool off = getenv("IRK_MG_NOFUSE") || getenv("IRK_CG_NOFUSE");
+    if (off || !s2_on || lev.size() < 2) return 0;
+    const int N = (int)lev[0].g.n1 - 1;
+    return N >= 512 ? ((N + 63) / 64) * ((N + 15) / 16) : ((N + 31) / 32) * ((N + 7) / 8);
+  }
+
+  int apply_fused(irk_ctx* ctx, cudaStream_t s, const double* r, double* z,
+                  const irk::SkipCtl& sk, double* rz_part) override {
+    const int* stop = sk.st ? &sk.st->skip : nullptr;
+    const int e = vcycle2(ctx, s, 0, r, z, stop, sk, rz_part);
+    if (e != IRK_OK || cudaGetLastError() != cudaSuccess) {
+      irk::set_error("irk_mg: fused structured V-cycle launch failed");
+      return IRK_ECUDA;
+    }
     return IRK_OK;
   }
 
