@@ -90,7 +90,13 @@ def to_dev(x, dtype=None):
         return x.to(device=device(), dtype=dt).contiguous()
     np_dt = np.float64 if dt == torch.float64 else np.int64 if dt == torch.int64 else None
     arr = np.ascontiguousarray(np.asarray(x, dtype=np_dt))
-    return _STAGER.upload(torch.from_numpy(arr))
+    t = torch.from_numpy(arr)
+    if arr.nbytes >= (1 << 20) and t.is_pinned():
+        # numpy over pinned memory (e.g. an array step() returned): direct DMA
+        out = t.to(device(), non_blocking=True)
+        torch.cuda.current_stream(out.device).synchronize()
+        return out
+    return _STAGER.upload(t)
 
 
 class _PinnedStager:
