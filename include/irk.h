@@ -347,6 +347,26 @@ int irk_mg_pcg(irk_ctx* ctx, irk_mg* mg, const double* rhs_dev, int64_t ld_rhs, 
                int64_t ld_x, double rtol, double atol, int maxit, int* its_host,
                double* relres_host);
 
+/* ---- complex multigrid for the Schur-pair blocks ------------------------
+ * alpha M + beta K with complex alpha, beta (the 2x2 real-Schur pairs of the
+ * transformed stage preconditioner): levels M_l, K_l on N_l = N_0 / 2^l
+ * grids sharing one pattern per level, masked rows identity and masked
+ * columns eliminated (the caller passes eliminated copies); Chebyshev
+ * smoothing on D^-1 A with complex D over a real interval.  Replaces the
+ * batched Jacobi-COCG of irk_cocg for P1 grid blocks. */
+typedef struct irk_mgc irk_mgc;
+int irk_mgc_create(irk_ctx* ctx, int dim, int nlev, const int64_t* N_host,
+                   const irk_mat* const* M_levels, const irk_mat* const* K_levels,
+                   const uint8_t* const* masks, double alpha_re, double alpha_im, double beta_re,
+                   double beta_im, int nu, int ncoarse, irk_mgc** out);
+int irk_mgc_destroy(irk_mgc* mg);
+/* COCG on the level-0 block preconditioned by one complex V-cycle per
+ * iteration; rhs/x interleaved complex (re, im) with leading dimensions in
+ * doubles (even), 16-byte aligned; status and deferred logging as irk_pcg. */
+int irk_mgc_cocg(irk_ctx* ctx, irk_mgc* mg, const double* rhs_dev, int64_t ld_rhs,
+                 double* x_dev, int64_t ld_x, double rtol, double atol, int maxit,
+                 int* its_host, double* relres_host);
+
 #ifdef __cplusplus
 }
 #endif

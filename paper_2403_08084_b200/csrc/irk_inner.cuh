@@ -876,38 +876,42 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 // r.z partials of iteration parity c after an external preconditioner
-// (real, one system).  Same grid as the A/B kernels.
-static __global__ void __launch_bounds__(kBlock)
-    k_cg_dot_rz(int64_t m, const double* __restrict__ r, const double* __restrict__ z,
-                double* red, int c, const int* skip) {
+// (one system; the unconjugated bilinear form for complex COCG).  Same grid
+// as the A/B kernels.
+template <typename T>
+__global__ void __launch_bounds__(kBlock)
+    k_cg_dot_rz(int64_t m, const T* __restrict__ r, const T* __restrict__ z, double* red, int c,
+                const int* skip) {
   IRK_PDL_ENTER();
   if (skip && *skip) return;
-  double v = 0.0;
+  T v = s_zero(T{});
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x)
-    v += r[i] * z[i];
-  double vs[1] = {v};
-  block_reduce_store<double, 1>(vs, cg_part<double, 1>(red, gridDim.x, c).rz);
+    v = s_add(v, s_mul(r[i], z[i]));
+  T vs[1] = {v};
+  block_reduce_store<T, 1>(vs, cg_part<T, 1>(red, gridDim.x, c).rz);
 }
 
 // After the init kernel: rho = r.z for an external preconditioner's z
 // (last-block reduction, once per solve); breakdown ends the solve.
-static __global__ void __launch_bounds__(kBlock)
-    k_cg_rho_init(int64_t m, const double* __restrict__ r, const double* __restrict__ z,
-                  SysState<double>* st, double* part, unsigned int* counter) {
+template <typename T>
+__global__ void __launch_bounds__(kBlock)
+    k_cg_rho_init(int64_t m, const T* __restrict__ r, const T* __restrict__ z, SysState<T>* st,
+                  double* part, unsigned int* counter) {
   IRK_PDL_ENTER();
-  double v = 0.0;
+  T v = s_zero(T{});
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x)
-    v += r[i] * z[i];
-  double vs[1] = {v};
-  block_reduce_store<double, 1>(vs, part);
+    v = s_add(v, s_mul(r[i], z[i]));
+  T vs[1] = {v};
+  T* pt = reinterpret_cast<T*>(part);
+  block_reduce_store<T, 1>(vs, pt);
   if (last_block_inner(counter)) {
-    __shared__ double srho[1];
-    reduce_partials<double, 1>(part, gridDim.x, srho);
+    __shared__ T srho[1];
+    reduce_partials<T, 1>(pt, gridDim.x, srho);
     if (threadIdx.x == 0 && !st->done) {
       st->rho[0] = srho[0];
-      if (st->active[0] && (!isfinite(srho[0]) || srho[0] == 0.0)) {
+      if (st->active[0] && (!s_finite(srho[0]) || s_isnull(srho[0]))) {
         st->active[0] = 0;
         st->code[0] = 2;
         st->done = 1;
@@ -918,7 +922,8 @@ static __global__ void __launch_bounds__(kBlock)
 
 // The skip predicate (shared by k_cg_skip and the fused preconditioners):
 // the next A kernel will end the solve (converged, cap, finished).
-__device__ __forceinline__ bool cg_skip_pred(const SysState<double>* st, double rr, int maxit) {
+template <typename T>
+__device__ __forceinline__ bool cg_skip_pred(const SysState<T>* st, double rr, int maxit) {
   return __ldcg(&st->done) || !__ldcg(&st->active[0]) || !(rr > __ldcg(&st->tol2[0])) ||
          __ldcg(&st->its[0]) + 1 >= maxit;
 }
@@ -927,11 +932,12 @@ __device__ __forceinline__ bool cg_skip_pred(const SysState<double>* st, double 
 // decide from the ||r||^2 partials (same reduction order as the next A
 // kernel) whether that A kernel will end the solve (converged, cap,
 // non-finite); then the preconditioner application and r.z are skipped.
-static __global__ void __launch_bounds__(kBlock)
-    k_cg_skip(SysState<double>* st, const double* red, int G, int c, int maxit) {
+template <typename T>
+__global__ void __launch_bounds__(kBlock)
+    k_cg_skip(SysState<T>* st, const double* red, int G, int c, int maxit) {
   IRK_PDL_ENTER();
   __shared__ double srr[1];
-  reduce_partials<double, 1>(cg_part<double, 1>(const_cast<double*>(red), G, c).rr, G, srr);
+  reduce_partials<double, 1>(cg_part<T, 1>(const_cast<double*>(red), G, c).rr, G, srr);
   if (threadIdx.x == 0) st->skip = cg_skip_pred(st, srr[0], maxit);
 }
 
@@ -1075,8 +1081,8 @@ template <typename T, int NB, bool HASB, int MAXW>
 int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, const double* shift,
            const uint8_t* mask, const T* rhs, int64_t ld_rhs, T* xout, int64_t ld_x, double rtol,
            double atol, int maxit, int* its_host, double* relres_host, CgPrec* prec = nullptr) {
-  constexpr bool kExtOk = NB == 1 && sizeof(T) == 8;
-  IRK_REQUIRE(!prec || kExtOk, "run_cg: external preconditioner needs one real system");
+  constexpr bool kExtOk = NB == 1;
+  IRK_REQUIRE(!prec || kExtOk, "run_cg: external preconditioner needs one system");
   Workspace<T> w;
   int64_t pad = 0;
   if (A.sw > 0) {
@@ -1117,12 +1123,10 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
                                   reinterpret_cast<double*>(w.z), SkipCtl{},
                                   red + red_base + n_ext));
       } else if (prec) {
-        double* rr_ = reinterpret_cast<double*>(w.r);
-        double* zz_ = reinterpret_cast<double*>(w.z);
-        IRK_TRY(prec->apply(ctx, cs, rr_, zz_, nullptr));
-        launch(k_cg_rho_init, G, kBlock, 0, cs, m, rr_, zz_,
-                                            reinterpret_cast<SysState<double>*>(st1),
-                                            red + 2 * cg_part_doubles<T, NB>(G), cnt);
+        IRK_TRY(prec->apply(ctx, cs, reinterpret_cast<double*>(w.r),
+                            reinterpret_cast<double*>(w.z), nullptr));
+        launch(k_cg_rho_init<T>, G, kBlock, 0, cs, m, w.r, w.z, st1,
+               red + 2 * cg_part_doubles<T, NB>(G), cnt);
         IRK_CHECK_LAUNCH(ctx);
       }
     }
@@ -1192,7 +1196,8 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
         IRK_CHECK_LAUNCH(ctx);
         double* rr_ = reinterpret_cast<double*>(w.r);
         double* zz_ = reinterpret_cast<double*>(w.z);
-        SysState<double>* sc = reinterpret_cast<SysState<double>*>(c ? st1 : st0);
+        SysState<T>* sct = c ? st1 : st0;
+        SysState<double>* sc = reinterpret_cast<SysState<double>*>(sct);  // real path only
         if (n_ext) {
           // the preconditioner decides the skip and writes r.z partials
           SkipCtl sk;
@@ -1202,10 +1207,10 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
           sk.maxit = maxit;
           return prec->apply_fused(ctx, cs, rr_, zz_, sk, red + red_base + (size_t)c * n_ext);
         }
-        launch(k_cg_skip, 1, kBlock, 0, cs, sc, red, G, c, maxit);
+        launch(k_cg_skip<T>, 1, kBlock, 0, cs, sct, red, G, c, maxit);
         IRK_CHECK_LAUNCH(ctx);
-        IRK_TRY(prec->apply(ctx, cs, rr_, zz_, &sc->skip));
-        launch(k_cg_dot_rz, G, kBlock, 0, cs, m, rr_, zz_, red, c, &sc->skip);
+        IRK_TRY(prec->apply(ctx, cs, rr_, zz_, &sct->skip));
+        launch(k_cg_dot_rz<T>, G, kBlock, 0, cs, m, w.r, w.z, red, c, &sct->skip);
         IRK_CHECK_LAUNCH(ctx);
         return IRK_OK;
       }

@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(kBlock)
     // the V-cycle
     __shared__ double srr[1];
     reduce_partials<double, 1>(sk.rr, sk.G, srr);
-    const bool skip = cg_skip_pred(sk.st, srr[0], sk.maxit);
+    const bool skip = cg_skip_pred<double>(sk.st, srr[0], sk.maxit);
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) sk.st->skip = skip ? 1 : 0;
     if (skip) return;
   } else if (stop && *stop) {

@@ -262,6 +262,23 @@ class StagePreconditioner:
                            ca=(ca_re, ca_im), cb=(cb_re, cb_im), ra=real_a, rb=real_b)
         return self._schur
 
+    def _schur_mg(self, plan, Md, Kd):
+        """Complex multigrid hierarchies of the pair blocks (None when the
+        blocks are not P1 grid operators with a full-boundary mask)."""
+        if "mgc" not in plan:
+            hs = []
+            for k in range(plan["np"]):
+                a = complex(plan["ca"][0][k], plan["ca"][1][k])
+                b = complex(plan["cb"][0][k], plan["cb"][1][k])
+                h = la._MgcHierarchy.build(self.M, self.Ks[0], Md, Kd, a, b, self.mask(),
+                                           self.settings)
+                if h is None:
+                    hs = None
+                    break
+                hs.append(h)
+            plan["mgc"] = hs
+        return plan["mgc"]
+
     def _apply_schur(self, R, X):
         plan = self._schur_plan()
         mats = [d.eliminated(self.mask()) for d in self._device_mats()]
@@ -274,7 +291,23 @@ class StagePreconditioner:
         call("irk_stage_mix", ctx(), m, sp_, s, hptr(plan["L"]), ptr(R), ptr(W))
         st = self.settings
         npairs, nr = plan["np"], plan["nr"]
-        if npairs:
+        mgc = self._schur_mg(plan, Md, Kd) if npairs else None
+        if mgc is not None:
+            # one multigrid-preconditioned COCG per pair block (complex V-cycle)
+            defer = self.defer_solves and not st.raise_on_maxit
+            for k in range(npairs):
+                its = np.zeros(1, dtype=np.int32)
+                rel = np.zeros(1)
+                status = _lib.load().irk_mgc_cocg(
+                    ctx(), mgc[k].handle, ptr(W[2 * k:]), sp_, ptr(Z[2 * k:]), sp_,
+                    float(st.rtol), float(st.atol), int(st.maxit),
+                    None if defer else hptr(its), None if defer else hptr(rel))
+                if defer:
+                    _lib.check(status, "deferred pair solve")
+                    self.inner_iterations.append([None])
+                else:
+                    self._inner_status(status, its[:1])
+        elif npairs:
             its = np.zeros(8, dtype=np.int32)
             rel = np.zeros(8)
             arrs = [np.ascontiguousarray(v + [0.0] * (8 - npairs), dtype=np.float64)

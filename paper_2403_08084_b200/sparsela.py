@@ -128,7 +128,9 @@ class _PinnedStager:
             buf = self._buf[i] = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8,
                                              pin_memory=True)
         host = buf[:nbytes].view(t.dtype).view(t.shape)
-        host.copy_(t)
+        # single-threaded numpy copy into the pinned slot (torch's CPU copy_
+        # fans out to the intra-op thread pool: milliseconds on a busy host)
+        np.copyto(host.numpy(), t.numpy())
         out = host.to(device(), non_blocking=True)
         ev = self._ev[i] = self._ev[i] or torch.cuda.Event()
         ev.record()
@@ -656,6 +658,80 @@ class _MgHierarchy:
     @structured.setter
     def structured(self, on: bool):
         call("irk_mg_set_structured", self.handle, int(bool(on)))
+
+
+class _MgcHierarchy:
+    """Complex multigrid of a Schur-pair block alpha*M + beta*K (complex
+    alpha, beta; libirk irk_mgc_*): the P1 levels of M and K re-assembled on
+    N/2^l grids, masked rows/columns eliminated, combined on the fly.  Same
+    coarsening rule as _MgHierarchy with |beta| / (|alpha| H^2)."""
+
+    def __init__(self, handle, keep):
+        self.handle = handle
+        self._keep = keep
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.load().irk_mgc_destroy(self.handle)
+        except Exception:  # interpreter shutdown
+            pass
+
+    @property
+    def levels(self):
+        return len(self._keep[0])
+
+    @staticmethod
+    def build(M, K, Md, Kd, alpha: complex, beta: complex, mask, settings):
+        """M, K: the SparseMatrix pair (grid-tagged); Md, Kd: their device
+        copies with the mask eliminated (level 0)."""
+        grid = getattr(M, "_p1_grid", None)
+        if grid is None or getattr(K, "_p1_grid", None) != grid or abs(alpha) == 0:
+            return None
+        if settings.method not in ("auto", "mg"):
+            return None
+        dim, N = grid
+        torch = _torch()
+        n1 = N + 1
+        if mask is not None:
+            idx = torch.arange(n1 ** dim, device=mask.device)
+            on = torch.zeros_like(idx, dtype=torch.bool)
+            for d in range(dim):
+                k = (idx // n1 ** d) % n1
+                on |= (k == 0) | (k == N)
+            if not torch.equal(on, mask.bool()):
+                return None
+        Ns, ms, ks, masks = [N], [Md], [Kd], [mask]
+        while Ns[-1] % 2 == 0 and Ns[-1] // 2 >= 4 and len(Ns) < 12:
+            H = 1.0 / Ns[-1]
+            if abs(beta) / (abs(alpha) * H * H) <= settings.mg_coarse_ratio:
+                break
+            Nc = Ns[-1] // 2
+            hM, hK = C.c_void_p(), C.c_void_p()
+            call("irk_mat_assemble_p1", ctx(), dim, Nc, C.byref(hM), C.byref(hK))
+            Mc, Kc = DeviceMatrix(hM), DeviceMatrix(hK)
+            mc = None
+            if mask is not None:
+                shape = (Ns[-1] + 1,) * dim
+                mc = masks[-1].reshape(shape)[(slice(None, None, 2),) * dim].contiguous()
+                mc = mc.reshape(-1)
+                Mc, Kc = Mc.eliminated(mc), Kc.eliminated(mc)
+            Ns.append(Nc)
+            ms.append(Mc)
+            ks.append(Kc)
+            masks.append(mc)
+        L = len(Ns)
+        Nh = np.ascontiguousarray(Ns, dtype=np.int64)
+        hm = (C.c_void_p * L)(*[A.handle for A in ms])
+        hk = (C.c_void_p * L)(*[A.handle for A in ks])
+        mp = (C.c_void_p * L)(*[ptr(m) if m is not None else None for m in masks])
+        h = C.c_void_p()
+        nu = int(settings.mg_nu) or 2
+        call("irk_mgc_create", ctx(), dim, L, hptr(Nh), C.cast(hm, C.c_void_p),
+             C.cast(hk, C.c_void_p), C.cast(mp, C.c_void_p), float(alpha.real),
+             float(alpha.imag), float(beta.real), float(beta.imag), nu,
+             int(settings.mg_coarse_steps), C.byref(h))
+        return _MgcHierarchy(h, (ms, ks, masks))
 
 
 class BlockFactorization:
