@@ -769,7 +769,21 @@ def _step_newton_semilinear(stepper, problem):
             pc = stepper._preconditioner(Splitting.AI, problem, Ks)
         rhs = R.clone()
         call("irk_axpby", ctx(), m * s, -1.0, ptr(R), 0.0, ptr(rhs))
-        res = fgmres_device(op, rhs, pc._dev_op() if pc is not None else None, stepper.krylov)
+        if isinstance(pc, _SurrogateBlockJacobi):
+            # batched block solves without a host round trip each; their
+            # iteration counts come back in one copy
+            pc.defer = True
+            try:
+                with _lib.deferred_solves() as log:
+                    res = fgmres_device(op, rhs, pc._dev_op(), stepper.krylov)
+            finally:
+                pc.defer = False
+            entries = iter(log.entries[:, 0].tolist())
+            pc.inner_iterations = [[next(entries, -1)] if v is None else v
+                                   for v in pc.inner_iterations]
+        else:
+            res = fgmres_device(op, rhs, pc._dev_op() if pc is not None else None,
+                                stepper.krylov)
         krylov_total += res.iterations
         if pc is not None:
             inner.extend(pc.inner_iterations)
@@ -800,6 +814,7 @@ class _SurrogateBlockJacobi:
         self.Md, self.Kd = Md.eliminated(mask), Kd.eliminated(mask)
         self.settings = settings
         self.inner_iterations = []
+        self.defer = False  # set around deferred_solves: no per-apply host sync
 
     def _dev_op(self):
         pc = self
@@ -822,10 +837,15 @@ class _SurrogateBlockJacobi:
         rel = np.zeros(8)
         al = np.ascontiguousarray(self.alpha + [0.0] * (8 - s))
         be = np.ascontiguousarray(self.beta + [0.0] * (8 - s))
+        defer = self.defer and not st.raise_on_maxit
         status = _lib.load().irk_pcg(ctx(), s, hptr(al), hptr(be), self.Md.handle, self.Kd.handle,
                                      ptr(self.shift), ptr(self.mask), ptr(R), s, ptr(X), s,
-                                     float(st.rtol), float(st.atol), int(st.maxit), hptr(its),
-                                     hptr(rel))
+                                     float(st.rtol), float(st.atol), int(st.maxit),
+                                     None if defer else hptr(its), None if defer else hptr(rel))
+        if defer:
+            _lib.check(status, "deferred surrogate block-Jacobi")
+            self.inner_iterations.append(None)
+            return X
         self.inner_iterations.append([int(v) for v in its[:s]])
         if status not in (_lib.IRK_OK, _lib.IRK_ENOCONV, _lib.IRK_ESINGULAR):
             _lib.check(status, "surrogate block-Jacobi")
