@@ -391,20 +391,6 @@ __device__ __forceinline__ void boundary_lines(int N, F&& f) {
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) f(0, 0);
 }
 
-// Region loops of the temporally blocked smoothers: f(local index, gx, gy)
-// over the (TX + 2h) x (TY + 2h) points of halo h of a tile whose shared
-// buffers have halo HX (row width WL); (ox, oy) = global coordinates of local
-// (0, 0).  h is a compile-time constant after unrolling.
-template <int TX, int TY, int HX, typename F>
-__device__ __forceinline__ void for_halo(int h, int ox, int oy, F&& f) {
-  constexpr int WL = TX + 2 * HX;
-  const int w = TX + 2 * h, hh = TY + 2 * h, lo = HX - h;
-  for (int k = threadIdx.x; k < w * hh; k += kBlock) {
-    const int i = lo + k % w, j = lo + k / w;
-    f(j * WL + i, ox + i, oy + j);
-  }
-}
-
 // One Chebyshev step on halo h of a tile (shared buffers of halo HX, row
 // width WL), register-blocked: thread t owns column t % w (w = TX + 2h) over
 // a segment of rows and slides a 3x3 window of x_k down it, so each point
