@@ -1006,6 +1006,17 @@ def _all_finite(x) -> bool:
     return bool(res.value)
 
 
+# diagnostics (env IRK_FGMRES_GAPS): CUDA events around the per-iteration
+# host read of the Hessenberg column; profiles/fgmres_gaps.py reads them
+_GAPS = [] if __import__("os").environ.get("IRK_FGMRES_GAPS") else None
+
+
+def _ev_rec():
+    e = _torch().cuda.Event(enable_timing=True)
+    e.record()
+    return e
+
+
 def fgmres_device(A: _DevOp, b, P: _DevOp | None = None, settings: KrylovSettings | None = None,
                   x0=None) -> FgmresResult:
     """Restarted flexible GMRES on device vectors (control flow of
@@ -1068,6 +1079,8 @@ def fgmres_device(A: _DevOp, b, P: _DevOp | None = None, settings: KrylovSetting
         j = -1
         for j in range(cycle):
             w = V[j + 1]
+            if _GAPS is not None and j > 0:
+                _GAPS.append(_ev_rec())  # first enqueue after the host read of h
             if left:
                 A.dev_apply(V[j], tmp)
                 P.dev_apply(tmp, w)
@@ -1081,6 +1094,8 @@ def fgmres_device(A: _DevOp, b, P: _DevOp | None = None, settings: KrylovSetting
             call("irk_multidot", ctx(), n, j + 1, ptr(V), n, ptr(w), ptr(hbuf))
             call("irk_orth_update", ctx(), n, j + 1, ptr(V), n, ptr(hbuf), ptr(w),
                  1 if st.reorth else 0)
+            if _GAPS is not None:
+                _GAPS.append(_ev_rec())  # GPU work of the iteration ends here
             hcol = hbuf[: j + 2].cpu().numpy()
             H[: j + 2, j] = hcol
             lucky = H[j + 1, j] < breakdown_tol
