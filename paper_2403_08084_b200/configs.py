@@ -28,7 +28,7 @@ DESCRIPTIONS = {
     4: "2D heat P1 2048x2048 (~4.2M DOFs), Alexander SDIRK, dt=1e-3, 50 steps, one reused "
        "stage operator, multigrid-PCG 1e-12",
     5: "Allen-Cahn eps=0.02 P1 1024x1024, Neumann, RadauIIA s=3, AI, dt=1e-3, 20 steps, "
-       "Newton atol 1e-10, GMRES 1e-10, block-Jacobi",
+       "Newton atol 1e-10, GMRES 1e-10, block-Jacobi (surrogate blocks, inner Jacobi-PCG 1e-2)",
 }
 
 SEEDS = {1: 0, 2: 1, 3: 2, 4: 3, 5: 4}
@@ -58,7 +58,16 @@ def initial_state(k: int, grid: pb.StructuredGrid) -> np.ndarray:
     return 0.1 * noise
 
 
-def build(k: int, n: int | None = None, inner_rtol: float = 1e-6, **block) -> Workload:
+# Inner block-solve tolerance where BASELINE.json leaves it open (configs 1,
+# 3, 5; config 2 fixes 1e-6, config 4 solves its stages to the Krylov rtol):
+# 1e-6 except config 5, whose block-Jacobi blocks are an SPD
+# surrogate of the Newton Jacobian (lumped reaction) anyway: there 1e-2
+# measured 47.6 vs 30.5 steps/s for 28.6 vs 26.2 FGMRES iterations per step
+# (profiles/inner_rtol_sweep.py); looser inner solves do not pay on 1 and 3.
+INNER_RTOL = {5: 1e-2}
+
+
+def build(k: int, n: int | None = None, inner_rtol: float | None = None, **block) -> Workload:
     dim, n0 = GRID[k]
     grid = pb.StructuredGrid(dim, n or n0)
     u0 = initial_state(k, grid)
@@ -75,6 +84,8 @@ def build(k: int, n: int | None = None, inner_rtol: float = 1e-6, **block) -> Wo
             5: StageFormulation.STAGE_DERIVATIVE_AI}[k]
     pc = {1: PreconditionerKind.BLOCK_DIAGONAL, 2: PreconditionerKind.BLOCK_LOWER,
           3: PreconditionerKind.SCHUR, 4: None, 5: PreconditionerKind.BLOCK_DIAGONAL}[k]
+    if inner_rtol is None:
+        inner_rtol = INNER_RTOL.get(k, 1e-6)
     kw = dict(formulation=form, krylov=KrylovSettings(rtol=1e-10 if k == 5 else 1e-12),
               pc_kind=pc, block_solver=BlockSolveSettings(rtol=inner_rtol, **block))
     if k == 5:
