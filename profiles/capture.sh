@@ -30,3 +30,10 @@ IRK_NO_GRAPH=1 ncu --set full --clock-control none \
     -k regex:"k_cg_spmv|k_cg_update|k_cg_skip|k_cg_dot_rz" -s 40 -c 8 \
     -o "$OUT/cg" python profiles/solve_probe.py 2 > "$OUT/ncu_cg.log" 2>&1
 echo done
+# config 3: complex multigrid-COCG kernels (Schur pairs) and the GS coupling of config 2
+IRK_NO_GRAPH=1 ncu --set full --clock-control none -k regex:"k_mgc_(cheb|residual|restrict|prolong)|k_cg_spmv_stn" \
+    -s 30 -c 12 -o "$OUT/mgc" python bench.py --config 3 --steps 1 --warmup 1 --no-cpu-baseline \
+    > "$OUT/ncu_mgc.log" 2>&1
+ncu --set full --clock-control none -k regex:"k_stage_couple" -s 6 -c 2 \
+    -o "$OUT/couple" python bench.py --steps 1 --warmup 1 --no-cpu-baseline > "$OUT/ncu_couple.log" 2>&1
+echo done2

@@ -27,6 +27,26 @@ RAW = {
 }
 
 
+PEAK = 6546.9  # GB/s, MEASURED_PEAKS.json copy bandwidth on this pool's B200s
+_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
+          "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0,
+          "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
+
+
+def achieved(hdr, units, r):
+    """(dram read + write bytes) / duration in GB/s, or None."""
+    try:
+        b = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = hdr.index(k)
+            b += float(r[i].replace(",", "")) * _SCALE[units[i]]
+        i = hdr.index("gpu__time_duration.sum")
+        t = float(r[i].replace(",", "")) * _SCALE[units[i]]
+        return b / t / 1e9 if t > 0 else None
+    except (ValueError, KeyError):
+        return None
+
+
 def raw_rows(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True)
     rows = list(csv.reader(io.StringIO(out.stdout)))
@@ -59,6 +79,10 @@ def main():
         stalls.sort(reverse=True)
         print(name[:90])
         print("   " + "  ".join(f"{k}={v}" for k, v in vals.items()))
+        bw = achieved(hdr, units, r)
+        if bw is not None:
+            print(f"   achieved DRAM {bw:.0f} GB/s = {bw / PEAK:.2f} of the measured "
+                  f"{PEAK:.0f} GB/s copy peak")
         if stalls:
             print("   stalls: " + ", ".join(f"{n}={v:.3g}" for v, n in stalls[:6]))
 
