@@ -490,7 +490,7 @@ struct SellRow {
 
 // out[r*ld] = R[r*s+i] - sum_c C[r,c] sum_{j in J} coef[j] X[c*s+j]  (masked);
 // J = the stages with a nonzero coefficient (jmask), gathered only those
-template <int S>
+template <int S, int W>
 __global__ void __launch_bounds__(kBlock)
     k_stage_couple(int64_t m, int i, const int* __restrict__ slice_ptr, int ellw,
                    const int* __restrict__ colhdr, const int* __restrict__ sell_col,
@@ -507,14 +507,35 @@ __global__ void __launch_bounds__(kBlock)
   }
   const SellRow sr(slice_ptr, ellw, r);
   double acc = 0.0;
-  for (int k = 0; k < sr.width; ++k) {
-    const int pos = sr.base + k * kSlice + sr.lane;
-    const int c = sell_col_at(colhdr, sell_col, sr.q0 + k, pos, r);
-    double w = 0.0;
+  if (W > 0) {
+    // ELL pattern of width W: every header, column and gather of the row is
+    // issued before the first use (one dependency level)
+    int cs[W > 0 ? W : 1];
+    double av[W > 0 ? W : 1];
 #pragma unroll
-    for (int j = 0; j < S; ++j)
-      if (jmask & (1u << j)) w += coef.q[j] * __ldg(X + (int64_t)c * S + j);
-    acc += sell_val_at(uval, cval, sr.q0 + k, pos) * w;
+    for (int k = 0; k < W; ++k) {
+      const int pos = sr.base + k * kSlice + sr.lane;
+      cs[k] = sell_col_at(colhdr, sell_col, sr.q0 + k, pos, r);
+      av[k] = sell_val_at(uval, cval, sr.q0 + k, pos);
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      double w = 0.0;
+#pragma unroll
+      for (int j = 0; j < S; ++j)
+        if (jmask & (1u << j)) w += coef.q[j] * __ldg(X + (int64_t)cs[k] * S + j);
+      acc += av[k] * w;
+    }
+  } else {
+    for (int k = 0; k < sr.width; ++k) {
+      const int pos = sr.base + k * kSlice + sr.lane;
+      const int c = sell_col_at(colhdr, sell_col, sr.q0 + k, pos, r);
+      double w = 0.0;
+#pragma unroll
+      for (int j = 0; j < S; ++j)
+        if (jmask & (1u << j)) w += coef.q[j] * __ldg(X + (int64_t)c * S + j);
+      acc += sell_val_at(uval, cval, sr.q0 + k, pos) * w;
+    }
   }
   out[r * ld_out] = rv - acc;
 }
@@ -951,9 +972,18 @@ int irk_stage_couple(irk_ctx* ctx, int s, int i, const double* coef_host, const 
     if (coef_host[j] != 0.0) jm |= 1u << j;
   const Pattern* P = C->pat;
   unsigned g = (unsigned)((m + kBlock - 1) / kBlock);
-  IRK_STAGE_SWITCH(s, (k_stage_couple<SS><<<g, kBlock, 0, ctx->stream>>>(
-                          m, i, P->slice_ptr, P->ellw, P->colhdr, P->sell_col, C->uval, C->val,
+#define IRK_CPL(WW)                                                                          \
+  IRK_STAGE_SWITCH(s, (k_stage_couple<SS, WW><<<g, kBlock, 0, ctx->stream>>>(                   \
+                          m, i, P->slice_ptr, P->ellw, P->colhdr, P->sell_col, C->uval, C->val, \
                           cf, jm, rowmask_dev, R_dev, X_dev, out_dev, ld_out)))
+  if (P->ellw == 7) {
+    IRK_CPL(7)
+  } else if (P->ellw == 15) {
+    IRK_CPL(15)
+  } else {
+    IRK_CPL(0)
+  }
+#undef IRK_CPL
   IRK_CHECK_LAUNCH(ctx);
   return IRK_OK;
 }
