@@ -353,6 +353,49 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// Init of a solve with an external preconditioner (one system): reads the
+// strided right-hand side directly (launched eagerly, so no staging copy),
+// x = 0, r = b, p_old = 0, bb = ||b||^2; the preconditioner forms z and
+// rho afterwards (rho = 0 here).  Last block initialises the state.
+template <typename T>
+__global__ void __launch_bounds__(kBlock)
+    k_cg_init_ext(int64_t m, const T* __restrict__ rhs, int64_t ld_rhs, T* __restrict__ x,
+                  T* __restrict__ r, T* __restrict__ pold, double rtol2, double atol2,
+                  SysState<T>* st, double* __restrict__ part, unsigned int* counter) {
+  IRK_PDL_ENTER();
+  double bb = 0.0;
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < m;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    const T b = rhs[row * ld_rhs];
+    x[row] = s_zero(T{});
+    r[row] = b;
+    pold[row] = s_zero(T{});
+    bb += s_abs2(b);
+  }
+  double bbs[1] = {bb};
+  block_reduce_store_d<1>(bbs, part);
+  if (last_block_inner(counter)) {
+    __shared__ double sbb[1];
+    reduce_partials<double, 1>(part, gridDim.x, sbb);
+    if (threadIdx.x == 0) {
+      const double tol2 = fmax(rtol2 * sbb[0], atol2);
+      st->rho[0] = s_zero(T{});
+      st->bb[0] = sbb[0];
+      st->rr[0] = sbb[0];
+      st->tol2[0] = tol2;
+      st->beta[0] = s_zero(T{});
+      st->alpha[0] = s_zero(T{});
+      st->its[0] = 0;
+      st->code[0] = 0;
+      const int act = (sbb[0] > tol2) ? 1 : 0;
+      st->active[0] = act;
+      st->done = act ? 0 : 1;
+      st->iter = 0;
+      st->fresh = 1;
+    }
+  }
+}
+
 // --------------------------------------------- tail-free iteration control
 // Iteration k is two kernels, A_k (SpMV + direction) and B_k (update), with
 // parity c = k & 1.  Neither kernel ends in a last-block reduction: each
@@ -1108,13 +1151,25 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   // arguments and replays as one cached graph.
   double* red = ctx->red;
   static const bool graph_off = getenv("IRK_NO_GRAPH") != nullptr;
-  launch(k_cg_stage_rhs<T, NB>, grid_for(ctx, m), kBlock, 0, s, m, rhs, ld_rhs, w.rb);
-  IRK_CHECK_LAUNCH(ctx);
-  auto init_body = [&](cudaStream_t cs) -> int {
-    launch(k_cg_init<T, NB, HASB>, G, kBlock, 0, cs, m, A, P, shift, mask, w.rb, NB, w.x, w.r, w.z,
-                                                 w.p0, w.dinv, rtol * rtol, atol * atol, st1,
-                                                 red + 2 * cg_part_doubles<T, NB>(G), cnt);
+  if constexpr (kExtOk) {
+    if (prec) {
+      // external preconditioner: the eager init reads the strided rhs itself
+      launch(k_cg_init_ext<T>, G, kBlock, 0, s, m, rhs, ld_rhs, w.x, w.r, w.p0, rtol * rtol,
+             atol * atol, st1, red + 2 * cg_part_doubles<T, NB>(G), cnt);
+      IRK_CHECK_LAUNCH(ctx);
+    }
+  }
+  if (!prec) {
+    launch(k_cg_stage_rhs<T, NB>, grid_for(ctx, m), kBlock, 0, s, m, rhs, ld_rhs, w.rb);
     IRK_CHECK_LAUNCH(ctx);
+  }
+  auto init_body = [&](cudaStream_t cs) -> int {
+    if (!prec) {
+      launch(k_cg_init<T, NB, HASB>, G, kBlock, 0, cs, m, A, P, shift, mask, w.rb, NB, w.x, w.r,
+             w.z, w.p0, w.dinv, rtol * rtol, atol * atol, st1,
+             red + 2 * cg_part_doubles<T, NB>(G), cnt);
+      IRK_CHECK_LAUNCH(ctx);
+    }
     if constexpr (kExtOk) {
       if (prec && n_ext) {
         // rho comes from the preconditioner's r.z partials (parity 1, read
