@@ -135,6 +135,10 @@ int irk_mat_rowsum(irk_ctx* ctx, const irk_mat* A, double* rowsum_dev);
 /* y = A x (k right-hand sides, interleaved: x[c*k + j]).  Replaces spmv
  * (sparsela.py:118-123). */
 int irk_spmv(irk_ctx* ctx, const irk_mat* A, int k, const double* x_dev, double* y_dev);
+/* y[r*ldy] = sum_c A[r,c] x[c*ldx], A dense row-major n x n on the device
+ * (the direct solve of small blocks: A = the precomputed block inverse). */
+int irk_dense_gemv(irk_ctx* ctx, int64_t n, const double* A_dev, const double* x_dev,
+                   int64_t ldx, double* y_dev, int64_t ldy);
 
 /* ------------------------------------------------------ stage operator (K2)
  * Out = (C1 (x) M + dt * C2 (x) K) Y on interleaved m-by-s blocks, computed

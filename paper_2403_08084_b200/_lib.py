@@ -89,6 +89,7 @@ _SIGS = {
     "irk_mg_destroy": [_vp],
     "irk_mg_vcycle": [_vp, _vp, _vp, _vp],
     "irk_mg_set_structured": [_vp, _int],
+    "irk_dense_gemv": [_vp, _i64, _vp, _vp, _i64, _vp, _i64],
     "irk_mgc_create": [_vp, _int, _int, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _dbl, _int, _int,
                        _vp],
     "irk_mgc_destroy": [_vp],
@@ -182,9 +183,7 @@ class _Context:
         self._stream = None
 
     def bind(self):
-        import torch
-
-        s = torch.cuda.current_stream(self.device).cuda_stream
+        s = _raw_stream(self.device)
         if s != self._stream:
             check(load().irk_ctx_set_stream(self.handle, _vp(s)), "irk_ctx_set_stream")
             self._stream = s
@@ -197,13 +196,30 @@ class _Context:
 _tls = threading.local()
 
 
-def device_index() -> int:
+_cuda_ok = False
+
+
+def _raw_stream(dev: int) -> int:
+    """torch's current stream on `dev` as an integer handle (the C++ fast
+    path; the Python wrapper costs microseconds per call on small problems)."""
     import torch
 
-    if not torch.cuda.is_available():
-        raise LibraryUnavailable(
-            "paper_2403_08084_b200 needs a CUDA device (sm_100a); there is no CPU fallback"
-        )
+    fast = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if fast is not None:
+        return int(fast(dev))
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def device_index() -> int:
+    global _cuda_ok
+    import torch
+
+    if not _cuda_ok:
+        if not torch.cuda.is_available():
+            raise LibraryUnavailable(
+                "paper_2403_08084_b200 needs a CUDA device (sm_100a); there is no CPU fallback"
+            )
+        _cuda_ok = True
     return torch.cuda.current_device()
 
 

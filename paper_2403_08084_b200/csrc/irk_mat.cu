@@ -1060,6 +1060,38 @@ int irk_mat_rowsum(irk_ctx* ctx, const irk_mat* A, double* rowsum_dev) {
   return IRK_OK;
 }
 
+}  // extern "C"
+
+namespace irk {
+// y[r * ldy] = sum_c A[r, c] x[c * ldx] (A dense row-major n x n): one warp
+// per row, lanes stride the row (coalesced), x from L1/L2
+__global__ void __launch_bounds__(kBlock)
+    k_dense_gemv(int64_t n, const double* __restrict__ A, const double* __restrict__ x,
+                 int64_t ldx, double* __restrict__ y, int64_t ldy) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (r >= n) return;
+  const double* a = A + r * n;
+  double acc = 0.0;
+  for (int64_t c = lane; c < n; c += 32) acc += __ldg(a + c) * __ldg(x + c * ldx);
+  acc = warp_sum(acc);
+  if (lane == 0) y[r * ldy] = acc;
+}
+}  // namespace irk
+
+extern "C" {
+
+int irk_dense_gemv(irk_ctx* ctx, int64_t n, const double* A_dev, const double* x_dev,
+                   int64_t ldx, double* y_dev, int64_t ldy) {
+  IRK_REQUIRE(ctx && A_dev && x_dev && y_dev, "irk_dense_gemv: NULL argument");
+  IRK_REQUIRE(n >= 0 && ldx >= 1 && ldy >= 1, "irk_dense_gemv: bad sizes");
+  if (n == 0) return IRK_OK;
+  const unsigned g = (unsigned)((n * 32 + kBlock - 1) / kBlock);
+  k_dense_gemv<<<g, kBlock, 0, ctx->stream>>>(n, A_dev, x_dev, ldx, y_dev, ldy);
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
 int irk_spmv(irk_ctx* ctx, const irk_mat* A, int k, const double* x_dev, double* y_dev) {
   IRK_REQUIRE(ctx && A && x_dev && y_dev, "irk_spmv: NULL argument");
   IRK_REQUIRE(k >= 1 && k <= 8, "irk_spmv: 1 <= k <= 8 right-hand sides");

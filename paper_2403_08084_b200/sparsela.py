@@ -546,12 +546,21 @@ def as_dev_op(obj, n):
 # -------------------------------------------------------- block solves
 
 
+# blocks of at most this many rows are solved directly (dense inverse):
+# below it the iterative solves are launch-latency-bound
+DIRECT_MAX = 2048
+
+
 @dataclass
 class BlockSolveSettings:
     """Inner diagonal-block solver (replaces SuperLU, sparsela.py:149-191).
 
-    method: "auto" (multigrid-preconditioned CG for blocks of P1 grid
-    operators, Jacobi-PCG otherwise), "mg" (multigrid required), "pcg"
+    method: "auto" (a direct solve for blocks of at most DIRECT_MAX rows,
+    multigrid-preconditioned CG for larger blocks of P1 grid operators,
+    Jacobi-PCG otherwise), "direct" (the block inverse, formed once on the
+    device, applied by one dense matrix-vector kernel: the exact solve of
+    the reference's SuperLU factorisation at sizes where the iterative
+    solvers are launch-latency-bound), "mg" (multigrid required), "pcg"
     (Jacobi-preconditioned CG) or "chebyshev" (Jacobi-Chebyshev,
     ``cheb_iters`` sweeps with Gershgorin/Lanczos-free bounds).
     mg_nu / mg_coarse_steps: Chebyshev smoothing steps per level (0: automatic
@@ -572,7 +581,7 @@ class BlockSolveSettings:
     mg_coarse_ratio: float = 0.5
 
     def __post_init__(self):
-        if self.method not in ("auto", "pcg", "mg", "chebyshev"):
+        if self.method not in ("auto", "pcg", "mg", "chebyshev", "direct"):
             raise ValueError(f"unknown block solver {self.method!r}")
         if self.rtol < 0 or self.atol < 0 or self.maxit < 0:
             raise ValueError("block solver tolerances must be non-negative")
@@ -759,12 +768,31 @@ class BlockFactorization:
         self.last_relres = 0.0
         self._check_regular()
         self._mg = None
-        if self.settings.method in ("auto", "mg"):
+        self._inv = None
+        meth = self.settings.method
+        if meth == "direct" or (meth == "auto" and 0 < self.n <= DIRECT_MAX):
+            self._inv = self._dense_inverse()
+        elif meth in ("auto", "mg"):
             self._mg = _MgHierarchy.build(M, K, self.alpha, self.beta, self.mask, B,
                                           self.settings)
             if self._mg is None and self.settings.method == "mg":
                 raise ValueError("multigrid block solver needs M, K from assemble_p1 "
                                  "(nested structured-grid P1 operators)")
+
+    def _dense_inverse(self):
+        """B^-1 as a dense row-major device array (one-time setup, cuSOLVER
+        through torch; the per-solve work is irk_dense_gemv)."""
+        torch = _torch()
+        if self.n > 8192:
+            raise ValueError(f"direct block solve limited to 8192 rows, got {self.n}")
+        dense = torch.from_numpy(self.matrix.to_dense()).to(device())
+        try:
+            inv = torch.linalg.inv(dense)
+        except RuntimeError as exc:  # torch.linalg.LinAlgError
+            raise FactorizationError(f"stage block is singular: {exc}") from exc
+        if not bool(torch.isfinite(inv).all()):
+            raise FactorizationError("stage block is singular (non-finite inverse)")
+        return inv.contiguous()
 
     def _check_regular(self):
         torch = _torch()
@@ -796,6 +824,11 @@ class BlockFactorization:
         one = np.ones(8)
         defer = defer and not st.raise_on_maxit
         its_p, rel_p = (None, None) if defer else (hptr(its), hptr(rel))
+        if self._inv is not None and st.method in ("auto", "direct"):
+            call("irk_dense_gemv", ctx(), self.n, ptr(self._inv), ptr(rhs), int(ld_rhs), ptr(x),
+                 int(ld_x))
+            self.last_iterations, self.last_relres = 1, 0.0
+            return 1  # exact: no log entry even when deferred
         if self._mg is not None and st.method in ("auto", "mg"):
             status = _lib.load().irk_mg_pcg(
                 ctx(), self._mg.handle, ptr(rhs), int(ld_rhs), ptr(x), int(ld_x),

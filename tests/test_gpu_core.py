@@ -334,9 +334,35 @@ def _p1_block(irk, dim, n, alpha, beta):
     from paper_2403_08084_b200 import sparsela as la
 
     M, K, bd = irk.assemble_p1(irk.StructuredGrid(dim, n))
-    st = la.BlockSolveSettings(rtol=1e-12, raise_on_maxit=True)
+    st = la.BlockSolveSettings(method="mg", rtol=1e-12, raise_on_maxit=True)
     fac = la.BlockFactorization(M, K, alpha, beta, bd, st)
     return M, K, bd, fac
+
+
+@pytest.mark.gpu
+def test_direct_small_blocks(cuda, irk, oracle):
+    """Blocks of at most DIRECT_MAX rows are solved exactly through the
+    device-resident inverse (one dense matrix-vector kernel): equal to a
+    sparse direct solve, one 'iteration', nothing logged when deferred."""
+    import scipy.sparse.linalg as spla
+
+    from paper_2403_08084_b200 import _lib
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(2, 32))
+    fac = la.BlockFactorization(M, K, 1.0, 5e-3, bd, la.BlockSolveSettings(rtol=1e-6))
+    assert fac._inv is not None and fac._mg is None
+    Mo, Ko = oracle.p1_matrices(2, 32)
+    B = oracle.dirichlet_identity((Mo + 5e-3 * Ko).tocsr(), bd)
+    rhs = np.random.default_rng(9).standard_normal(M.nrows)
+    x = fac.solve(rhs)
+    assert rel(x, spla.spsolve(B.tocsc(), rhs)) < 1e-12
+    assert fac.last_iterations == 1
+    rd, xd = la.to_dev(rhs), la.dev_empty(3 * M.nrows)
+    with _lib.deferred_solves() as log:
+        assert fac.dev_solve(rd, xd[1:], ld_x=3, defer=True) == 1
+    assert log.entries.shape[0] == 0
+    assert rel(la.to_host(xd).reshape(-1, 3)[:, 1], x) < 1e-14
 
 
 @pytest.mark.gpu
