@@ -29,11 +29,18 @@ ncu --set full --clock-control none --import-source on -k regex:"k_mg2_" -s 60 -
 IRK_NO_GRAPH=1 ncu --set full --clock-control none \
     -k regex:"k_cg_spmv|k_cg_update|k_cg_skip|k_cg_dot_rz" -s 40 -c 8 \
     -o "$OUT/cg" python profiles/solve_probe.py 2 > "$OUT/ncu_cg.log" 2>&1
-echo done
+
 # config 3: complex multigrid-COCG kernels (Schur pairs) and the GS coupling of config 2
 IRK_NO_GRAPH=1 ncu --set full --clock-control none -k regex:"k_mgc_(cheb|residual|restrict|prolong)|k_cg_spmv_stn" \
     -s 30 -c 12 -o "$OUT/mgc" python bench.py --config 3 --steps 1 --warmup 1 --no-cpu-baseline \
     > "$OUT/ncu_mgc.log" 2>&1
 ncu --set full --clock-control none -k regex:"k_stage_couple" -s 6 -c 2 \
     -o "$OUT/couple" python bench.py --steps 1 --warmup 1 --no-cpu-baseline > "$OUT/ncu_couple.log" 2>&1
-echo done2
+
+# summaries on the box (the .ncu-rep files exceed gpurun's 64 MiB copy-back)
+for r in stage_apply stage_apply_c3 mg2 cg mgc couple; do
+  [ -f "$OUT/$r.ncu-rep" ] && python profiles/ncu_summary.py "$OUT/$r.ncu-rep" > "$OUT/$r.txt" 2>&1
+done
+python profiles/ncu_launch_summary.py "$OUT/launches.csv" > "$OUT/launches_summary.txt" 2>&1
+rm -f "$OUT"/*.ncu-rep
+echo done3
