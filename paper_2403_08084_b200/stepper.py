@@ -337,7 +337,10 @@ class TimeStepper:
             # The reference solves DIRK stages with an exact factorisation (one
             # FGMRES iteration reaches round-off); Jacobi-PCG stops on its
             # recursive residual, so it is driven 1000x below the Krylov
-            # tolerance to keep the stage error at the exact solve's level.
+            # tolerance to keep the stage error at the exact solve's level
+            # (config 4, 50 steps, worst state vs the reference: 1.6e-11 here;
+            # 2.1e-10 at 100x for 7 % fewer iterations; 3.1e-9 at 1x,
+            # profiles/dirk_rtol_probe.py).
             st = self.dirk_solver or BlockSolveSettings(
                 rtol=self.krylov.rtol * 1e-3, atol=self.krylov.atol,
                 maxit=max(20000, 10 * problem.m), raise_on_maxit=True)
