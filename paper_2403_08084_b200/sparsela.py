@@ -814,15 +814,17 @@ class BlockFactorization:
         return self._matrix
 
     def dev_solve(self, rhs, x, ld_rhs=1, ld_x=1, nb=1, settings: BlockSolveSettings | None = None,
-                  defer: bool = False):
+                  defer: bool = False, checked: bool = False):
         """Solve on device data.  defer=True (inside _lib.deferred_solves, for
         preconditioner use that never raises): no host synchronisation, the
-        outcome goes to the context's solve log and None is returned."""
+        outcome goes to the context's solve log and None is returned.
+        checked=True defers even with raise_on_maxit: the caller reads the
+        log codes (1 cap, 2 breakdown) and raises."""
         st = settings or self.settings
         its = np.zeros(8, dtype=np.int32)
         rel = np.zeros(8, dtype=np.float64)
         one = np.ones(8)
-        defer = defer and not st.raise_on_maxit
+        defer = defer and (checked or not st.raise_on_maxit)
         its_p, rel_p = (None, None) if defer else (hptr(its), hptr(rel))
         if self._inv is not None and st.method in ("auto", "direct"):
             call("irk_dense_gemv", ctx(), self.n, ptr(self._inv), ptr(rhs), int(ld_rhs), ptr(x),

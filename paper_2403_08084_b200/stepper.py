@@ -40,6 +40,7 @@ from .bcs import (
 from .precond import PreconditionerKind, build_preconditioner
 from .sparsela import (
     BlockSolveSettings,
+    FactorizationError,
     KroneckerStageOperator,
     KrylovSettings,
     NonConvergenceError,
@@ -580,6 +581,50 @@ def _step_dirk_dev(stepper: TimeStepper, problem: SemidiscreteProblem):
     hist = []
     inner = []
     A = np.asarray(tab.A)
+    # linear stages: the stage solves run deferred (no host round trip per
+    # stage); their status is checked once after the loop, before commit
+    log = _lib.deferred_solves() if problem.is_linear else None
+    if log is not None:
+        log.__enter__()
+    try:
+        last = _dirk_stages(stepper, problem, tab, dt, t, u, svals, K_il, A, log, hist, inner)
+    finally:
+        if log is not None:
+            log.__exit__(None, None, None)
+    if log is not None:
+        for its, code, _, _ in log.entries.tolist():
+            if code == 1:
+                raise NonConvergenceError(
+                    f"DIRK stage solve: no convergence in {its} iterations", [])
+            if code == 2:
+                raise FactorizationError("DIRK stage solve: breakdown (singular stage block)")
+        done = iter(log.entries[:, 0].tolist())
+        inner = [next(done, -1) if v is None else v for v in inner]
+        krylov_total = int(sum(inner))
+        fac, srhs, ki = last
+        r = la.dev_empty(m)
+        fac._B.spmv(ki, r)
+        call("irk_axpby", ctx(), m, 1.0, ptr(srhs), -1.0, ptr(r))
+        final_res = la._norm(r)
+    else:
+        krylov_total, newton_total, final_res = last
+    u_next = la.dev_empty(m)
+    wb = np.ascontiguousarray(dt * np.asarray(tab.b))
+    call("irk_stage_update", ctx(), m, s, 1.0, ptr(u), hptr(wb), -1, ptr(K_il), ptr(u_next))
+    report = StepReport(newton_total, krylov_total, final_res, hist, inner)
+    stepper._commit(u_next)
+    return u_next, report
+
+
+def _dirk_stages(stepper, problem, tab, dt, t, u, svals, K_il, A, log, hist, inner):
+    """The stage loop of _step_dirk_dev.  Linear stages (log given): returns
+    (factor, constrained rhs, k) of the last stage; nonlinear: (krylov,
+    newton, final residual)."""
+    s, m = tab.s, problem.m
+    bc = problem.dirichlet
+    krylov_total = newton_total = 0
+    final_res = 0.0
+    last = None
     for i in range(s):
         ti = t + tab.c[i] * dt
         w = np.zeros(s)
@@ -598,10 +643,9 @@ def _step_dirk_dev(stepper: TimeStepper, problem: SemidiscreteProblem):
                 srhs = rhs
             fac = stepper._dirk_factor(A[i, i], problem)
             ki = la.dev_empty(m)
-            its = fac.dev_solve(srhs, ki)
-            krylov_total += its
+            its = fac.dev_solve(srhs, ki, defer=log is not None, checked=True)
             inner.append(its)
-            final_res = fac.last_relres * la._norm(srhs) if its else 0.0
+            last = (fac, srhs, ki)
         else:
             ki, nit, kit, h = _dirk_stage_newton_dev(stepper, problem, ti, acc, A[i, i],
                                                      svals[i] if svals is not None else None)
@@ -612,12 +656,7 @@ def _step_dirk_dev(stepper: TimeStepper, problem: SemidiscreteProblem):
         if svals is not None:
             scatter_stage_values(ki, bc.dofs_dev(), svals[i:i + 1], 1)
         call("irk_stage_set", ctx(), m, s, i, ptr(ki), ptr(K_il))
-    u_next = la.dev_empty(m)
-    wb = np.ascontiguousarray(dt * np.asarray(tab.b))
-    call("irk_stage_update", ctx(), m, s, 1.0, ptr(u), hptr(wb), -1, ptr(K_il), ptr(u_next))
-    report = StepReport(newton_total, krylov_total, final_res, hist, inner)
-    stepper._commit(u_next)
-    return u_next, report
+    return last if log is not None else (krylov_total, newton_total, final_res)
 
 
 def step_dirk(stepper: TimeStepper, problem: SemidiscreteProblem):
