@@ -263,6 +263,299 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Structured 3D path (P1 Kuhn-tetrahedra grid levels with the full-boundary
+// Dirichlet set, nu = 2): every level operator alpha M_l + beta K_l is ONE
+// 3x3x3 stencil (15 nonzero slots) on the interior, extracted from the
+// assembled level matrices and verified against every row at setup.  A
+// level is three matrix-free tile kernels with shared-memory halos (as the
+// 2D path of irk_mg.cu): pre (two Chebyshev steps from zero), residual +
+// restriction, prolongation + two post steps.  Tiles cover every grid point
+// (boundary points included: x = b there); the coarsest level stays on the
+// generic kernels.
+struct Sten3 {
+  cplx c[27];  // c[(dz+1)*9 + (dy+1)*3 + dx+1]
+  cplx dinv;
+  unsigned nz;  // bit k: c[k] != 0
+};
+
+__device__ __forceinline__ bool interior3(int x, int y, int z, int N) {
+  return x >= 1 && x < N && y >= 1 && y < N && z >= 1 && z < N;
+}
+
+// sum_k c_k s[i + off_k] over the nonzero slots (region row width W, plane WH)
+__device__ __forceinline__ cplx sten3_apply(const Sten3& S, const cplx* s, int i, int W, int WH) {
+  cplx acc = {0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < 27; ++k) {
+    if (!((S.nz >> k) & 1u)) continue;
+    const int dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
+    acc = s_add(acc, s_mul(S.c[k], s[i + dz * WH + dy * W + dx]));
+  }
+  return acc;
+}
+
+// region [ox, ox+W) x [oy, oy+H) x [oz, oz+D) of a grid vector into shared
+// memory, zero outside the interior
+__device__ __forceinline__ void load3(cplx* dst, const cplx* __restrict__ src, int n1, int ox,
+                                      int oy, int oz, int W, int H, int D) {
+  const int N = n1 - 1;
+  for (int k = threadIdx.x; k < W * H * D; k += blockDim.x) {
+    const int x = ox + k % W, y = oy + (k / W) % H, z = oz + k / (W * H);
+    dst[k] = interior3(x, y, z, N) ? ldv(src + ((int64_t)z * n1 + y) * n1 + x) : cplx{0.0, 0.0};
+  }
+}
+
+struct Cheb2c {
+  double cr0, cd1, cr1;
+};
+
+// x2 = two Chebyshev steps from zero (boundary points: x2 = b)
+template <int TX, int TY, int TZ>
+__global__ void __launch_bounds__(kBlock)
+    k_mg3_pre(int n1, Sten3 S, Cheb2c C, const cplx* __restrict__ b, cplx* __restrict__ x2,
+              const int* stop) {
+  IRK_PDL_ENTER();
+  if (stop && *stop) return;
+  constexpr int W = TX + 2, H = TY + 2, D = TZ + 2;
+  __shared__ cplx sb[W * H * D];
+  const int N = n1 - 1;
+  const int x0 = TX * blockIdx.x, y0 = TY * blockIdx.y, z0 = TZ * blockIdx.z;
+  load3(sb, b, n1, x0 - 1, y0 - 1, z0 - 1, W, H, D);
+  __syncthreads();
+  const cplx s0 = s_mul(s_real<cplx>(C.cr0), S.dinv);
+  const cplx k1 = s_mul(s_real<cplx>(1.0 + C.cd1), s0);
+  const cplx k2 = s_mul(s_real<cplx>(C.cr1), S.dinv);
+  for (int k = threadIdx.x; k < TX * TY * TZ; k += blockDim.x) {
+    const int lx = k % TX, ly = (k / TX) % TY, lz = k / (TX * TY);
+    const int x = x0 + lx, y = y0 + ly, z = z0 + lz;
+    if (x > N || y > N || z > N) continue;
+    const int64_t g = ((int64_t)z * n1 + y) * n1 + x;
+    if (!interior3(x, y, z, N)) {
+      x2[g] = ldv(b + g);
+      continue;
+    }
+    const int i = ((lz + 1) * H + ly + 1) * W + lx + 1;
+    const cplx bi = sb[i];
+    const cplx ax1 = s_mul(s0, sten3_apply(S, sb, i, W, W * H));
+    x2[g] = s_add(s_mul(k1, bi), s_mul(k2, s_sub(bi, ax1)));
+  }
+}
+
+// b_c = P^T (b - A x2) on the coarse tile (fine boundary: r = 0; coarse
+// boundary rows 0); P^T weights 1 at 2c and 1/2 at 2c +- p for the seven
+// Kuhn edge directions p in {0,1}^3 \ 0
+template <int CX, int CY, int CZ>
+__global__ void __launch_bounds__(kBlock)
+    k_mg3_restrict(int n1f, int n1c, Sten3 S, const cplx* __restrict__ bf,
+                   const cplx* __restrict__ x2, cplx* __restrict__ bc, const int* stop) {
+  IRK_PDL_ENTER();
+  if (stop && *stop) return;
+  constexpr int RW = 2 * CX + 1, RH = 2 * CY + 1, RD = 2 * CZ + 1;
+  constexpr int XW = RW + 2, XH = RH + 2, XD = RD + 2;
+  __shared__ cplx sx[XW * XH * XD];
+  __shared__ cplx sr[RW * RH * RD];
+  const int Nf = n1f - 1, Nc = n1c - 1;
+  const int cx0 = CX * blockIdx.x, cy0 = CY * blockIdx.y, cz0 = CZ * blockIdx.z;
+  const int rx0 = 2 * cx0 - 1, ry0 = 2 * cy0 - 1, rz0 = 2 * cz0 - 1;
+  load3(sx, x2, n1f, rx0 - 1, ry0 - 1, rz0 - 1, XW, XH, XD);
+  __syncthreads();
+  for (int k = threadIdx.x; k < RW * RH * RD; k += blockDim.x) {
+    const int lx = k % RW, ly = (k / RW) % RH, lz = k / (RW * RH);
+    const int x = rx0 + lx, y = ry0 + ly, z = rz0 + lz;
+    cplx r = {0.0, 0.0};
+    if (interior3(x, y, z, Nf)) {
+      const int64_t g = ((int64_t)z * n1f + y) * n1f + x;
+      r = s_sub(ldv(bf + g),
+                sten3_apply(S, sx, ((lz + 1) * XH + ly + 1) * XW + lx + 1, XW, XW * XH));
+    }
+    sr[k] = r;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < CX * CY * CZ; k += blockDim.x) {
+    const int cx = cx0 + k % CX, cy = cy0 + (k / CX) % CY, cz = cz0 + k / (CX * CY);
+    if (cx > Nc || cy > Nc || cz > Nc) continue;
+    cplx v = {0.0, 0.0};
+    if (interior3(cx, cy, cz, Nc)) {
+      const int i = ((2 * cz - rz0) * RH + (2 * cy - ry0)) * RW + (2 * cx - rx0);
+      v = sr[i];
+      cplx h = {0.0, 0.0};
+#pragma unroll
+      for (int p = 1; p < 8; ++p) {
+        const int o = (p >> 2) * RW * RH + ((p >> 1) & 1) * RW + (p & 1);
+        h = s_add(h, s_add(sr[i + o], sr[i - o]));
+      }
+      v = s_add(v, s_mul(s_real<cplx>(0.5), h));
+    }
+    bc[((int64_t)cz * n1c + cy) * n1c + cx] = v;
+  }
+}
+
+// z = two Chebyshev steps from x_p = x2 + P e_c (boundary points z = b):
+// x_p on the tile + halo 2, x_a on halo 1
+template <int TX, int TY, int TZ>
+__global__ void __launch_bounds__(kBlock)
+    k_mg3_post(int n1, int n1c, Sten3 S, Cheb2c C, const cplx* __restrict__ b,
+               const cplx* __restrict__ x2, const cplx* __restrict__ ec,
+               cplx* __restrict__ z, const int* stop) {
+  IRK_PDL_ENTER();
+  if (stop && *stop) return;
+  constexpr int PW = TX + 4, PH = TY + 4, PD = TZ + 4;
+  constexpr int AW = TX + 2, AH = TY + 2, AD = TZ + 2;
+  __shared__ cplx sp[PW * PH * PD];
+  __shared__ cplx sa[AW * AH * AD];
+  __shared__ cplx sb[AW * AH * AD];
+  const int N = n1 - 1;
+  const int x0 = TX * blockIdx.x, y0 = TY * blockIdx.y, z0 = TZ * blockIdx.z;
+  const int px = x0 - 2, py = y0 - 2, pz = z0 - 2;
+  for (int k = threadIdx.x; k < PW * PH * PD; k += blockDim.x) {
+    const int x = px + k % PW, y = py + (k / PW) % PH, zz = pz + k / (PW * PH);
+    cplx v = {0.0, 0.0};
+    if (interior3(x, y, zz, N)) {
+      const int64_t c = ((int64_t)(zz >> 1) * n1c + (y >> 1)) * n1c + (x >> 1);
+      const cplx e0 = ldv(ec + c);
+      const int odd = (x & 1) | (y & 1) | (zz & 1);
+      cplx e = e0;
+      if (odd) {
+        const int64_t c2 = c + ((int64_t)(zz & 1) * n1c + (y & 1)) * n1c + (x & 1);
+        e = s_mul(s_real<cplx>(0.5), s_add(e0, ldv(ec + c2)));
+      }
+      v = s_add(ldv(x2 + ((int64_t)zz * n1 + y) * n1 + x), e);
+    }
+    sp[k] = v;
+  }
+  load3(sb, b, n1, x0 - 1, y0 - 1, z0 - 1, AW, AH, AD);
+  __syncthreads();
+  const cplx s0 = s_mul(s_real<cplx>(C.cr0), S.dinv);
+  for (int k = threadIdx.x; k < AW * AH * AD; k += blockDim.x) {
+    const int lx = k % AW, ly = (k / AW) % AH, lz = k / (AW * AH);
+    const int x = x0 - 1 + lx, y = y0 - 1 + ly, zz = z0 - 1 + lz;
+    cplx v = {0.0, 0.0};
+    if (interior3(x, y, zz, N)) {
+      const int i = ((lz + 1) * PH + ly + 1) * PW + lx + 1;
+      v = s_add(sp[i], s_mul(s0, s_sub(sb[k], sten3_apply(S, sp, i, PW, PW * PH))));
+    }
+    sa[k] = v;
+  }
+  __syncthreads();
+  const cplx cd1 = s_real<cplx>(C.cd1), k2 = s_mul(s_real<cplx>(C.cr1), S.dinv);
+  for (int k = threadIdx.x; k < TX * TY * TZ; k += blockDim.x) {
+    const int lx = k % TX, ly = (k / TX) % TY, lz = k / (TX * TY);
+    const int x = x0 + lx, y = y0 + ly, zz = z0 + lz;
+    if (x > N || y > N || zz > N) continue;
+    const int64_t g = ((int64_t)zz * n1 + y) * n1 + x;
+    if (!interior3(x, y, zz, N)) {
+      z[g] = ldv(b + g);
+      continue;
+    }
+    const int ia = ((lz + 1) * AH + ly + 1) * AW + lx + 1;
+    const int ip = ((lz + 2) * PH + ly + 2) * PW + lx + 2;
+    const cplx xa = sa[ia];
+    z[g] = s_add(s_add(xa, s_mul(cd1, s_sub(xa, sp[ip]))),
+                 s_mul(k2, s_sub(sb[ia], sten3_apply(S, sa, ia, AW, AW * AH))));
+  }
+}
+
+// 3x3x3 stencil of `row` of a real matrix (out[27]); err = 1 for entries
+// outside the box
+__global__ void k_mg3_row_stencil(MatView A, bool useb, int64_t row, int n1, double* out,
+                                  int* err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int k = 0; k < 27; ++k) out[k] = 0.0;
+  const int64_t sl = row / kSlice;
+  const int lane = (int)(row % kSlice);
+  int base, width;
+  if (A.ellw) {
+    base = (int)(sl * kSlice * A.ellw);
+    width = A.ellw;
+  } else {
+    base = A.slice_ptr[sl];
+    width = (A.slice_ptr[sl + 1] - base) / kSlice;
+  }
+  const int q0 = base / kSlice;
+  for (int k = 0; k < width; ++k) {
+    const int pos = base + k * kSlice + lane;
+    const int c = sell_col_at(A.colhdr, A.sell_col, q0 + k, pos, row);
+    const double v = useb ? sell_val_at(A.ub, A.b, q0 + k, pos) : sell_val_at(A.ua, A.a, q0 + k, pos);
+    const int64_t d = (int64_t)c - row;
+    int hit = -1;
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx)
+          if (d == dx + (int64_t)n1 * (dy + (int64_t)n1 * dz)) hit = (dz + 1) * 9 + (dy + 1) * 3 + dx + 1;
+    if (hit >= 0)
+      out[hit] += v;
+    else if (v != 0.0)
+      err[0] = 1;
+  }
+}
+
+// max over rows of |(A v) - (S v)| and |A v| for v_i = sin(0.37 i + 0.11)
+// (A = M or K by useb; S the real stencil cs; masked rows identity)
+__global__ void __launch_bounds__(kBlock)
+    k_mg3_verify(MatView A, bool useb, int n1, const double* __restrict__ cs,
+                 const uint8_t* __restrict__ mask, double* part) {
+  const int N = n1 - 1;
+  const int64_t m = (int64_t)n1 * n1 * n1;
+  double emax = 0.0, amax = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % n1), y = (int)((i / n1) % n1), z = (int)(i / ((int64_t)n1 * n1));
+    const bool in = interior3(x, y, z, N);
+    if (in == (mask[i] != 0)) {
+      emax = INFINITY;
+      continue;
+    }
+    if (!in) continue;  // masked rows: identity in the kernels, zero in M, K
+    const int64_t sl = i / kSlice;
+    const int lane = (int)(i % kSlice);
+    int base, width;
+    if (A.ellw) {
+      base = (int)(sl * kSlice * A.ellw);
+      width = A.ellw;
+    } else {
+      base = __ldg(A.slice_ptr + sl);
+      width = (__ldg(A.slice_ptr + sl + 1) - base) / kSlice;
+    }
+    const int q0 = base / kSlice;
+    double av = 0.0;
+    for (int k = 0; k < width; ++k) {
+      const int pos = base + k * kSlice + lane;
+      const int c = sell_col_at(A.colhdr, A.sell_col, q0 + k, pos, i);
+      const double a = useb ? sell_val_at(A.ub, A.b, q0 + k, pos) : sell_val_at(A.ua, A.a, q0 + k, pos);
+      av += a * sin(0.37 * c + 0.11);
+    }
+    double sv = 0.0;
+    for (int k = 0; k < 27; ++k) {
+      const int dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
+      if (interior3(x + dx, y + dy, z + dz, N))
+        sv += cs[k] * sin(0.37 * (((int64_t)(z + dz) * n1 + y + dy) * n1 + x + dx) + 0.11);
+    }
+    emax = fmax(emax, fabs(av - sv));
+    amax = fmax(amax, fabs(av));
+  }
+  __shared__ double re[kBlock / 32], ra[kBlock / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  }
+  if (lane == 0) {
+    re[warp] = emax;
+    ra[warp] = amax;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double e = 0.0, a = 0.0;
+    for (int w = 0; w < kBlock / 32; ++w) {
+      e = fmax(e, re[w]);
+      a = fmax(a, ra[w]);
+    }
+    part[2 * blockIdx.x] = e;
+    part[2 * blockIdx.x + 1] = a;
+  }
+}
+
 struct McLevel {
   int64_t m = 0;
   GridC g{};
@@ -285,9 +578,119 @@ std::atomic<uint64_t> g_mgc_uid{1ull << 40};
 struct irk_mgc : public irk::CgPrec {
   int nu = 2, ncoarse = 4;
   int maxw = 0;  // widest row of the level-0 pattern (CG kernel dispatch)
+  int dim = 0;
   irk::cplx al{}, be{};
   std::vector<irk::McLevel> lev;
   void* mem = nullptr;
+  // structured 3D path (k_mg3_*): levels 0..nlev-2 as stencil tile kernels
+  bool s3_on = false;
+  std::vector<irk::Sten3> s3;
+  std::vector<irk::Cheb2c> c3;
+
+  int setup_s3(irk_ctx* ctx) {
+    using namespace irk;
+    static const bool off = getenv("IRK_MG_GENERIC") != nullptr;
+    s3_on = false;
+    const int nl = (int)lev.size();
+    if (off || dim != 3 || nu != 2 || nl < 2) return IRK_OK;
+    for (const McLevel& L : lev)
+      if (!L.mask || L.g.n1 - 1 < 4 || L.g.n1 > 1290) return IRK_OK;
+    const int G = ctx->num_sms * 4;
+    IRK_TRY(ensure_red(ctx, 2 * (size_t)G + 64));
+    s3.assign(nl, Sten3{});
+    c3.assign(nl, Cheb2c{});
+    double* dst = nullptr;
+    IRK_CUDA(cudaMalloc(&dst, 2 * 27 * sizeof(double)));
+    int* err = (int*)ctx->counters + (kNumCounters - 2);
+    int rc = IRK_OK;
+    for (int l = 0; l + 1 < nl && rc == IRK_OK; ++l) {
+      const McLevel& L = lev[l];
+      const int n1 = (int)L.g.n1, N = n1 - 1;
+      const int64_t row = ((int64_t)(N / 2) * n1 + N / 2) * n1 + N / 2;
+      double cs[2][27];
+      bool ok = true;
+      for (int which = 0; which < 2 && ok; ++which) {
+        cudaMemsetAsync(err, 0, sizeof(int), ctx->stream);
+        k_mg3_row_stencil<<<1, 32, 0, ctx->stream>>>(L.A, which == 1, row, n1, dst + 27 * which,
+                                                      err);
+        int herr = 0;
+        cudaMemcpyAsync(cs[which], dst + 27 * which, 27 * sizeof(double), cudaMemcpyDeviceToHost,
+                        ctx->stream);
+        cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+        if (cudaStreamSynchronize(ctx->stream) != cudaSuccess || herr) {
+          ok = false;
+          break;
+        }
+        k_mg3_verify<<<G, kBlock, 0, ctx->stream>>>(L.A, which == 1, n1, dst + 27 * which,
+                                                     L.mask, ctx->red);
+        std::vector<double> part(2 * G);
+        cudaMemcpyAsync(part.data(), ctx->red, part.size() * sizeof(double),
+                        cudaMemcpyDeviceToHost, ctx->stream);
+        if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+          ok = false;
+          break;
+        }
+        double e = 0.0, a = 0.0;
+        for (int b = 0; b < G; ++b) {
+          e = std::fmax(e, part[2 * b]);
+          a = std::fmax(a, part[2 * b + 1]);
+        }
+        if (!(e <= 1e-12 * a)) ok = false;
+      }
+      if (!ok) {
+        rc = -1;
+        break;
+      }
+      Sten3& S = s3[l];
+      S.nz = 0;
+      for (int k = 0; k < 27; ++k) {
+        S.c[k] = {al.re * cs[0][k] + be.re * cs[1][k], al.im * cs[0][k] + be.im * cs[1][k]};
+        if (S.c[k].re != 0.0 || S.c[k].im != 0.0) S.nz |= 1u << k;
+      }
+      if (S.c[13].re == 0.0 && S.c[13].im == 0.0) {
+        rc = -1;
+        break;
+      }
+      const double dd = S.c[13].re * S.c[13].re + S.c[13].im * S.c[13].im;
+      S.dinv = {S.c[13].re / dd, -S.c[13].im / dd};
+      std::vector<double> cd, cr;
+      cheb(0.25 * L.lmax, L.lmax, 2, cd, cr);
+      c3[l] = Cheb2c{cr[0], cd[1], cr[1]};
+    }
+    cudaFree(dst);
+    cudaGetLastError();
+    s3_on = rc == IRK_OK;
+    return IRK_OK;
+  }
+
+  // structured 3D V-cycle on level l (l < nlev-1); the result lands in out
+  int vcycle3(irk_ctx* ctx, cudaStream_t s, int l, const irk::cplx* b, irk::cplx* out,
+              const int* stop) {
+    using namespace irk;
+    McLevel& L = lev[l];
+    McLevel& Cc = lev[l + 1];
+    const int n1 = (int)L.g.n1, n1c = (int)Cc.g.n1;
+    const dim3 gt((n1 + 15) / 16, (n1 + 3) / 4, (n1 + 3) / 4);
+    const dim3 gr((n1c + 3) / 4, (n1c + 3) / 4, (n1c + 3) / 4);
+    launch(k_mg3_pre<16, 4, 4>, gt, kBlock, 0, s, n1, s3[l], c3[l], b, L.x[0], stop);
+    launch(k_mg3_restrict<4, 4, 4>, gr, kBlock, 0, s, n1, n1c, s3[l], b, (const cplx*)L.x[0],
+           Cc.b, stop);
+    ctx->launches += 2;
+    if (cudaPeekAtLastError() != cudaSuccess) return IRK_ECUDA;
+    cplx* ec;
+    if (l + 2 == (int)lev.size()) {
+      int res;
+      IRK_TRY(smooth(ctx, s, l + 1, Cc.b, -1, ncoarse, 0.05, Cc.r, stop, &res));
+      ec = Cc.r;
+    } else {
+      IRK_TRY(vcycle3(ctx, s, l + 1, Cc.b, Cc.x[1], stop));
+      ec = Cc.x[1];
+    }
+    launch(k_mg3_post<16, 4, 4>, gt, kBlock, 0, s, n1, n1c, s3[l], c3[l], b,
+           (const cplx*)L.x[0], (const cplx*)ec, out, stop);
+    ctx->launches++;
+    return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
+  }
 
   static void cheb(double lo, double hi, int n, std::vector<double>& cd, std::vector<double>& cr) {
     const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
@@ -380,6 +783,15 @@ struct irk_mgc : public irk::CgPrec {
   }
 
   int apply(irk_ctx* ctx, cudaStream_t s, const double* r, double* z, const int* stop) override {
+    if (s3_on) {
+      const int e = vcycle3(ctx, s, 0, reinterpret_cast<const irk::cplx*>(r),
+                            reinterpret_cast<irk::cplx*>(z), stop);
+      if (e != IRK_OK || cudaGetLastError() != cudaSuccess) {
+        irk::set_error("irk_mgc: structured V-cycle launch failed");
+        return IRK_ECUDA;
+      }
+      return IRK_OK;
+    }
     int c;
     const int e = vcycle(ctx, s, 0, reinterpret_cast<const irk::cplx*>(r),
                          reinterpret_cast<irk::cplx*>(z), stop, &c);
@@ -413,6 +825,7 @@ int irk_mgc_create(irk_ctx* ctx, int dim, int nlev, const int64_t* N_host,
   mg->nu = nu;
   mg->ncoarse = ncoarse;
   mg->al = {alpha_re, alpha_im};
+  mg->dim = dim;
   mg->maxw = M_levels[0] ? M_levels[0]->pat->maxw : 0;
   mg->be = {beta_re, beta_im};
   size_t total = 0;  // complex elements
@@ -484,6 +897,7 @@ int irk_mgc_create(irk_ctx* ctx, int dim, int nlev, const int64_t* N_host,
     }
     L.lmax = mx;
   }
+  IRK_TRY(mg->setup_s3(ctx));
   *out = mg;
   return IRK_OK;
 }
