@@ -283,12 +283,27 @@ __device__ __forceinline__ bool interior3(int x, int y, int z, int N) {
   return x >= 1 && x < N && y >= 1 && y < N && z >= 1 && z < N;
 }
 
-// sum_k c_k s[i + off_k] over the nonzero slots (region row width W, plane WH)
+// The 15 slots of the Kuhn-split P1 stencil: the centre and +-p for the
+// seven 0/1 directions p (every one an edge of the triangulation)
+constexpr unsigned kuhn_mask() {
+  unsigned m = 0;
+  for (int k = 0; k < 27; ++k) {
+    const int dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
+    const bool pos = dx >= 0 && dy >= 0 && dz >= 0, neg = dx <= 0 && dy <= 0 && dz <= 0;
+    if (pos || neg) m |= 1u << k;
+  }
+  return m;
+}
+constexpr unsigned kKuhnNZ = kuhn_mask();
+
+// sum_k c_k s[i + off_k] over the nonzero slots (region row width W, plane
+// WH); KUHN: the slot set is kKuhnNZ, resolved at compile time
+template <bool KUHN>
 __device__ __forceinline__ cplx sten3_apply(const Sten3& S, const cplx* s, int i, int W, int WH) {
   cplx acc = {0.0, 0.0};
 #pragma unroll
   for (int k = 0; k < 27; ++k) {
-    if (!((S.nz >> k) & 1u)) continue;
+    if (KUHN ? !((kKuhnNZ >> k) & 1u) : !((S.nz >> k) & 1u)) continue;
     const int dx = k % 3 - 1, dy = (k / 3) % 3 - 1, dz = k / 9 - 1;
     acc = s_add(acc, s_mul(S.c[k], s[i + dz * WH + dy * W + dx]));
   }
@@ -311,7 +326,7 @@ struct Cheb2c {
 };
 
 // x2 = two Chebyshev steps from zero (boundary points: x2 = b)
-template <int TX, int TY, int TZ>
+template <int TX, int TY, int TZ, bool KUHN>
 __global__ void __launch_bounds__(kBlock)
     k_mg3_pre(int n1, Sten3 S, Cheb2c C, const cplx* __restrict__ b, cplx* __restrict__ x2,
               const int* stop) {
@@ -337,7 +352,7 @@ __global__ void __launch_bounds__(kBlock)
     }
     const int i = ((lz + 1) * H + ly + 1) * W + lx + 1;
     const cplx bi = sb[i];
-    const cplx ax1 = s_mul(s0, sten3_apply(S, sb, i, W, W * H));
+    const cplx ax1 = s_mul(s0, sten3_apply<KUHN>(S, sb, i, W, W * H));
     x2[g] = s_add(s_mul(k1, bi), s_mul(k2, s_sub(bi, ax1)));
   }
 }
@@ -345,7 +360,7 @@ __global__ void __launch_bounds__(kBlock)
 // b_c = P^T (b - A x2) on the coarse tile (fine boundary: r = 0; coarse
 // boundary rows 0); P^T weights 1 at 2c and 1/2 at 2c +- p for the seven
 // Kuhn edge directions p in {0,1}^3 \ 0
-template <int CX, int CY, int CZ>
+template <int CX, int CY, int CZ, bool KUHN>
 __global__ void __launch_bounds__(kBlock)
     k_mg3_restrict(int n1f, int n1c, Sten3 S, const cplx* __restrict__ bf,
                    const cplx* __restrict__ x2, cplx* __restrict__ bc, const int* stop) {
@@ -367,7 +382,7 @@ __global__ void __launch_bounds__(kBlock)
     if (interior3(x, y, z, Nf)) {
       const int64_t g = ((int64_t)z * n1f + y) * n1f + x;
       r = s_sub(ldv(bf + g),
-                sten3_apply(S, sx, ((lz + 1) * XH + ly + 1) * XW + lx + 1, XW, XW * XH));
+                sten3_apply<KUHN>(S, sx, ((lz + 1) * XH + ly + 1) * XW + lx + 1, XW, XW * XH));
     }
     sr[k] = r;
   }
@@ -393,7 +408,7 @@ __global__ void __launch_bounds__(kBlock)
 
 // z = two Chebyshev steps from x_p = x2 + P e_c (boundary points z = b):
 // x_p on the tile + halo 2, x_a on halo 1
-template <int TX, int TY, int TZ>
+template <int TX, int TY, int TZ, bool KUHN>
 __global__ void __launch_bounds__(kBlock)
     k_mg3_post(int n1, int n1c, Sten3 S, Cheb2c C, const cplx* __restrict__ b,
                const cplx* __restrict__ x2, const cplx* __restrict__ ec,
@@ -433,7 +448,7 @@ __global__ void __launch_bounds__(kBlock)
     cplx v = {0.0, 0.0};
     if (interior3(x, y, zz, N)) {
       const int i = ((lz + 1) * PH + ly + 1) * PW + lx + 1;
-      v = s_add(sp[i], s_mul(s0, s_sub(sb[k], sten3_apply(S, sp, i, PW, PW * PH))));
+      v = s_add(sp[i], s_mul(s0, s_sub(sb[k], sten3_apply<KUHN>(S, sp, i, PW, PW * PH))));
     }
     sa[k] = v;
   }
@@ -452,7 +467,7 @@ __global__ void __launch_bounds__(kBlock)
     const int ip = ((lz + 2) * PH + ly + 2) * PW + lx + 2;
     const cplx xa = sa[ia];
     z[g] = s_add(s_add(xa, s_mul(cd1, s_sub(xa, sp[ip]))),
-                 s_mul(k2, s_sub(sb[ia], sten3_apply(S, sa, ia, AW, AW * AH))));
+                 s_mul(k2, s_sub(sb[ia], sten3_apply<KUHN>(S, sa, ia, AW, AW * AH))));
   }
 }
 
@@ -672,9 +687,16 @@ struct irk_mgc : public irk::CgPrec {
     const int n1 = (int)L.g.n1, n1c = (int)Cc.g.n1;
     const dim3 gt((n1 + 15) / 16, (n1 + 3) / 4, (n1 + 3) / 4);
     const dim3 gr((n1c + 3) / 4, (n1c + 3) / 4, (n1c + 3) / 4);
-    launch(k_mg3_pre<16, 4, 4>, gt, kBlock, 0, s, n1, s3[l], c3[l], b, L.x[0], stop);
-    launch(k_mg3_restrict<4, 4, 4>, gr, kBlock, 0, s, n1, n1c, s3[l], b, (const cplx*)L.x[0],
-           Cc.b, stop);
+    const bool kuhn = s3[l].nz == kKuhnNZ;
+    if (kuhn) {
+      launch(k_mg3_pre<16, 4, 4, true>, gt, kBlock, 0, s, n1, s3[l], c3[l], b, L.x[0], stop);
+      launch(k_mg3_restrict<4, 4, 4, true>, gr, kBlock, 0, s, n1, n1c, s3[l], b,
+             (const cplx*)L.x[0], Cc.b, stop);
+    } else {
+      launch(k_mg3_pre<16, 4, 4, false>, gt, kBlock, 0, s, n1, s3[l], c3[l], b, L.x[0], stop);
+      launch(k_mg3_restrict<4, 4, 4, false>, gr, kBlock, 0, s, n1, n1c, s3[l], b,
+             (const cplx*)L.x[0], Cc.b, stop);
+    }
     ctx->launches += 2;
     if (cudaPeekAtLastError() != cudaSuccess) return IRK_ECUDA;
     cplx* ec;
@@ -686,8 +708,12 @@ struct irk_mgc : public irk::CgPrec {
       IRK_TRY(vcycle3(ctx, s, l + 1, Cc.b, Cc.x[1], stop));
       ec = Cc.x[1];
     }
-    launch(k_mg3_post<16, 4, 4>, gt, kBlock, 0, s, n1, n1c, s3[l], c3[l], b,
-           (const cplx*)L.x[0], (const cplx*)ec, out, stop);
+    if (kuhn)
+      launch(k_mg3_post<16, 4, 4, true>, gt, kBlock, 0, s, n1, n1c, s3[l], c3[l], b,
+             (const cplx*)L.x[0], (const cplx*)ec, out, stop);
+    else
+      launch(k_mg3_post<16, 4, 4, false>, gt, kBlock, 0, s, n1, n1c, s3[l], c3[l], b,
+             (const cplx*)L.x[0], (const cplx*)ec, out, stop);
     ctx->launches++;
     return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
   }

@@ -31,7 +31,7 @@ IRK_NO_GRAPH=1 ncu --set full --clock-control none \
     -o "$OUT/cg" python profiles/solve_probe.py 2 > "$OUT/ncu_cg.log" 2>&1
 
 # config 3: complex multigrid-COCG kernels (Schur pairs) and the GS coupling of config 2
-IRK_NO_GRAPH=1 ncu --set full --clock-control none -k regex:"k_mgc_(cheb|residual|restrict|prolong)|k_cg_spmv_stn" \
+IRK_NO_GRAPH=1 ncu --set full --clock-control none -k regex:"k_mg3_|k_mgc_cheb|k_cg_spmv_stn" \
     -s 30 -c 12 -o "$OUT/mgc" python bench.py --config 3 --steps 1 --warmup 1 --no-cpu-baseline \
     > "$OUT/ncu_mgc.log" 2>&1
 ncu --set full --clock-control none -k regex:"k_stage_couple" -s 6 -c 2 \
