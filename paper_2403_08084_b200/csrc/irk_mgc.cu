@@ -333,7 +333,8 @@ __global__ void __launch_bounds__(kBlock)
   IRK_PDL_ENTER();
   if (stop && *stop) return;
   constexpr int W = TX + 2, H = TY + 2, D = TZ + 2;
-  __shared__ cplx sb[W * H * D];
+  extern __shared__ cplx dyn3[];
+  cplx* sb = dyn3;  // W * H * D
   const int N = n1 - 1;
   const int x0 = TX * blockIdx.x, y0 = TY * blockIdx.y, z0 = TZ * blockIdx.z;
   load3(sb, b, n1, x0 - 1, y0 - 1, z0 - 1, W, H, D);
@@ -368,8 +369,9 @@ __global__ void __launch_bounds__(kBlock)
   if (stop && *stop) return;
   constexpr int RW = 2 * CX + 1, RH = 2 * CY + 1, RD = 2 * CZ + 1;
   constexpr int XW = RW + 2, XH = RH + 2, XD = RD + 2;
-  __shared__ cplx sx[XW * XH * XD];
-  __shared__ cplx sr[RW * RH * RD];
+  extern __shared__ cplx dyn3[];
+  cplx* sx = dyn3;                // XW * XH * XD
+  cplx* sr = dyn3 + XW * XH * XD;  // RW * RH * RD
   const int Nf = n1f - 1, Nc = n1c - 1;
   const int cx0 = CX * blockIdx.x, cy0 = CY * blockIdx.y, cz0 = CZ * blockIdx.z;
   const int rx0 = 2 * cx0 - 1, ry0 = 2 * cy0 - 1, rz0 = 2 * cz0 - 1;
@@ -417,9 +419,10 @@ __global__ void __launch_bounds__(kBlock)
   if (stop && *stop) return;
   constexpr int PW = TX + 4, PH = TY + 4, PD = TZ + 4;
   constexpr int AW = TX + 2, AH = TY + 2, AD = TZ + 2;
-  __shared__ cplx sp[PW * PH * PD];
-  __shared__ cplx sa[AW * AH * AD];
-  __shared__ cplx sb[AW * AH * AD];
+  extern __shared__ cplx dyn3[];
+  cplx* sp = dyn3;                             // PW * PH * PD
+  cplx* sa = sp + PW * PH * PD;                // AW * AH * AD
+  cplx* sb = sa + AW * AH * AD;                // AW * AH * AD
   const int N = n1 - 1;
   const int x0 = TX * blockIdx.x, y0 = TY * blockIdx.y, z0 = TZ * blockIdx.z;
   const int px = x0 - 2, py = y0 - 2, pz = z0 - 2;
@@ -674,7 +677,36 @@ struct irk_mgc : public irk::CgPrec {
     }
     cudaFree(dst);
     cudaGetLastError();
-    s3_on = rc == IRK_OK;
+    s3_on = rc == IRK_OK && set_smem_attrs() == IRK_OK;
+    cudaGetLastError();
+    return IRK_OK;
+  }
+
+  // 3D tiles: pre/post TX x TY x TZ fine points, restriction CX x CY x CZ
+  // coarse points (dynamic shared memory; sizes below)
+  static constexpr int TX3 = 16, TY3 = 4, TZ3 = 4, CX3 = 8, CY3 = 4, CZ3 = 4;  // 16x8x8, 16x8x4: no better
+  static constexpr size_t kPreSmem = (size_t)(TX3 + 2) * (TY3 + 2) * (TZ3 + 2) * 16;
+  static constexpr size_t kResSmem =
+      ((size_t)(2 * CX3 + 3) * (2 * CY3 + 3) * (2 * CZ3 + 3) +
+       (size_t)(2 * CX3 + 1) * (2 * CY3 + 1) * (2 * CZ3 + 1)) * 16;
+  static constexpr size_t kPostSmem =
+      ((size_t)(TX3 + 4) * (TY3 + 4) * (TZ3 + 4) + 2 * (size_t)(TX3 + 2) * (TY3 + 2) * (TZ3 + 2)) *
+      16;
+
+  static int set_smem_attrs() {
+    using namespace irk;
+    for (const void* fn : {(const void*)k_mg3_pre<TX3, TY3, TZ3, true>,
+                           (const void*)k_mg3_pre<TX3, TY3, TZ3, false>})
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPreSmem))
+        return IRK_ECUDA;
+    for (const void* fn : {(const void*)k_mg3_restrict<CX3, CY3, CZ3, true>,
+                           (const void*)k_mg3_restrict<CX3, CY3, CZ3, false>})
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kResSmem))
+        return IRK_ECUDA;
+    for (const void* fn : {(const void*)k_mg3_post<TX3, TY3, TZ3, true>,
+                           (const void*)k_mg3_post<TX3, TY3, TZ3, false>})
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPostSmem))
+        return IRK_ECUDA;
     return IRK_OK;
   }
 
@@ -685,16 +717,18 @@ struct irk_mgc : public irk::CgPrec {
     McLevel& L = lev[l];
     McLevel& Cc = lev[l + 1];
     const int n1 = (int)L.g.n1, n1c = (int)Cc.g.n1;
-    const dim3 gt((n1 + 15) / 16, (n1 + 3) / 4, (n1 + 3) / 4);
-    const dim3 gr((n1c + 3) / 4, (n1c + 3) / 4, (n1c + 3) / 4);
+    const dim3 gt((n1 + TX3 - 1) / TX3, (n1 + TY3 - 1) / TY3, (n1 + TZ3 - 1) / TZ3);
+    const dim3 gr((n1c + CX3 - 1) / CX3, (n1c + CY3 - 1) / CY3, (n1c + CZ3 - 1) / CZ3);
     const bool kuhn = s3[l].nz == kKuhnNZ;
     if (kuhn) {
-      launch(k_mg3_pre<16, 4, 4, true>, gt, kBlock, 0, s, n1, s3[l], c3[l], b, L.x[0], stop);
-      launch(k_mg3_restrict<4, 4, 4, true>, gr, kBlock, 0, s, n1, n1c, s3[l], b,
+      launch(k_mg3_pre<TX3, TY3, TZ3, true>, gt, kBlock, kPreSmem, s, n1, s3[l], c3[l], b,
+             L.x[0], stop);
+      launch(k_mg3_restrict<CX3, CY3, CZ3, true>, gr, kBlock, kResSmem, s, n1, n1c, s3[l], b,
              (const cplx*)L.x[0], Cc.b, stop);
     } else {
-      launch(k_mg3_pre<16, 4, 4, false>, gt, kBlock, 0, s, n1, s3[l], c3[l], b, L.x[0], stop);
-      launch(k_mg3_restrict<4, 4, 4, false>, gr, kBlock, 0, s, n1, n1c, s3[l], b,
+      launch(k_mg3_pre<TX3, TY3, TZ3, false>, gt, kBlock, kPreSmem, s, n1, s3[l], c3[l], b,
+             L.x[0], stop);
+      launch(k_mg3_restrict<CX3, CY3, CZ3, false>, gr, kBlock, kResSmem, s, n1, n1c, s3[l], b,
              (const cplx*)L.x[0], Cc.b, stop);
     }
     ctx->launches += 2;
@@ -709,11 +743,11 @@ struct irk_mgc : public irk::CgPrec {
       ec = Cc.x[1];
     }
     if (kuhn)
-      launch(k_mg3_post<16, 4, 4, true>, gt, kBlock, 0, s, n1, n1c, s3[l], c3[l], b,
-             (const cplx*)L.x[0], (const cplx*)ec, out, stop);
+      launch(k_mg3_post<TX3, TY3, TZ3, true>, gt, kBlock, kPostSmem, s, n1, n1c, s3[l], c3[l],
+             b, (const cplx*)L.x[0], (const cplx*)ec, out, stop);
     else
-      launch(k_mg3_post<16, 4, 4, false>, gt, kBlock, 0, s, n1, n1c, s3[l], c3[l], b,
-             (const cplx*)L.x[0], (const cplx*)ec, out, stop);
+      launch(k_mg3_post<TX3, TY3, TZ3, false>, gt, kBlock, kPostSmem, s, n1, n1c, s3[l], c3[l],
+             b, (const cplx*)L.x[0], (const cplx*)ec, out, stop);
     ctx->launches++;
     return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
   }
