@@ -796,7 +796,12 @@ def _step_newton_semilinear(stepper, problem):
             #   M + dt a_ii kscale K + diag(dt a_ii * rowsum(M) * D_i)
             if lumped is None:
                 lumped = Md.rowsum()
-            shift = la.dev_empty(m * s)
+            # one persistent buffer: its address is part of the cached CUDA
+            # graphs' keys (a fresh allocation per Newton iteration re-captured
+            # them whenever the allocator handed out a new address)
+            shift = getattr(stepper, "_shift_buf", None)
+            if shift is None or shift.numel() != m * s:
+                shift = stepper._shift_buf = la.dev_empty(m * s)
             wdiag = np.ascontiguousarray(dt * np.diag(A))
             call("irk_stage_scale", ctx(), m, s, hptr(wdiag), ptr(lumped), ptr(D), ptr(shift))
             pc = _SurrogateBlockJacobi(problem, tab, dt, form.kscale, shift, Md, Kd, mask,
