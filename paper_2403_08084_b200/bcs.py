@@ -63,6 +63,17 @@ class DirichletBC:
         return mk
 
 
+_INV_CACHE: dict = {}
+
+
+def _tableau_inverse(tab):
+    key = id(tab)
+    hit = _INV_CACHE.get(key)
+    if hit is None or hit[0] is not tab:
+        hit = _INV_CACHE[key] = (tab, np.linalg.inv(np.asarray(tab.A, dtype=np.float64)))
+    return hit[1]
+
+
 def _values_at(fn, t, shape):
     return np.broadcast_to(np.asarray(fn(t), dtype=np.float64), shape)
 
@@ -97,7 +108,9 @@ def stage_bc_values(method: BcMethod, tab, bc: DirichletBC, u_n, t: float, dt: f
             raise ValueError(
                 "DAE boundary conditions on stage derivatives need an invertible "
                 f"tableau, got {tab.name!r}")
-        return np.linalg.solve(tab.A, W)
+        # A^-1 W with the s x s inverse formed once per tableau (a many-rhs
+        # LAPACK solve over |Gamma| columns costs ~1 ms per step at config 3)
+        return _tableau_inverse(tab) @ W
     if bc.g_dot is None:
         raise ValueError("ODE boundary conditions require g_dot")
     Gd = np.stack([_values_at(bc.g_dot, ti, shape) for ti in stage_t])
@@ -142,17 +155,27 @@ class ConstrainedStageOperator:
         return la._like_input(out, v)
 
 
-def scatter_stage_values(X_il, dofs_dev, svals: np.ndarray, s: int):
-    """X[dof*s + i] = svals[i, k] on an interleaved device block."""
-    sv = la.to_dev(np.ascontiguousarray(svals, dtype=np.float64).reshape(-1))
+def stage_values_dev(svals):
+    """The (s, |Gamma|) stage values as one flat device array (upload once,
+    scatter several times)."""
+    if la.is_torch(svals) and svals.device.type == "cuda":
+        return svals.reshape(-1)
+    return la.to_dev(np.ascontiguousarray(svals, dtype=np.float64).reshape(-1))
+
+
+def scatter_stage_values(X_il, dofs_dev, svals, s: int):
+    """X[dof*s + i] = svals[i, k] on an interleaved device block (svals:
+    numpy, or the device array of stage_values_dev)."""
+    sv = stage_values_dev(svals)
     call("irk_bc_scatter", ctx(), s, int(dofs_dev.numel()), ptr(dofs_dev), ptr(sv), ptr(X_il))
 
 
-def constrain_stage_system_dev(op, rhs_il, bc: DirichletBC, svals: np.ndarray):
+def constrain_stage_system_dev(op, rhs_il, bc: DirichletBC, svals):
     """Device form of constrain_stage_system on interleaved data:
     srhs = rhs - op(g_ext); srhs[Gamma] = g_ext[Gamma] (bcs.py:137-142)."""
     s, m = op.s, op.m
     dofs = bc.dofs_dev()
+    svals = stage_values_dev(svals)
     g_ext = la.dev_zeros(m * s)
     scatter_stage_values(g_ext, dofs, svals, s)
     lifted = la.dev_empty(m * s)

@@ -35,6 +35,7 @@ from .bcs import (
     StageUnknown,
     constrain_stage_system_dev,
     scatter_stage_values,
+    stage_values_dev,
     stage_bc_values,
 )
 from .precond import PreconditionerKind, build_preconditioner
@@ -465,8 +466,9 @@ def _solve_constrained_dev(stepper, problem, op, rhs_il, unknown, t):
     bc = problem.dirichlet
     svals = None
     if bc is not None and len(bc.dofs):
-        svals = stage_bc_values(stepper.bc_method, stepper.tableau, bc, stepper._u_dev, t,
-                                stepper.dt, unknown)
+        svals = stage_values_dev(stage_bc_values(stepper.bc_method, stepper.tableau, bc,
+                                                 stepper._u_dev, t, stepper.dt, unknown)
+                                 ).reshape(op.s, -1)
         sop, srhs = constrain_stage_system_dev(op, rhs_il, bc, svals)
         A = sop._dev_op()
     else:

@@ -32,7 +32,7 @@ def main():
     pr.disable()
     print(f"{(time.perf_counter() - t0) / steps * 1e3:.2f} ms/step wall (profiled)")
     s = io.StringIO()
-    st_ = pstats.Stats(pr, stream=s); st_.sort_stats("cumtime").print_stats(40)
+    st_ = pstats.Stats(pr, stream=s); st_.sort_stats(sys.argv[3] if len(sys.argv) > 3 else "cumtime").print_stats(40)
     print(s.getvalue())
 
 
