@@ -259,7 +259,9 @@ def run_ours(args, world, rank, local):
     barrier(world)
     # the e2e arm below replays exactly these timed steps (same states, same
     # solver work): snapshot the stepper state
-    snap = (st.u_device.clone(), st.step_index, st._t_base)
+    # (a host copy: a device clone here occupied a cached allocator block
+    # the first timed step then had to cudaMalloc afresh, 2-7x slower)
+    snap = (st.u.copy(), st.step_index, st._t_base)
     reps = []
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
