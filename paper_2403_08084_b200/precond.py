@@ -137,6 +137,27 @@ class StagePreconditioner:
             self._mats = la.shared_pattern([self.M.device()] + [K.device() for K in self.Ks])
         return self._mats
 
+    def _sweep_plan(self):
+        """(block order, per-block coupling coefficients or None) of the
+        sequential sweep, built once."""
+        plan = getattr(self, "_sweep", None)
+        if plan is None:
+            s, kind = self.s, self.kind
+            if kind is PreconditionerKind.BLOCK_DIAGONAL:
+                order, deps = list(range(s)), (lambda i: ())
+            elif kind in _LOWER_KINDS:
+                order, deps = list(range(s)), (lambda i: range(i))
+            else:
+                order, deps = list(range(s - 1, -1, -1)), (lambda i: range(i + 1, s))
+            coefs = []
+            for i in range(s):
+                coef = np.zeros(s)
+                for j in deps(i):
+                    coef[j] = self._coef[i, j]
+                coefs.append(np.ascontiguousarray(coef) if np.any(coef != 0.0) else None)
+            plan = self._sweep = (order, coefs)
+        return plan
+
     def _mg_blocks(self) -> bool:
         """Blocks are solved one by one when each has a multigrid hierarchy
         (P1 grid operators, no diagonal shift: ~5 instead of O(100) batched
@@ -195,22 +216,16 @@ class StagePreconditioner:
             a, b = self._block_coefs()
             self._pcg(s, a, b, Md, Ks[0], self._shift, R, s, X, s)
             return X
-        # sequential Gauss-Seidel sweep (precond.py:97-117)
-        X.zero_()
-        if kind is PreconditionerKind.BLOCK_DIAGONAL:
-            order, deps = range(s), (lambda i: ())
-        elif kind in _LOWER_KINDS:
-            order, deps = range(s), (lambda i: range(i))
-        else:
-            order, deps = range(s - 1, -1, -1), (lambda i: range(i + 1, s))
+        # sequential Gauss-Seidel sweep (precond.py:97-117); every block
+        # solve writes its whole stage column of X before a later block reads
+        # it, so X needs no zeroing
+        order, coefs = self._sweep_plan()
         tmp = la.dev_empty(m)
         for i in order:
-            coef = np.zeros(s)
-            for j in deps(i):
-                coef[j] = self._coef[i, j]
-            if np.any(coef != 0.0):
+            coef = coefs[i]
+            if coef is not None:
                 C_ = Md if self.form is Splitting.IA else (Ks[0] if len(Ks) == 1 else Ks[i])
-                call("irk_stage_couple", ctx(), s, i, hptr(np.ascontiguousarray(coef)), C_.handle,
+                call("irk_stage_couple", ctx(), s, i, hptr(coef), C_.handle,
                      ptr(self.mask()), ptr(R), ptr(X), ptr(tmp), 1)
             else:
                 call("irk_stage_get", ctx(), m, s, i, ptr(R), ptr(tmp))

@@ -821,16 +821,16 @@ class BlockFactorization:
         checked=True defers even with raise_on_maxit: the caller reads the
         log codes (1 cap, 2 breakdown) and raises."""
         st = settings or self.settings
-        its = np.zeros(8, dtype=np.int32)
-        rel = np.zeros(8, dtype=np.float64)
-        one = np.ones(8)
-        defer = defer and (checked or not st.raise_on_maxit)
-        its_p, rel_p = (None, None) if defer else (hptr(its), hptr(rel))
         if self._inv is not None and st.method in ("auto", "direct"):
             call("irk_dense_gemv", ctx(), self.n, ptr(self._inv), ptr(rhs), int(ld_rhs), ptr(x),
                  int(ld_x))
             self.last_iterations, self.last_relres = 1, 0.0
             return 1  # exact: no log entry even when deferred
+        its = np.zeros(8, dtype=np.int32)
+        rel = np.zeros(8, dtype=np.float64)
+        one = np.ones(8)
+        defer = defer and (checked or not st.raise_on_maxit)
+        its_p, rel_p = (None, None) if defer else (hptr(its), hptr(rel))
         if self._mg is not None and st.method in ("auto", "mg"):
             status = _lib.load().irk_mg_pcg(
                 ctx(), self._mg.handle, ptr(rhs), int(ld_rhs), ptr(x), int(ld_x),
