@@ -364,6 +364,12 @@ int irk_mgc_create(irk_ctx* ctx, int dim, int nlev, const int64_t* N_host,
                    const uint8_t* const* masks, double alpha_re, double alpha_im, double beta_re,
                    double beta_im, int nu, int ncoarse, irk_mgc** out);
 int irk_mgc_destroy(irk_mgc* mg);
+/* Structured 3D path (matrix-free Kuhn-stencil tile kernels, chosen at
+ * create time for 3D levels with the full-boundary Dirichlet set and nu = 2;
+ * env IRK_MG_GENERIC disables it): switch it on (IRK_EINVAL when unavailable)
+ * or off, and query the hierarchy. */
+int irk_mgc_set_structured(irk_mgc* mg, int on);
+int irk_mgc_info(const irk_mgc* mg, int* nlev, int* structured);
 /* COCG on the level-0 block preconditioned by one complex V-cycle per
  * iteration; rhs/x interleaved complex (re, im) with leading dimensions in
  * doubles (even), 16-byte aligned; status and deferred logging as irk_pcg. */

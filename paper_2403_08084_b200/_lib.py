@@ -93,6 +93,8 @@ _SIGS = {
     "irk_mgc_create": [_vp, _int, _int, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _dbl, _int, _int,
                        _vp],
     "irk_mgc_destroy": [_vp],
+    "irk_mgc_set_structured": [_vp, _int],
+    "irk_mgc_info": [_vp, _vp, _vp],
     "irk_mgc_cocg": [_vp, _vp, _vp, _i64, _vp, _i64, _dbl, _dbl, _int, _vp, _vp],
     "irk_mg_info": [_vp, _vp, _vp],
     "irk_mg_pcg": [_vp, _vp, _vp, _i64, _vp, _i64, _dbl, _dbl, _int, _vp, _vp],

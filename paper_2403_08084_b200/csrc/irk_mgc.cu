@@ -601,7 +601,7 @@ struct irk_mgc : public irk::CgPrec {
   std::vector<irk::McLevel> lev;
   void* mem = nullptr;
   // structured 3D path (k_mg3_*): levels 0..nlev-2 as stencil tile kernels
-  bool s3_on = false;
+  bool s3_on = false, s3_ok = false;
   std::vector<irk::Sten3> s3;
   std::vector<irk::Cheb2c> c3;
 
@@ -677,7 +677,7 @@ struct irk_mgc : public irk::CgPrec {
     }
     cudaFree(dst);
     cudaGetLastError();
-    s3_on = rc == IRK_OK && set_smem_attrs() == IRK_OK;
+    s3_ok = s3_on = rc == IRK_OK && set_smem_attrs() == IRK_OK;
     cudaGetLastError();
     return IRK_OK;
   }
@@ -959,6 +959,25 @@ int irk_mgc_create(irk_ctx* ctx, int dim, int nlev, const int64_t* N_host,
   }
   IRK_TRY(mg->setup_s3(ctx));
   *out = mg;
+  return IRK_OK;
+}
+
+int irk_mgc_set_structured(irk_mgc* mg, int on) {
+  IRK_REQUIRE(mg, "irk_mgc_set_structured: NULL argument");
+  IRK_REQUIRE(!on || mg->s3_ok,
+              "irk_mgc_set_structured: no structured path for this hierarchy (needs 3D levels "
+              "with the full-boundary Dirichlet set and nu = 2)");
+  if ((on != 0) != mg->s3_on) {
+    mg->s3_on = on != 0;
+    mg->uid = g_mgc_uid.fetch_add(1);  // cached graphs hold the other kernel sequence
+  }
+  return IRK_OK;
+}
+
+int irk_mgc_info(const irk_mgc* mg, int* nlev, int* structured) {
+  IRK_REQUIRE(mg, "irk_mgc_info: NULL argument");
+  if (nlev) *nlev = (int)mg->lev.size();
+  if (structured) *structured = mg->s3_on ? 1 : 0;
   return IRK_OK;
 }
 

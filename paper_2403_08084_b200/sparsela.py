@@ -690,6 +690,17 @@ class _MgcHierarchy:
     def levels(self):
         return len(self._keep[0])
 
+    @property
+    def structured(self) -> bool:
+        """True when the V-cycle runs the matrix-free 3D stencil kernels."""
+        on = C.c_int()
+        call("irk_mgc_info", self.handle, None, C.byref(on))
+        return bool(on.value)
+
+    @structured.setter
+    def structured(self, on: bool):
+        call("irk_mgc_set_structured", self.handle, int(bool(on)))
+
     @staticmethod
     def build(M, K, Md, Kd, alpha: complex, beta: complex, mask, settings):
         """M, K: the SparseMatrix pair (grid-tagged); Md, Kd: their device

@@ -518,6 +518,18 @@ def test_mgc_cocg_schur_pair(cuda, irk, oracle, dim, n):
                               _lib.hptr(itj), _lib.hptr(relj))
     assert st == 0
     assert its[0] * 2 < itj[0], (its[0], itj[0])
+    if dim == 3:
+        # the structured 3D kernels (k_mg3_*) and the generic ones give the
+        # same preconditioner: same iterations, same solution
+        assert h.structured
+        h.structured = False
+        xg = la.dev_zeros(2 * m)
+        itg = np.zeros(1, dtype=np.int32)
+        st = _lib.load().irk_mgc_cocg(_lib.ctx(), h.handle, _lib.ptr(b), 2, _lib.ptr(xg), 2,
+                                      1e-10, 0.0, 500, _lib.hptr(itg), _lib.hptr(rel_))
+        h.structured = True
+        assert st == 0 and itg[0] == its[0]
+        assert float((xg - x).norm()) <= 1e-9 * float(x.norm())
 
 
 @pytest.mark.gpu
