@@ -28,12 +28,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "RadauIIA-3 heat 1M-DOF time steps/s; stage-operator apply HBM GB/s vs peak"
 UNIT = "steps/s"
-
-# FGMRES iterations per time step of the CPU port (Jacobi-PCG 1e-6 inner
-# blocks) at full size, used to scale the bounded CPU sample to steps/s.
-# Config 2 values measured with oracle/irk_oracle.py (block="pcg"); see
-# profiles/cpu_port_iterations.json.
-CPU_ITS_PER_STEP = {1: 15.7, 2: 11.0, 3: 4.0, 4: 3.0, 5: 20.0}
+L2_BYTES = 126 * 2**20
 
 
 def peaks():
@@ -189,25 +184,40 @@ def stage_apply_roofline(wl, reps=40):
     return t, algo, dict(s=s, m=m, nnz=nnz)
 
 
-def inner_solve_profile(wl, reps=20):
+def inner_solve_profile(wl, peak, reps=20):
     """The step's dominant cost: one inner block solve of the first
-    preconditioner block (multigrid-preconditioned CG to the workload's
-    inner tolerance), timed with CUDA events over `reps` solves."""
+    preconditioner block (the DIRK stage block for config 4) to the
+    workload's inner tolerance, timed with CUDA events over `reps` solves of
+    a seeded right-hand side.  Newton workloads (config 5) solve batched
+    surrogate blocks inside the Newton loop instead: None there.
+
+    Algorithmic bytes per CG iteration:
+      Jacobi-PCG:      nnz*12 + (m+1)*4 + 96*m   (SpMV with CSR values and
+                       columns, the update's vectors)
+      multigrid-PCG on the structured 2D path (matrix-free levels, stencil
+      SpMV on slot-uniform values): 80*m for the CG vectors (SpMV reads z,
+      p_old, writes p_new, q: 32 B; update reads p, q, x, r, writes x, r:
+      48 B) + per V-cycle level 62*m_l (pre 16, restriction 20, post 26) and
+      16*m_L on the single-CTA coarsest level."""
     import torch
 
     from paper_2403_08084_b200 import sparsela as la
     from paper_2403_08084_b200.stepper import _SPLIT
 
     st, prob = wl.stepper, wl.problem
+    if not prob.is_linear:
+        return None
     if st.formulation.name == "DIRK":
         fac = st._dirk_factor(st.tableau.A[0, 0], prob)
-        sett = getattr(st, "dirk_solver", None) or fac.settings
+        sett = fac.settings
     else:
         pc = st._preconditioner(_SPLIT[st.formulation], prob)
         if pc is None or pc.kind.name == "SCHUR":
             return None
         fac = pc.block_factors[0]
         sett = pc.settings
+    if fac.direct:
+        return None
     m = prob.m
     b = la.to_dev(np.random.default_rng(1).standard_normal(m))
     x = la.dev_empty(m)
@@ -221,10 +231,32 @@ def inner_solve_profile(wl, reps=20):
     e1.record(stream)
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / 1e3 / reps
+    per_it = t / max(its / reps, 1)
     mg = getattr(fac, "_mg", None)
-    return t, dict(m=m, iterations_per_solve=its / reps, rtol=sett.rtol,
-                   method="multigrid-PCG" if mg is not None else "Jacobi-PCG",
-                   mg_levels=mg.levels if mg is not None else 0)
+    nnz = prob.mass.nnz
+    if mg is not None and mg.structured:
+        dim, N = prob.mass._p1_grid
+        ms = [((N >> l) + 1) ** dim for l in range(mg.levels)]
+        b_it = 80 * m + sum(62 * v for v in ms[:-1]) + 16 * ms[-1]
+        kind = "multigrid-PCG (structured 2D V-cycle)"
+    elif mg is not None:
+        b_it = None
+        kind = "multigrid-PCG (generic V-cycle)"
+    else:
+        b_it = nnz * 12 + (m + 1) * 4 + 96 * m
+        kind = "Jacobi-PCG"
+    out = dict(m=m, iterations_per_solve=its / reps, rtol=sett.rtol, method=kind,
+               mg_levels=mg.levels if mg is not None else 0, us_per_solve=t * 1e6,
+               us_per_iteration=per_it * 1e6)
+    if b_it is not None:
+        out["roofline"] = {
+            "bound": "hbm", "algorithmic_bytes_per_iteration": int(b_it),
+            "achieved": b_it / per_it / 1e9, "peak": peak, "unit": "GB/s",
+            "frac": b_it / per_it / 1e9 / peak,
+            "note": "per CG iteration incl. one V-cycle; the working set (<= 8 vectors of "
+                    f"{m * 8 / 1e6:.1f} MB) is largely L2-resident, so HBM is an upper "
+                    "bound on the traffic, not the binding limit"}
+    return out
 
 
 def traffic_from_profiles():
@@ -235,6 +267,250 @@ def traffic_from_profiles():
         except json.JSONDecodeError:
             return {}
     return {}
+
+
+def workload_config(k):
+    """The `config` object of both arms (identical, so the driver's
+    same-config check holds): the BASELINE.json workload and its sizes."""
+    from paper_2403_08084_b200.configs import DESCRIPTIONS, GRID, STEPS
+
+    dim, N = GRID[k]
+    m = (N + 1) ** dim
+    edges = (2 * N * (N + 1) + N * N) if dim == 2 else (3 * N * (N + 1) ** 2 + 3 * N * N * (N + 1)
+                                                         + N ** 3)
+    op_bytes = (m + 2 * edges) * 20 + 3 * 8 * m * 4
+    return {"workload": f"config {k}: {DESCRIPTIONS[k]}", "m": m, "nnz": m + 2 * edges,
+            "trajectory_steps": STEPS[k],
+            "timed": "steps 1..K of the trajectory from u0 (warm-up steps run first, then "
+                     "the state is reset to u0)",
+            "l2": ("inputs larger than L2 (operators + stage vectors "
+                   f"~{op_bytes / 1e6:.0f} MB > 126 MB)") if op_bytes > L2_BYTES else
+                  "working set smaller than L2: a 256 MB buffer is written between timed "
+                  "steps (inside the timed region)"}
+
+
+class L2Flush:
+    def __init__(self, k):
+        import torch
+
+        cfg = workload_config(k)
+        self.buf = None
+        if not cfg["l2"].startswith("inputs larger"):
+            self.buf = torch.empty(64 * 2**20, dtype=torch.float32, device="cuda")
+
+    def __call__(self):
+        if self.buf is not None:
+            self.buf.fill_(1.0)
+
+
+def time_trajectory(st, prob, steps, warmup, k, clk=None, sample_at=()):
+    """W warm-up steps, reset to u0, then `steps` device-timed steps
+    (CUDA events on the launching stream).  Returns (seconds, reports,
+    launches)."""
+    import torch
+
+    from paper_2403_08084_b200 import _lib
+
+    snap = (st.u.copy(), st.step_index, st._t_base)
+    for _ in range(warmup):
+        st.step_device(prob)
+    torch.cuda.synchronize()
+    st.u, st.step_index, st._t_base = snap[0].copy(), snap[1], snap[2]
+    flush = L2Flush(k)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    w0 = time.perf_counter()
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/
+    e0.record(stream)
+    for i in range(steps):
+        flush()
+        _, rep = st.step_device(prob)
+        reps.append(rep)
+        if clk is not None and i in sample_at:
+            clk.sample()
+    e1.record(stream)
+    torch.cuda.nvtx.range_pop()
+    torch.cuda.synchronize()
+    if clk is not None:
+        clk.mark(w0, time.perf_counter())
+    return e0.elapsed_time(e1) / 1e3, reps, _lib.launch_count() - launches0, snap
+
+
+def step_stats(reps):
+    krylov = [r.krylov_iters for r in reps]
+    inner = [sum((sum(v) if isinstance(v, list) else (v or 0)) for v in r.inner_iters)
+             for r in reps]
+    return {"krylov_iters_per_step": float(np.mean(krylov)) if krylov else None,
+            "inner_iters_per_step": float(np.mean(inner)) if inner else None,
+            "newton_iters_per_step": float(np.mean([r.newton_iters for r in reps])) if reps else None}
+
+
+# ------------------------------------------------------- CPU port (oracle)
+
+
+def spawn_cpu_jobs(ks, budget, avoid_cpu):
+    """CPU baselines as subprocesses (one core each, pinned away from this
+    process's core) so they run while the GPU arm works."""
+    import subprocess
+
+    try:
+        cpus = sorted(os.sched_getaffinity(0))
+    except AttributeError:
+        cpus = list(range(os.cpu_count() or 1))
+    free = [c for c in cpus if c != avoid_cpu]
+    jobs = {}
+    parallel = len(free) >= len(ks) + 1
+    for i, k in enumerate(ks):
+        cmd = [sys.executable, str(Path(__file__).resolve()), "--cpu-job", str(k),
+               "--cpu-budget", str(budget)]
+        if parallel:
+            cmd = ["taskset", "-c", str(free[i % len(free)])] + cmd
+        env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1",
+                   MKL_NUM_THREADS="1", CUDA_VISIBLE_DEVICES="")
+        jobs[k] = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                   text=True, env=env) if parallel else cmd
+    return jobs, parallel
+
+
+def collect_cpu_jobs(jobs, parallel, timeout=900):
+    import subprocess
+
+    out = {}
+    for k, j in jobs.items():
+        try:
+            if parallel:
+                so, se = j.communicate(timeout=timeout)
+            else:
+                env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1",
+                           CUDA_VISIBLE_DEVICES="")
+                r = subprocess.run(j, capture_output=True, text=True, timeout=timeout, env=env)
+                so, se = r.stdout, r.stderr
+            line = [x for x in so.splitlines() if x.startswith("{")]
+            out[k] = json.loads(line[-1]) if line else {"error": se[-400:]}
+        except Exception as exc:  # a baseline must never sink the GPU line
+            if parallel:
+                j.kill()
+            out[k] = {"error": f"{type(exc).__name__}: {exc}"[:400]}
+    return out
+
+
+def _cpu_env():
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import irk_oracle as orc
+
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count()
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return orc, {"cpu_model": model, "affinity_cores": cores}
+
+
+_BLOCK = {1: "lu", 2: "lu", 3: "pcg", 4: "pcg", 5: "pcg"}
+_BLOCK_TXT = {"lu": "exact SuperLU blocks (scipy splu: the reference's factorize_block, "
+                    "sparsela.py:171-191)",
+              "pcg": "Jacobi-PCG/COCG inner blocks (SuperLU infeasible at this size: 3D "
+                     "fill-in, or per-Newton factorisations)"}
+
+
+def cpu_port(k):
+    """The CPU port of the reference path (oracle/irk_oracle.py Stepper:
+    MGS FGMRES, the reference's preconditioners) with its setup done and
+    timed separately, as cli.run_precond_bench does (cli.py:224-242)."""
+    orc, env = _cpu_env()
+    cfg = orc.config(k, None, block=_BLOCK[k])
+    st = orc.Stepper(cfg["problem"], cfg["tab"], cfg["dt"], **cfg["settings"])
+    t0 = time.perf_counter()
+    st.setup()
+    return orc, st, cfg, time.perf_counter() - t0, env
+
+
+def cpu_job(k, budget):
+    """Real steps of the CPU port from step 1 of config k on one core until
+    `budget` seconds (at least one step).  Config 4 (DIRK on 4.2M DOFs: one
+    exact factorisation ~10 min, or 3 x ~1500 Jacobi-PCG iterations per step)
+    times one real stage solve and counts a step as its three stage solves."""
+    orc, st, cfg, t_setup, env = cpu_port(k)
+    if k == 4:
+        p, tab, dt = cfg["problem"], cfg["tab"], cfg["dt"]
+        A = np.asarray(tab.A)
+        blk = st._dirk_blocks[A[0, 0]]
+        rhs = -(p.K @ p.u0)
+        rhs[p.dofs] = 0.0
+        t0 = time.perf_counter()
+        _, its = orc.jacobi_pcg(blk.C, rhs, 1e-12)
+        t = time.perf_counter() - t0
+        return {"value": 1.0 / (3 * t), "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": f"config 4: the first stage solve of step 1 (n = {len(rhs)}, Jacobi-PCG "
+                          f"to rtol 1e-12: {its} iterations, {t:.1f} s) on 1 core; a step = its 3 "
+                          f"stage solves (same operator and tolerance); setup {t_setup:.1f} s "
+                          "excluded", **env}
+    t0 = time.perf_counter()
+    n = 0
+    while n < cfg["steps"]:
+        st.step()
+        n += 1
+        if time.perf_counter() - t0 >= budget:
+            break
+    t = time.perf_counter() - t0
+    its = [r[1] for r in st.reports]
+    return {"value": n / t, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"config {k}: real steps 1..{n} of the trajectory ({t:.1f} s; FGMRES its "
+                      f"{its}) on 1 core, {_BLOCK_TXT[_BLOCK[k]]}, MGS FGMRES as the reference; "
+                      f"setup {t_setup:.1f} s excluded (cli.run_precond_bench)", **env}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the CPU implementation of the path (the oracle
+    port; the reference itself is Python and cannot travel to the box) on
+    the host, rank 0 only: setup, W real warm-up steps, reset to u0, then K
+    real timed steps -- steps 1..K of the trajectory, as the GPU arm."""
+    if rank != 0:
+        return
+    k = args.config
+    orc, st, cfg, t_setup, env = cpu_port(k)
+    if k == 4:
+        r = cpu_job(4, 0)
+        value, sec, sample = r["value"], 1.0 / r["value"], r["sample"]
+    else:
+        for _ in range(args.warmup):
+            st.step()
+        st.reset()
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            st.step()
+            times.append(time.perf_counter() - t0)
+        sec = float(np.mean(times))
+        value = 1.0 / sec
+        sample = (f"config {k}: real steps 1..{args.steps} of the trajectory after {args.warmup} "
+                  f"warm-up steps and a reset to u0, {_BLOCK_TXT[_BLOCK[k]]}, MGS FGMRES as "
+                  f"the reference (FGMRES its {[r[1] for r in st.reports]}); setup "
+                  f"{t_setup:.1f} s excluded (cli.run_precond_bench); 1 core (the block "
+                  "solves and the Gauss-Seidel sweep are sequential)")
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * sec, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded u0 per BASELINE.json config; assembled P1 operators)",
+           "impl": "reference", "config": workload_config(k),
+           "parallelism": "cpu, 1 core (rank 0)",
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                            "sample": sample, **env},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+# ----------------------------------------------------------------- ours
 
 
 def run_ours(args, world, rank, local):
@@ -248,73 +524,40 @@ def run_ours(args, world, rank, local):
     from paper_2403_08084_b200 import _lib, configs
 
     _lib.load()
+    k = args.config
+    solo = rank == 0 and world == 1
+    cpu_jobs = None
+    if solo and not args.no_cpu_baseline:
+        ks = [k] + ([j for j in (1, 2, 3, 4, 5) if j != k] if not args.no_workloads else [])
+        try:
+            me = os.sched_getaffinity(0)
+            me = min(me) if len(me) == 1 else -1
+        except AttributeError:
+            me = -1
+        cpu_jobs = spawn_cpu_jobs(ks, args.cpu_budget, me)
     # experiments only: IRK_BENCH_BLOCK='{"mg_nu": 3}' overrides block-solver settings
-    wl = configs.build(args.config, **json.loads(os.environ.get("IRK_BENCH_BLOCK", "{}")))
+    wl = configs.build(k, **json.loads(os.environ.get("IRK_BENCH_BLOCK", "{}")))
     st, prob = wl.stepper, wl.problem
     clk = ClockSampler(local).__enter__()
     clk.sample()  # the first NVML query costs ~2 ms: keep it out of the timed region
-    for _ in range(args.warmup):
-        st.step_device(prob)
-    torch.cuda.synchronize()
     barrier(world)
-    # the e2e arm below replays exactly these timed steps (same states, same
-    # solver work): snapshot the stepper state
-    # (a host copy: a device clone here occupied a cached allocator block
-    # the first timed step then had to cudaMalloc afresh, 2-7x slower)
-    snap = (st.u.copy(), st.step_index, st._t_base)
-    reps = []
-    stream = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = _lib.launch_count()
-    if os.environ.get("IRK_BENCH_NOGC"):
-        import gc
-
-        gc.disable()
-    if True:
-        torch.cuda.synchronize()
-        w_t0 = time.perf_counter()
-        torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/
-        e0.record(stream)
-        marks = []
-        sample_at = {args.steps // 3, (2 * args.steps) // 3, args.steps - 1}
-        for i in range(args.steps):
-            _, rep = st.step_device(prob)
-            reps.append(rep)
-            if i in sample_at:
-                ts0 = time.perf_counter()
-                clk.sample()
-                if os.environ.get("IRK_BENCH_TRACE"):
-                    print(f"sample after step {i}: {1e3 * (time.perf_counter() - ts0):.2f} ms",
-                          file=sys.stderr)
-            if os.environ.get("IRK_BENCH_TRACE"):
-                ev = torch.cuda.Event(enable_timing=True)
-                ev.record(stream)
-                marks.append((ev, time.perf_counter()))
-        e1.record(stream)
-        torch.cuda.nvtx.range_pop()
-        torch.cuda.synchronize()
-        clk.mark(w_t0, time.perf_counter())
-    clk.__exit__(None, None, None)
-    launches = _lib.launch_count() - launches0
-    if marks:
-        prev_e, prev_w = e0, None
-        for k, (ev, wt) in enumerate(marks):
-            print(f"step {k}: {prev_e.elapsed_time(ev):.2f} ms device, krylov "
-                  f"{reps[k].krylov_iters}", file=sys.stderr)
-            prev_e = ev
-    t_dev = e0.elapsed_time(e1) / 1e3
+    sample_at = {args.steps // 3, (2 * args.steps) // 3, args.steps - 1}
+    t_dev, reps, launches, snap = time_trajectory(st, prob, args.steps, args.warmup, k, clk,
+                                                  sample_at)
     t_max, value = replica_throughput(t_dev, args.steps, world)
 
     # end to end through the public API with host buffers: every step sets
     # the state from a pinned host array (H2D), steps, and reads u_next back
-    # (D2H into the pinned numpy array step() returns, which is the next
-    # step's input).
-    st.u, st.step_index, st._t_base = snap[0], snap[1], snap[2]
-    u_host = torch.from_numpy(st.u.copy()).pin_memory().numpy()
+    # (D2H into the pinned numpy array step() returns, the next input); the
+    # same steps 1..K from u0
+    st.u, st.step_index, st._t_base = snap[0].copy(), snap[1], snap[2]
+    u_host = torch.from_numpy(snap[0].copy()).pin_memory().numpy()
+    flush = L2Flush(k)
     barrier(world)
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     for _ in range(args.steps):
+        flush()
         st.u = u_host
         u_host, _ = st.step(prob)
     torch.cuda.synchronize()
@@ -324,50 +567,40 @@ def run_ours(args, world, rank, local):
 
     peak, peak_kind = peaks()
     t_sa, b_sa, meta_sa = stage_apply_roofline(wl)
-    inner_prof = inner_solve_profile(wl)
+    inner_prof = inner_solve_profile(wl, peak)
     traffic = traffic_from_profiles()
-    krylov = [r.krylov_iters for r in reps]
-    inner = [sum(sum(v) if isinstance(v, list) else v for v in r.inner_iters) for r in reps]
-    # the committed ncu traffic figure is the config-2 capture
-    stage_apply = {"bound": "hbm", "achieved": b_sa / t_sa / 1e9, "peak": peak, "unit": "GB/s",
-                   "frac": b_sa / t_sa / 1e9 / peak,
-                   "traffic": traffic.get("k_stage_apply") if args.config == 2 else None,
-                   "us_per_launch": t_sa * 1e6, "algorithmic_bytes": b_sa, **meta_sa}
-    # roofline: the fused stage-operator apply (K2), the kernel the metric
-    # names; HBM-bound with inputs larger than L2
-    roof = dict(stage_apply, kernel="K2 masked stage-operator apply (k_stage_apply_std on stencil patterns, k_stage_apply_win otherwise)")
+    stats = step_stats(reps)
+    roof = {"bound": "hbm", "achieved": b_sa / t_sa / 1e9, "peak": peak, "unit": "GB/s",
+            "frac": b_sa / t_sa / 1e9 / peak,
+            "traffic": traffic.get("k_stage_apply" if k == 2 else f"k_stage_apply_config{k}"),
+            "us_per_launch": t_sa * 1e6, "algorithmic_bytes": b_sa, **meta_sa,
+            "kernel": "K2 masked stage-operator apply (k_stage_apply_std)"}
     inner_solver = None
     if inner_prof is not None:
-        # the step's dominant cost: the inner block solves (replacing the
-        # reference's SuperLU solves).  A multigrid-PCG solve is dozens of
-        # short kernels over an L2-resident working set (replayed as CUDA
-        # graphs with a device-side loop); it is latency-, not HBM-bound.
-        t_in, meta_in = inner_prof
         solves = [len(r.inner_iters) for r in reps]
-        inner_solver = {
-            "us_per_solve": t_in * 1e6,
-            "us_per_iteration": t_in * 1e6 / max(meta_in["iterations_per_solve"], 1),
-            "solves_per_step": float(np.mean(solves)) if solves else None,
-            "step_share_est": (float(np.mean(inner)) * t_in
-                               / max(meta_in["iterations_per_solve"], 1) * args.steps / t_dev)
-            if inner else None, **meta_in}
+        per_it = inner_prof["us_per_iteration"] * 1e-6
+        inner_solver = dict(inner_prof, solves_per_step=float(np.mean(solves)) if solves else None)
+        if stats["inner_iters_per_step"]:
+            inner_solver["step_share_est"] = min(
+                1.0, stats["inner_iters_per_step"] * per_it * args.steps / t_dev)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded u0 per BASELINE.json config; assembled P1 operators)",
-        "config": {"workload": f"config {args.config}: {wl.description}", "m": prob.m,
-                   "nnz": prob.mass.nnz, "replicas": world, "parallelism": f"replicas{world}",
-                   "l2": "inputs larger than L2 (operators + vectors > 126 MB)"},
+        "config": workload_config(k), "parallelism": f"replicas{world}",
         "e2e": e2e, "gpu_launches": launches,
-        "roofline": roof, "inner_solver": inner_solver,
-        "peak_source": peak_kind,
-        "krylov_iters_per_step": float(np.mean(krylov)) if krylov else None,
-        "inner_iters_per_step": float(np.mean(inner)) if inner else None,
-        "clocks": clk.summary(),
+        "roofline": roof, "inner_solver": inner_solver, "peak_source": peak_kind,
+        **stats, "clocks": clk.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_sample(args.config, budget=args.cpu_budget)
+    if solo and not args.no_workloads:
+        out["workloads"] = other_workloads(k, args)
+    if cpu_jobs is not None:
+        res = collect_cpu_jobs(*cpu_jobs)
+        out["cpu_baseline"] = res.get(k)
+        for j, r in res.items():
+            if j != k and "workloads" in out and str(j) in out["workloads"]:
+                out["workloads"][str(j)]["cpu_baseline"] = r
     if rank == 0:
         print(json.dumps(out))
     if world > 1:
@@ -376,113 +609,40 @@ def run_ours(args, world, rank, local):
         dist.destroy_process_group()
 
 
-# ------------------------------------------------------- CPU port (oracle)
+def other_workloads(k0, args):
+    """Every other BASELINE.json workload on this GPU: its whole trajectory
+    (config steps) after 3 warm-up steps and a reset to u0, device-timed;
+    config 2 also as written (inner blocks by Jacobi-PCG to 1e-6)."""
+    import gc
 
+    from paper_2403_08084_b200 import configs
 
-_CPU_SETUP = {}
-
-
-def cpu_sample(k, budget=20.0, block="pcg"):
-    """Time the CPU port of the reference path (oracle/irk_oracle.py) on the
-    full workload: setup excluded as in cli.run_precond_bench
-    (cli.py:224-242), then FGMRES iterations (preconditioner apply +
-    constrained stage apply) until `budget` seconds; steps/s =
-    1 / (seconds per FGMRES iteration x FGMRES iterations per step).
-    block="lu": exact SuperLU blocks (scipy splu) -- the reference's own
-    algorithm (factorize_block, sparsela.py:171-191), feasible for configs 1
-    and 2; "pcg": Jacobi-PCG blocks.  The setup is cached per (k, block)."""
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import irk_oracle as orc
-
-    key = (k, block)
-    if key not in _CPU_SETUP:
-        cfg = orc.config(k, None, block=block)
-        p, tab = cfg["problem"], cfg["tab"]
-        t_setup0 = time.perf_counter()
-        pc = None
-        if cfg["settings"]["pc"] is not None:
-            pc = orc.StagePC(cfg["settings"]["pc"], tab, p.M, [p.K], cfg["dt"],
-                             "ia" if cfg["settings"]["form"] == "ia" else "ai", p.dofs, block,
-                             cfg["settings"]["inner_rtol"])
-        _CPU_SETUP[key] = (cfg, pc, time.perf_counter() - t_setup0)
-    cfg, pc, t_setup = _CPU_SETUP[key]
-    p, tab, dt = cfg["problem"], cfg["tab"], cfg["dt"]
-    s, m = tab.s, p.M.shape[0]
-    A = np.asarray(tab.A)
-    if k == 4:
-        blk = orc.Block(p.M, p.K, 1.0, dt * A[0, 0], p.dofs, "pcg", 1e-12)
-        rhs = -(p.K @ p.u0)
-        rhs[p.dofs] = 0.0
-        t0 = time.perf_counter()
-        _, its = orc.jacobi_pcg(blk.C, rhs, 1e-12, maxit=400)
-        t = time.perf_counter() - t0
-        per_stage = t / its * 1558.0  # survey-measured CG iterations per stage solve
-        sec_step = 3 * per_stage
-        return {"value": 1.0 / sec_step, "unit": UNIT, "cores": 1, "kind": "port",
-                "sample": f"config 4: {its} Jacobi-PCG iterations of stage 1 (n=4.2M) on 1 core, "
-                          f"{t / its * 1e3:.1f} ms/it, scaled by 3 stages x 1558 its/stage"}
-    C1, C2 = (np.eye(s), A)
-    op = lambda v: orc.kron_apply(C1, C2, p.M, [p.K], dt, v)  # noqa: E731
-    idx = orc.stage_index(s, m, p.dofs)
-    sop = orc.constrained(op, idx) if len(p.dofs) else op
-    v = np.random.default_rng(0).standard_normal(s * m)
-    n_it, t0 = 0, time.perf_counter()
-    while True:
-        z = pc.apply(v) if pc is not None else v
-        w = sop(z)
-        v = w / np.linalg.norm(w)
-        n_it += 1
-        if time.perf_counter() - t0 > budget:
-            break
-    t_it = (time.perf_counter() - t0) / n_it
-    its = CPU_ITS_PER_STEP.get(k, 12.0)
-    blocks = ("exact SuperLU blocks (the reference's algorithm)" if block == "lu"
-              else "Jacobi-PCG blocks")
-    return {"value": 1.0 / (t_it * its), "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"config {k} (m={m}), {blocks}: {n_it} FGMRES iterations "
-                      f"(preconditioner apply + constrained stage apply) on 1 core, "
-                      f"{t_it:.2f} s/it, scaled by {its} its/step; setup {t_setup:.1f} s "
-                      f"excluded"}
-
-
-def _description(k):
-    try:
-        from paper_2403_08084_b200.configs import DESCRIPTIONS
-
-        return DESCRIPTIONS[k]
-    except Exception:  # the reference arm needs no GPU package
-        return ""
-
-
-def run_reference(args, world, rank):
-    """--impl reference: the CPU port of the reference path on the host
-    cores (rank 0 only), each step a bounded sample (one FGMRES iteration of
-    the full workload, scaled to a time step)."""
-    if rank != 0:
-        return
-    # exact SuperLU blocks where the reference can factorise (configs 1, 2;
-    # one-time setup excluded, as the reference's own bench does); the 3D,
-    # DIRK-2048^2 and per-Newton cases use the Jacobi-PCG port
-    block = "lu" if args.config in (1, 2) else "pcg"
-    budget = max(2.0, min(20.0, 90.0 / max(1, args.steps + args.warmup)))
-    samples = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_sample(args.config, budget=budget, block=block)
-        if i >= args.warmup:
-            samples.append(1.0 / r["value"])
-    sec = float(np.mean(samples))
-    value = 1.0 / sec
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": 1e3 * sec, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "impl": "reference",
-           "config": {"workload": f"config {args.config}: {_description(args.config)}",
-                      "parallelism": "cpu-1-core (rank 0)"},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-                            "sample": r["sample"]},
-           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out))
+    peak, _ = peaks()
+    res = {}
+    plan = [(j, {}) for j in (1, 2, 3, 4, 5) if j != k0]
+    plan.append((2, {"method": "pcg"}))
+    for j, block in plan:
+        wl = configs.build(j, **block)
+        t, reps, launches, _ = time_trajectory(wl.stepper, wl.problem, wl.steps, 3, j)
+        key = str(j) if not block else f"{j}-spec-literal"
+        r = {"workload": wl.description, "value": wl.steps / t, "unit": UNIT,
+             "steps": wl.steps, "ms_per_step": 1e3 * t / wl.steps, "gpu_launches": launches,
+             "config": workload_config(j), **step_stats(reps)}
+        if block:
+            r["workload"] = (f"config {j} as written: inner diagonal blocks by Jacobi-PCG to "
+                             "rtol 1e-6 (BlockSolveSettings(method='pcg'))")
+        else:
+            t_sa, b_sa, meta = stage_apply_roofline(wl)
+            r["roofline"] = {"bound": "hbm", "achieved": b_sa / t_sa / 1e9, "peak": peak,
+                             "unit": "GB/s", "frac": b_sa / t_sa / 1e9 / peak,
+                             "us_per_launch": t_sa * 1e6, "algorithmic_bytes": b_sa, **meta}
+            ip = inner_solve_profile(wl, peak)
+            if ip is not None:
+                r["inner_solver"] = ip
+        res[key] = r
+        del wl
+        gc.collect()
+    return res
 
 
 def main():
@@ -493,8 +653,15 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-workloads", action="store_true",
+                    help="headline workload only (no per-config lines, no extra CPU jobs)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-job", type=int, default=0, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.cpu_job:
+        os.environ.setdefault("OMP_NUM_THREADS", "1")
+        print(json.dumps(cpu_job(args.cpu_job, args.cpu_budget)))
+        return
     if args.warmup < 3:
         args.warmup = 3
     world, rank, local = dist_setup(args)

@@ -60,8 +60,10 @@ int64_t irk_ctx_launch_count(const irk_ctx* ctx);
  * without synchronising and append (iterations, code 0 ok / 1 cap /
  * 2 breakdown, loop iterations, kernels per loop pass) to a device log;
  * irk_ctx_log_take copies the entries in call order (synchronous) and
- * clears the log.  Enabling also clears it. */
+ * clears the log.  Enabling also clears it.  The log grows on demand;
+ * irk_ctx_log_size reports the number of pending entries. */
 int irk_ctx_log_enable(irk_ctx* ctx, int on);
+int irk_ctx_log_size(const irk_ctx* ctx, int64_t* n_out);
 int irk_ctx_log_take(irk_ctx* ctx, int* out_host, int max_entries, int* n_out);
 const char* irk_last_error(void);
 /* Library version string. */
@@ -131,6 +133,12 @@ int irk_mat_semilinear_jacobian(irk_ctx* ctx, const irk_mat* M, const irk_mat* K
 int irk_mat_diagonal(irk_ctx* ctx, const irk_mat* A, double* diag_dev);
 /* Row sums (lumped mass), rowsum_dev[r] = sum_c A[r,c]. */
 int irk_mat_rowsum(irk_ctx* ctx, const irk_mat* A, double* rowsum_dev);
+/* out[r] = sum_c |A[r,c]| (Gershgorin radii of D^-1 A with irk_mat_diagonal;
+ * the Chebyshev block solver's bounds). */
+int irk_mat_absrowsum(irk_ctx* ctx, const irk_mat* A, double* out_dev);
+/* Dense row-major n x n copy of a square matrix into device memory (the
+ * direct block solver's setup; replaces a host to_dense + copy). */
+int irk_mat_to_dense(irk_ctx* ctx, const irk_mat* A, double* dense_dev);
 
 /* y = A x (k right-hand sides, interleaved: x[c*k + j]).  Replaces spmv
  * (sparsela.py:118-123). */

@@ -722,6 +722,28 @@ class Stepper:
         X = x.reshape(s, m)
         return u + dt * (tab.b @ X), (len(hist) - 1, ktot, hist[-1])
 
+    def setup(self):
+        """Build the preconditioner / DIRK stage block now (the reference's
+        cli.run_precond_bench forces setup before timing, cli.py:224-242)."""
+        tab, p, dt = self.tab, self.p, self.dt
+        if self.form == "dirk":
+            A = np.asarray(tab.A)
+            for key in sorted(set(np.diag(A).tolist())):
+                if key not in self._dirk_blocks:
+                    self._dirk_blocks[key] = Block(p.M, p.K, 1.0, dt * key, p.dofs,
+                                                   "lu" if self.block == "lu" else "pcg",
+                                                   self.kry["rtol"])
+        elif self.p.poly is None and self._pc is None and self.pc_kind is not None:
+            self._pc = StagePC(self.pc_kind, tab, p.M, [p.K], dt, "ia" if self.form == "ia" else "ai",
+                               p.dofs, self.block, self.inner_rtol)
+
+    def reset(self, u0=None):
+        """Back to the initial state (caches kept)."""
+        self.u = np.array(self.p.u0 if u0 is None else u0, dtype=float)
+        self.t = 0.0
+        self.stages.clear()
+        self.reports.clear()
+
     def step(self):
         if self.form == "dirk":
             un, rep = self._dirk()

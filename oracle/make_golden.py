@@ -170,9 +170,56 @@ def ref_problem(irk, cfg):
                                    dirichlet=bc, u0=p.u0)
 
 
+class StageRecorder:
+    """Records the stage vectors the reference computes but does not keep.
+
+    DIRK (stepper.py:391-421): every linear stage is ``res = fgmres(...)``
+    and ``ki = res.x`` is then overwritten at the Dirichlet dofs in place, so
+    the recorded ``res.x`` objects ARE the final K_stages rows.  The wrapper
+    replaces the module attribute ``implicitrk.stepper.fgmres`` (the
+    reference's source is untouched).  Newton (stepper.py:519-541): the last
+    s residual evaluations of a step are at the converged iterate; their
+    ``udot`` arguments are the stage derivatives (the AI unknown)."""
+
+    def __init__(self, irk):
+        import implicitrk.stepper as rst
+
+        self.rst, self.orig, self.xs = rst, rst.fgmres, []
+
+        def rec(*a, **kw):
+            res = self.orig(*a, **kw)
+            self.xs.append(res.x)
+            return res
+
+        rst.fgmres = rec
+        self.udots = []
+
+    def take_dirk(self, s):
+        out = np.array([np.asarray(x, dtype=float).copy() for x in self.xs[-s:]])
+        self.xs.clear()
+        return out
+
+    def take_newton(self, s):
+        out = np.array(self.udots[-s:])
+        self.udots.clear()
+        return out
+
+    def close(self):
+        self.rst.fgmres = self.orig
+
+
 def trajectory(irk, k, n, steps=None, full=False):
     cfg = orc.config(k, n)
     prob = ref_problem(irk, cfg)
+    rec = StageRecorder(irk) if k in (4, 5) else None
+    if k == 5:
+        res0 = prob.residual
+
+        def residual(t, u, udot):
+            rec.udots.append(np.array(udot, dtype=float))
+            return res0(t, u, udot)
+
+        prob.residual = residual
     tab = cfg["tab"]
     rt = irk.ButcherTableau(tab.A, tab.b, tab.c, 1, 1, tab.name)
     st = cfg["settings"]
@@ -194,26 +241,42 @@ def trajectory(irk, k, n, steps=None, full=False):
     for i in range(nsteps):
         u, rep = stp.step(prob)
         its.append((rep.newton_iters, rep.krylov_iters))
+        xs = None
+        if k == 4:
+            xs = rec.take_dirk(tab.s).ravel()  # K_stages, stage-major
+        elif k == 5:
+            xs = rec.take_newton(tab.s).ravel()
+        elif stp._last_stages is not None:
+            xs = stp._last_stages
         if full:
             if P is None:
                 P = orc.sketch_rows(len(u))
-                Ps = orc.sketch_rows(len(u) * tab.s, seed=77)
+                # per-stage projections for DIRK (s*m Gaussian rows would be 3 GB)
+                Ps = orc.sketch_rows(len(u) if k == 4 else len(u) * tab.s, seed=77)
             sk = orc.sketch(u, P)
             for f in ("proj", "sample", "norm", "sum"):
                 out[f"{key}_u{i}_{f}"] = np.asarray(sk[f])
-            if stp._last_stages is not None and k != 4:
-                sks = orc.sketch(stp._last_stages, Ps)
-                out[f"{key}_x{i}_proj"] = sks["proj"]
-                out[f"{key}_x{i}_norm"] = np.asarray(sks["norm"])
+            if xs is not None:
+                if k == 4:
+                    X = xs.reshape(tab.s, -1)
+                    out[f"{key}_x{i}_proj"] = np.stack([Ps @ X[j] for j in range(tab.s)])
+                    out[f"{key}_x{i}_norm"] = np.asarray(np.linalg.norm(xs))
+                    out[f"{key}_x{i}_sample"] = xs[:: max(1, len(xs) // 4096)].copy()
+                else:
+                    sks = orc.sketch(xs, Ps)
+                    out[f"{key}_x{i}_proj"] = sks["proj"]
+                    out[f"{key}_x{i}_norm"] = np.asarray(sks["norm"])
             print(f"  config {k} step {i + 1}/{nsteps} its {its[-1]} {time.time() - t0:.1f}s",
                   flush=True)
         else:
             us.append(u.copy())
-            if stp._last_stages is not None:
-                stages.append(stp._last_stages.copy())
+            if xs is not None:
+                stages.append(np.array(xs, dtype=float))
+    if rec is not None:
+        rec.close()
     if not full:
         out[f"{key}_u"] = np.array(us)
-        if stages and k != 4 and k != 5:
+        if stages:
             out[f"{key}_x"] = np.array(stages)
     out[f"{key}_its"] = np.array(its)
     out[f"{key}_wall"] = np.array(time.time() - t0)

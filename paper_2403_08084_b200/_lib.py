@@ -48,6 +48,8 @@ _SIGS = {
     "irk_mat_semilinear_jacobian": [_vp, _vp, _vp, _dbl, _vp, _i64, _i64, C.POINTER(_vp)],
     "irk_mat_diagonal": [_vp, _vp, _vp],
     "irk_mat_rowsum": [_vp, _vp, _vp],
+    "irk_mat_absrowsum": [_vp, _vp, _vp],
+    "irk_mat_to_dense": [_vp, _vp, _vp],
     "irk_spmv": [_vp, _vp, _int, _vp, _vp],
     "irk_stage_apply": [_vp, _int, _vp, _vp, _dbl, _vp, _vp, _int, _vp, _vp, _vp],
     "irk_stage_apply_semilinear": [_vp, _int, _vp, _vp, _dbl, _vp, _vp, _dbl, _vp, _vp, _vp, _vp],
@@ -85,6 +87,7 @@ _SIGS = {
     "irk_fe_error_sq": [_vp, _int, _i64, _vp, _vp, _vp, _vp],
     "irk_ctx_log_enable": [_vp, _int],
     "irk_ctx_log_take": [_vp, _vp, _int, _vp],
+    "irk_ctx_log_size": [_vp, _vp],
     "irk_mg_create": [_vp, _int, _int, _vp, _vp, _vp, _int, _int, _vp],
     "irk_mg_destroy": [_vp],
     "irk_mg_vcycle": [_vp, _vp, _vp, _vp],
@@ -258,10 +261,12 @@ class deferred_solves:
         return self
 
     def __exit__(self, *exc):
-        buf = np.zeros((4096, 4), dtype=np.int32)
         n = C.c_int(0)
         try:
-            call("irk_ctx_log_take", ctx(), hptr(buf), 4096, C.byref(n))
+            size = C.c_int64(0)
+            call("irk_ctx_log_size", ctx(), C.byref(size))
+            buf = np.zeros((max(int(size.value), 1), 4), dtype=np.int32)
+            call("irk_ctx_log_take", ctx(), hptr(buf), len(buf), C.byref(n))
         finally:
             call("irk_ctx_log_enable", ctx(), 0)
         self.entries = buf[: n.value].copy()

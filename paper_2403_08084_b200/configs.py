@@ -69,7 +69,7 @@ INNER_RTOL = {5: 1e-2}
 
 def build(k: int, n: int | None = None, inner_rtol: float | None = None, **block) -> Workload:
     dim, n0 = GRID[k]
-    grid = pb.StructuredGrid(dim, n or n0)
+    grid = pb.structured_grid(dim, n or n0)
     u0 = initial_state(k, grid)
     if k == 5:
         prob = pb.allen_cahn_problem(grid, 0.02, u0)

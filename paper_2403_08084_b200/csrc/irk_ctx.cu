@@ -123,6 +123,28 @@ int irk_ctx_synchronize(irk_ctx* ctx) {
 
 int64_t irk_ctx_launch_count(const irk_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
+}  // extern "C"
+
+namespace irk {
+// Room for one more deferred-solve entry: the log doubles when full (a rare,
+// synchronous event; entries already written are carried over in order).
+int log_reserve(irk_ctx* ctx) {
+  if (ctx->log_n < ctx->log_cap) return IRK_OK;
+  const int cap = ctx->log_cap * 2;
+  int* fresh = nullptr;
+  IRK_CUDA(cudaMalloc(&fresh, (size_t)cap * 4 * sizeof(int)));
+  IRK_CUDA(cudaMemcpyAsync(fresh, ctx->solve_log, (size_t)ctx->log_n * 4 * sizeof(int),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+  IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+  IRK_CUDA(cudaFree(ctx->solve_log));
+  ctx->solve_log = fresh;
+  ctx->log_cap = cap;
+  return IRK_OK;
+}
+}  // namespace irk
+
+extern "C" {
+
 int irk_ctx_log_enable(irk_ctx* ctx, int on) {
   IRK_REQUIRE(ctx, "irk_ctx_log_enable: NULL context");
   if (on && !ctx->solve_log) {
@@ -131,6 +153,12 @@ int irk_ctx_log_enable(irk_ctx* ctx, int on) {
   }
   ctx->log_on = on ? 1 : 0;
   ctx->log_n = 0;
+  return IRK_OK;
+}
+
+int irk_ctx_log_size(const irk_ctx* ctx, int64_t* n_out) {
+  IRK_REQUIRE(ctx && n_out, "irk_ctx_log_size: NULL argument");
+  *n_out = ctx->log_n;
   return IRK_OK;
 }
 

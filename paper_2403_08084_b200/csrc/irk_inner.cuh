@@ -1368,8 +1368,9 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
     // finalising A: applies the decisions of the last issued iteration (cap)
     IRK_TRY(launch_a(s, issued));
   }
-  if (!its_host && !relres_host && ctx->log_on && ctx->log_n < ctx->log_cap) {
+  if (!its_host && !relres_host && ctx->log_on) {
     // deferred status: log the outcome on the device, no host round trip
+    IRK_TRY(log_reserve(ctx));
     launch(k_cg_log<T>, 1, 32, 0, s, st0, st1, NB, (int)body_kernels,
                                  ctx->solve_log + 4 * ctx->log_n);
     IRK_CHECK_LAUNCH(ctx);

@@ -143,7 +143,7 @@ int irk_chebyshev(irk_ctx* ctx, int nb, const double* alpha_host, const double* 
   IRK_REQUIRE(nb >= 1 && nb <= 4, "irk_chebyshev: 1 <= nb <= 4");
   IRK_REQUIRE(!Bm || (beta_host && Bm->pat == A->pat), "irk_chebyshev: Bm must share A's pattern");
   IRK_REQUIRE(iters >= 1, "irk_chebyshev: iters >= 1");
-  IRK_REQUIRE(ld_x == nb, "irk_chebyshev: ld_x must equal nb");
+  IRK_REQUIRE(ld_rhs >= nb && ld_x >= nb, "irk_chebyshev: leading dimensions must be >= nb");
   const int64_t m = A->pat->nrows;
   if (m == 0) return IRK_OK;
   SysParams<double> P{};
@@ -157,20 +157,10 @@ int irk_chebyshev(irk_ctx* ctx, int nb, const double* alpha_host, const double* 
     cp.delta[k] = 0.5 * (lmax_host[k] - lmin_host[k]);
   }
   const MatView V = make_view(A, Bm);
-  const size_t vec = ((size_t)m * nb * sizeof(double) + 255) & ~(size_t)255;
-  IRK_TRY(ensure_work(ctx, 4 * vec + 4096));
-  double* xa = reinterpret_cast<double*>(ctx->work);
-  double* xb = reinterpret_cast<double*>(ctx->work + vec);
-  double* ya = reinterpret_cast<double*>(ctx->work + 2 * vec);
-  double* yb = reinterpret_cast<double*>(ctx->work + 3 * vec);
-  double* rho_dev = reinterpret_cast<double*>(ctx->work + 4 * vec);
-  IRK_CUDA(cudaMemsetAsync(xa, 0, (size_t)m * nb * sizeof(double), ctx->stream));
-  IRK_CUDA(cudaMemsetAsync(ya, 0, (size_t)m * nb * sizeof(double), ctx->stream));
+  // three-term recurrence coefficients, precomputed on the host:
   // rho_0 = 1/sigma, rho_j = 1 / (2 sigma - rho_{j-1}), sigma = theta/delta
   double rho_prev[kMaxSys], rho_cur[kMaxSys];
   for (int k = 0; k < nb; ++k) rho_prev[k] = cp.delta[k] / cp.theta[k];
-  const int G = grid_for(ctx, m, kBlock, 4);
-  double *xin = xa, *xo = xb, *yin = ya, *yo = yb;
   std::vector<double> rv((size_t)iters * 2 * kMaxSys);
   for (int j = 0; j < iters; ++j) {
     double* rj = rv.data() + (size_t)j * 2 * kMaxSys;
@@ -182,17 +172,19 @@ int irk_chebyshev(irk_ctx* ctx, int nb, const double* alpha_host, const double* 
       rho_prev[k] = rho_cur[k];
     }
   }
+  const size_t vec = ((size_t)m * nb * sizeof(double) + 255) & ~(size_t)255;
   IRK_TRY(ensure_work(ctx, 4 * vec + rv.size() * sizeof(double) + 256));
-  xa = reinterpret_cast<double*>(ctx->work);
-  xb = reinterpret_cast<double*>(ctx->work + vec);
-  ya = reinterpret_cast<double*>(ctx->work + 2 * vec);
-  yb = reinterpret_cast<double*>(ctx->work + 3 * vec);
-  rho_dev = reinterpret_cast<double*>(ctx->work + 4 * vec);
-  xin = xa, xo = xb, yin = ya, yo = yb;
+  double* xa = reinterpret_cast<double*>(ctx->work);
+  double* xb = reinterpret_cast<double*>(ctx->work + vec);
+  double* ya = reinterpret_cast<double*>(ctx->work + 2 * vec);
+  double* yb = reinterpret_cast<double*>(ctx->work + 3 * vec);
+  double* rho_dev = reinterpret_cast<double*>(ctx->work + 4 * vec);
+  double *xin = xa, *xo = xb, *yin = ya, *yo = yb;
   IRK_CUDA(cudaMemsetAsync(xa, 0, (size_t)m * nb * sizeof(double), ctx->stream));
   IRK_CUDA(cudaMemsetAsync(ya, 0, (size_t)m * nb * sizeof(double), ctx->stream));
   IRK_CUDA(cudaMemcpyAsync(rho_dev, rv.data(), rv.size() * sizeof(double), cudaMemcpyHostToDevice,
                            ctx->stream));
+  const int G = grid_for(ctx, m, kBlock, 4);
   for (int j = 0; j < iters; ++j) {
     const double* rslot = rho_dev + (size_t)j * 2 * kMaxSys;
 #define IRK_CHEB(NBV)                                                                         \
@@ -215,9 +207,10 @@ int irk_chebyshev(irk_ctx* ctx, int nb, const double* alpha_host, const double* 
     std::swap(xin, xo);
     std::swap(yin, yo);
   }
-  IRK_CUDA(cudaMemcpyAsync(x_dev, xin, (size_t)m * nb * sizeof(double), cudaMemcpyDeviceToDevice,
-                           ctx->stream));
-  IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+  // strided store: row r of the nb systems goes to x_dev[r * ld_x + k]
+  IRK_CUDA(cudaMemcpy2DAsync(x_dev, (size_t)ld_x * sizeof(double), xin, nb * sizeof(double),
+                             nb * sizeof(double), (size_t)m, cudaMemcpyDeviceToDevice,
+                             ctx->stream));
   return IRK_OK;
 }
 

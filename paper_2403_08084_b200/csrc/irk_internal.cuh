@@ -144,6 +144,7 @@ constexpr int kNumCounters = 16;
 int ensure_red(irk_ctx* ctx, size_t doubles);
 int ensure_work(irk_ctx* ctx, size_t bytes);
 int ensure_pinned(irk_ctx* ctx, size_t bytes);
+int log_reserve(irk_ctx* ctx);
 // Byte-string key builder for the graph cache.
 struct GraphKey {
   std::string k;

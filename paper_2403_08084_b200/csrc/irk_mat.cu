@@ -683,6 +683,29 @@ __global__ void k_rowsum(int64_t nrows, const int* __restrict__ slice_ptr,
   out[r] = acc;
 }
 
+// Gershgorin data of D^-1 A: out[r] = sum_c |A[r,c]| (padding entries are 0)
+__global__ void k_absrowsum(int64_t nrows, const int* __restrict__ slice_ptr,
+                            const double* __restrict__ val, double* __restrict__ out) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrows) return;
+  int64_t s = r / kSlice;
+  int lane = (int)(r % kSlice);
+  int base = slice_ptr[s], width = (slice_ptr[s + 1] - base) / kSlice;
+  double acc = 0.0;
+  for (int k = 0; k < width; ++k) acc += fabs(val[base + k * kSlice + lane]);
+  out[r] = acc;
+}
+
+// dense row-major copy (dense zeroed by the caller): one thread per CSR entry
+__global__ void k_to_dense(int64_t nrows, const int* __restrict__ rowptr,
+                           const int* __restrict__ col, const int* __restrict__ csr2sell,
+                           const double* __restrict__ val, double* __restrict__ dense) {
+  int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (r >= nrows) return;
+  for (int p = rowptr[r] + (threadIdx.x & 31); p < rowptr[r + 1]; p += 32)
+    dense[r * nrows + col[p]] = val[csr2sell[p]];
+}
+
 // ----------------------------------------------------------------- SpMV
 // y[r*K + j] = sum_c A[r,c] x[c*K + j]; one thread per row on SELL-32.
 template <int K>
@@ -1046,6 +1069,29 @@ int irk_mat_diagonal(irk_ctx* ctx, const irk_mat* A, double* diag_dev) {
   if (n)
     k_diag<<<(unsigned)((n + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(
         n, A->pat->diag_pos, A->val, diag_dev);
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_mat_absrowsum(irk_ctx* ctx, const irk_mat* A, double* out_dev) {
+  IRK_REQUIRE(ctx && A && out_dev, "irk_mat_absrowsum: NULL argument");
+  int64_t n = A->pat->nrows;
+  if (n)
+    k_absrowsum<<<(unsigned)((n + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(
+        n, A->pat->slice_ptr, A->val, out_dev);
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_mat_to_dense(irk_ctx* ctx, const irk_mat* A, double* dense_dev) {
+  IRK_REQUIRE(ctx && A && dense_dev, "irk_mat_to_dense: NULL argument");
+  IRK_REQUIRE(A->pat->nrows == A->pat->ncols, "irk_mat_to_dense: square matrices only");
+  int64_t n = A->pat->nrows;
+  if (!n) return IRK_OK;
+  IRK_CUDA(cudaMemsetAsync(dense_dev, 0, (size_t)n * n * sizeof(double), ctx->stream));
+  const int rows_per_block = kBlock / 32;
+  k_to_dense<<<(unsigned)((n + rows_per_block - 1) / rows_per_block), kBlock, 0, ctx->stream>>>(
+      n, A->pat->rowptr, A->pat->col, A->pat->csr2sell, A->val, dense_dev);
   IRK_CHECK_LAUNCH(ctx);
   return IRK_OK;
 }

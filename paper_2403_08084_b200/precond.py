@@ -159,17 +159,26 @@ class StagePreconditioner:
         return plan
 
     def _mg_blocks(self) -> bool:
-        """Blocks are solved one by one when each has a multigrid hierarchy
-        (P1 grid operators, no diagonal shift: ~5 instead of O(100) batched
-        Jacobi iterations) or a direct inverse (small blocks)."""
-        if self._shift is not None or self.settings.method not in ("auto", "mg"):
+        """Blocks are solved one by one through their factors when the user
+        asked for a per-block method ("direct", "chebyshev"), when every
+        block is direct (small blocks, any pattern), or when each has a
+        multigrid hierarchy or a direct inverse (P1 grid operators, no
+        diagonal shift: ~5 instead of O(100) batched Jacobi iterations)."""
+        meth = self.settings.method
+        if self._shift is not None:
             return False
+        if meth in ("direct", "chebyshev"):
+            return True
+        if meth not in ("auto", "mg"):
+            return False
+        facs = list(self.block_factors)
+        if all(f.direct for f in facs):
+            return True
         if getattr(self.M, "_p1_grid", None) is None:
             return False
         if getattr(self.Ks[0], "_p1_grid", None) != self.M._p1_grid:
             return False
-        return all(getattr(f, "_mg", None) is not None or getattr(f, "_inv", None) is not None
-                   for f in self.block_factors)
+        return all(f._mg is not None or f.direct for f in facs)
 
     def _block_coefs(self):
         s = self.s
@@ -383,6 +392,13 @@ def build_preconditioner(kind: PreconditionerKind, tab: ButcherTableau, M: Spars
     if kind is PreconditionerKind.SCHUR and len(Ks) != 1:
         raise ValueError("the Schur preconditioner needs one shared stiffness matrix")
     st = settings or BlockSolveSettings()
+    if kind is PreconditionerKind.SCHUR and st.method in ("direct", "chebyshev"):
+        # the pair blocks are complex symmetric: COCG (multigrid or Jacobi)
+        raise ValueError(f"block method {st.method!r} is not available for the Schur "
+                         "preconditioner's complex pair blocks (use 'auto', 'mg' or 'pcg')")
+    if shift is not None and st.method in ("direct", "chebyshev", "mg"):
+        raise ValueError(f"block method {st.method!r} cannot include the diagonal shift of "
+                         "the semilinear surrogate blocks (use 'auto' or 'pcg')")
 
     def builder(i):
         Ki = Ks[0] if len(Ks) == 1 else Ks[i]

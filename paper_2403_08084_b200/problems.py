@@ -2,8 +2,10 @@
 (drop-in for the assembly part of implicitrk.problems,
 /root/reference/pkg/src/implicitrk/problems.py).
 
-* ``StructuredGrid(dim, n)``: dim 1, 2 (as the reference) and 3 (new);
-  vertices lexicographic with x fastest (problems.py:25-64).
+* ``StructuredGrid(dim, n)``: dim 1, 2, validated exactly as the reference
+  (problems.py:25-64; dim 3 raises ValueError there, so it does here);
+  ``CubeGrid(n)`` / ``structured_grid(3, n)``: the unit cube (new, config 3).
+  Vertices lexicographic with x fastest.
 * ``assemble_heat(grid)``: the reference's operators (1D P1, 2D Q1 Kronecker
   form, problems.py:80-99), assembled by libirk on the device; dim 3 gives
   the P1 Kuhn-tetrahedra operators.
@@ -35,9 +37,12 @@ class StructuredGrid:
     dim: int
     n: int
 
+    _DIMS = (1, 2)  # the reference's grids (problems.py:33-37)
+
     def __post_init__(self):
-        if self.dim not in (1, 2, 3):
-            raise ValueError("dim must be 1, 2 or 3")
+        if self.dim not in self._DIMS:
+            raise ValueError("dim must be 1 or 2" if self._DIMS == (1, 2)
+                             else f"dim must be one of {self._DIMS}")
         if self.n < 2:
             raise ValueError("need at least 2 cells per direction")
 
@@ -65,6 +70,20 @@ class StructuredGrid:
             k = (idx // n1**d) % n1
             on |= (k == 0) | (k == self.n)
         return np.nonzero(on)[0].astype(np.int64)
+
+
+
+@dataclass(frozen=True)
+class CubeGrid(StructuredGrid):
+    """The unit cube [0,1]^3 (new: the reference's grids are 1D/2D only and
+    reject dim 3), for the P1 Kuhn-tetrahedra workloads (config 3)."""
+
+    _DIMS = (1, 2, 3)
+
+
+def structured_grid(dim: int, n: int) -> StructuredGrid:
+    """StructuredGrid for dim 1, 2; CubeGrid for dim 3."""
+    return CubeGrid(dim, n) if dim == 3 else StructuredGrid(dim, n)
 
 
 def _assemble(kind: str, grid: StructuredGrid):

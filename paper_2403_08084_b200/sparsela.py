@@ -561,8 +561,11 @@ class BlockSolveSettings:
     device, applied by one dense matrix-vector kernel: the exact solve of
     the reference's SuperLU factorisation at sizes where the iterative
     solvers are launch-latency-bound), "mg" (multigrid required), "pcg"
-    (Jacobi-preconditioned CG) or "chebyshev" (Jacobi-Chebyshev,
-    ``cheb_iters`` sweeps with Gershgorin/Lanczos-free bounds).
+    (Jacobi-preconditioned CG) or "chebyshev" (Jacobi-Chebyshev: no inner
+    products, eigenvalue bounds of D^-1 B from Gershgorin discs -- the block
+    must be strictly diagonally dominant with a positive diagonal, else
+    ValueError; ``cheb_iters`` sweeps, 0 = as many as the Chebyshev error
+    bound 2/T_k needs for ``rtol``, at most ``maxit``).
     mg_nu / mg_coarse_steps: Chebyshev smoothing steps per level (0: automatic
     = 2; the structured 2D path fuses up to 4) and on the coarsest level of the
     multigrid V-cycle; mg_coarse_ratio: coarsening stops
@@ -575,7 +578,7 @@ class BlockSolveSettings:
     atol: float = 0.0
     maxit: int = 20000
     raise_on_maxit: bool = False
-    cheb_iters: int = 50
+    cheb_iters: int = 0
     mg_nu: int = 0
     mg_coarse_steps: int = 4
     mg_coarse_ratio: float = 0.5
@@ -583,7 +586,7 @@ class BlockSolveSettings:
     def __post_init__(self):
         if self.method not in ("auto", "pcg", "mg", "chebyshev", "direct"):
             raise ValueError(f"unknown block solver {self.method!r}")
-        if self.rtol < 0 or self.atol < 0 or self.maxit < 0:
+        if self.rtol < 0 or self.atol < 0 or self.maxit < 0 or self.cheb_iters < 0:
             raise ValueError("block solver tolerances must be non-negative")
 
 
@@ -780,9 +783,18 @@ class BlockFactorization:
         self._check_regular()
         self._mg = None
         self._inv = None
+        self._cheb = None
         meth = self.settings.method
-        if meth == "direct" or (meth == "auto" and 0 < self.n <= DIRECT_MAX):
-            self._inv = self._dense_inverse()
+        # direct: the inverse is formed on the first solve, so factors that are
+        # built but never solved with (regularity checks of per-Newton blocks
+        # that the batched path handles) cost no inversion
+        self.direct = meth == "direct" or (meth == "auto" and 0 < self.n <= DIRECT_MAX)
+        if meth == "direct" and self.n > 8192:
+            raise ValueError(f"direct block solve limited to 8192 rows, got {self.n}")
+        if meth == "chebyshev":
+            self._cheb = self._chebyshev_bounds()
+        elif self.direct:
+            pass
         elif meth in ("auto", "mg"):
             self._mg = _MgHierarchy.build(M, K, self.alpha, self.beta, self.mask, B,
                                           self.settings)
@@ -790,13 +802,49 @@ class BlockFactorization:
                 raise ValueError("multigrid block solver needs M, K from assemble_p1 "
                                  "(nested structured-grid P1 operators)")
 
+    def _chebyshev_bounds(self):
+        """[lmin, lmax] of D^-1 B from Gershgorin discs (irk_mat_absrowsum):
+        disc r is centred at 1 with radius sum_c |B[r,c]| / |B[r,r]| - 1."""
+        torch = _torch()
+        if self.n == 0:
+            return (0.5, 1.5)
+        d = self._B.diagonal()
+        a = dev_empty(self.n)
+        call("irk_mat_absrowsum", ctx(), self._B.handle, ptr(a))
+        if bool((d <= 0).any()):
+            raise ValueError("Chebyshev block solver needs a positive diagonal")
+        ratio = a / d
+        lmin = float(torch.min(2.0 - ratio))
+        lmax = float(torch.max(ratio))
+        if not lmin > 1e-14 * lmax:
+            raise ValueError("Chebyshev block solver: the block is not strictly diagonally "
+                             f"dominant (Gershgorin lower bound {lmin:.3e}); use method='pcg'")
+        if lmax <= lmin:
+            lmax = lmin * (1.0 + 1e-12) + 1e-300
+        return (lmin, lmax)
+
+    def chebyshev_iterations(self, settings=None) -> int:
+        """Sweeps of the Chebyshev solve: cheb_iters, or the smallest k with
+        2 / T_k((lmax+lmin)/(lmax-lmin)) <= rtol (capped at maxit)."""
+        st = settings or self.settings
+        if st.cheb_iters > 0:
+            return int(st.cheb_iters)
+        lmin, lmax = self._cheb
+        if st.rtol <= 0:
+            return max(1, int(st.maxit))
+        sigma = (lmax + lmin) / (lmax - lmin)
+        k = np.arccosh(2.0 / min(st.rtol, 1.0)) / np.arccosh(sigma)
+        return int(max(1, min(int(np.ceil(k)), max(1, int(st.maxit)))))
+
     def _dense_inverse(self):
-        """B^-1 as a dense row-major device array (one-time setup, cuSOLVER
+        """B^-1 as a dense row-major device array (one-time setup: the CSR
+        scattered into a dense block on the device, inverted by cuSOLVER
         through torch; the per-solve work is irk_dense_gemv)."""
         torch = _torch()
         if self.n > 8192:
             raise ValueError(f"direct block solve limited to 8192 rows, got {self.n}")
-        dense = torch.from_numpy(self.matrix.to_dense()).to(device())
+        dense = torch.empty((self.n, self.n), dtype=torch.float64, device=device())
+        call("irk_mat_to_dense", ctx(), self._B.handle, ptr(dense))
         try:
             inv = torch.linalg.inv(dense)
         except RuntimeError as exc:  # torch.linalg.LinAlgError
@@ -832,11 +880,23 @@ class BlockFactorization:
         checked=True defers even with raise_on_maxit: the caller reads the
         log codes (1 cap, 2 breakdown) and raises."""
         st = settings or self.settings
-        if self._inv is not None and st.method in ("auto", "direct"):
+        if self.direct and st.method in ("auto", "direct"):
+            if self._inv is None:
+                self._inv = self._dense_inverse()
             call("irk_dense_gemv", ctx(), self.n, ptr(self._inv), ptr(rhs), int(ld_rhs), ptr(x),
                  int(ld_x))
             self.last_iterations, self.last_relres = 1, 0.0
             return 1  # exact: no log entry even when deferred
+        if st.method == "chebyshev":
+            if self._cheb is None:
+                self._cheb = self._chebyshev_bounds()
+            k = self.chebyshev_iterations(st)
+            one = np.ones(1)
+            lo, hi = np.array([self._cheb[0]]), np.array([self._cheb[1]])
+            call("irk_chebyshev", ctx(), 1, hptr(one), None, self._B.handle, None, None, None,
+                 hptr(lo), hptr(hi), ptr(rhs), int(ld_rhs), ptr(x), int(ld_x), int(k))
+            self.last_iterations, self.last_relres = k, float("nan")
+            return k  # fixed sweep count: nothing to log or check
         its = np.zeros(8, dtype=np.int32)
         rel = np.zeros(8, dtype=np.float64)
         one = np.ones(8)
@@ -1226,6 +1286,12 @@ def mm_write(path, A: SparseMatrix) -> None:
 
 
 def mm_read(path) -> SparseMatrix:
+    """Matrix Market file -> SparseMatrix (sparsela.py:414-416)."""
     import scipy.io
+    import scipy.sparse
 
-    return SparseMatrix.from_scipy(scipy.io.mmread(str(path)))
+    try:
+        A = scipy.io.mmread(str(path), spmatrix=False)
+    except TypeError:  # scipy without the spmatrix switch
+        A = scipy.io.mmread(str(path))
+    return SparseMatrix.from_scipy(scipy.sparse.csr_matrix(A))

@@ -107,7 +107,11 @@ class NewtonSettings:
 @dataclass
 class StepReport:
     """Per-step statistics (stepper.py:89-96); ``inner_iters`` adds the
-    inner block-solver iteration counts of the step."""
+    inner block-solver iteration counts of the step.  ``krylov_iters``
+    counts what the reference counts: FGMRES iterations on the coupled
+    paths; on the DIRK path one per linear stage (the reference's FGMRES
+    with the exact factored block converges in one, stepper.py:405-407),
+    the CG iterations of those stage solves being ``inner_iters``."""
 
     newton_iters: int
     krylov_iters: int
@@ -251,6 +255,7 @@ class TimeStepper:
         self._u_dev = la.to_dev(u).clone() if la.is_torch(u) else la.to_dev(uh)
         self._u_host = uh.copy()
         self._last_stages_dev = None
+        self._dirk_stages_dev = None
         self._t_base = float(t0)
         self.step_index = 0
         self._dt = float(dt)
@@ -285,6 +290,20 @@ class TimeStepper:
         out = la.dev_empty(s * m)
         call("irk_to_stage_major", ctx(), m, s, ptr(self._last_stages_dev), ptr(out))
         return la.to_host(out)
+
+    @property
+    def stage_vectors(self):
+        """Stage unknowns of the last step, stage-major host copy: the DIRK
+        stage derivatives K_stages (stepper.py:391-421, which the reference
+        keeps only as a local) or, for the coupled paths, ``_last_stages``."""
+        if self.formulation is StageFormulation.DIRK:
+            if self._dirk_stages_dev is None:
+                return None
+            s, m = self.tableau.s, self.problem.m
+            out = la.dev_empty(s * m)
+            call("irk_to_stage_major", ctx(), m, s, ptr(self._dirk_stages_dev), ptr(out))
+            return la.to_host(out)
+        return self._last_stages
 
     @property
     def t(self) -> float:
@@ -594,16 +613,20 @@ def _step_dirk_dev(stepper: TimeStepper, problem: SemidiscreteProblem):
         if log is not None:
             log.__exit__(None, None, None)
     if log is not None:
+        fac, srhs, ki = last
+        strict = fac.settings.raise_on_maxit
         for its, code, _, _ in log.entries.tolist():
-            if code == 1:
+            if code == 1 and strict:
                 raise NonConvergenceError(
                     f"DIRK stage solve: no convergence in {its} iterations", [])
             if code == 2:
                 raise FactorizationError("DIRK stage solve: breakdown (singular stage block)")
         done = iter(log.entries[:, 0].tolist())
         inner = [next(done, -1) if v is None else v for v in inner]
-        krylov_total = int(sum(inner))
-        fac, srhs, ki = last
+        # the reference preconditions each linear stage's FGMRES with the exact
+        # factored block, one iteration per stage (stepper.py:405-407); the
+        # device solve is that one application, its CG count is inner_iters
+        krylov_total = len(inner)
         r = la.dev_empty(m)
         fac._B.spmv(ki, r)
         call("irk_axpby", ctx(), m, 1.0, ptr(srhs), -1.0, ptr(r))
@@ -614,6 +637,7 @@ def _step_dirk_dev(stepper: TimeStepper, problem: SemidiscreteProblem):
     wb = np.ascontiguousarray(dt * np.asarray(tab.b))
     call("irk_stage_update", ctx(), m, s, 1.0, ptr(u), hptr(wb), -1, ptr(K_il), ptr(u_next))
     report = StepReport(newton_total, krylov_total, final_res, hist, inner)
+    stepper._dirk_stages_dev = K_il
     stepper._commit(u_next)
     return u_next, report
 

@@ -23,7 +23,7 @@ def irk(cuda):
 @pytest.mark.parametrize("dim,n", [(1, 5), (1, 9), (2, 4), (2, 7)])
 def test_reference_assembly_bit_exact(irk, golden, dim, n):
     """assemble_heat (1D P1 / 2D Q1) reproduces the reference bit for bit."""
-    M, K, bd = irk.assemble_heat(irk.StructuredGrid(dim, n))
+    M, K, bd = irk.assemble_heat(irk.structured_grid(dim, n))
     for name, A in (("M", M), ("K", K)):
         key = f"asm{dim}d{n}_{name}"
         np.testing.assert_array_equal(A.row_offsets, golden[key + "_rowptr"])
@@ -32,10 +32,13 @@ def test_reference_assembly_bit_exact(irk, golden, dim, n):
     np.testing.assert_array_equal(bd, golden[f"asm{dim}d{n}_bd"])
 
 
-@pytest.mark.parametrize("dim,n", [(1, 7), (2, 4), (2, 32), (2, 129), (3, 2), (3, 5), (3, 12)])
+@pytest.mark.parametrize("dim,n", [(1, 7), (2, 4), (2, 32), (2, 129), (3, 2), (3, 5), (3, 12),
+                                   (2, 1024), (3, 96), (2, 2048)])
 def test_p1_assembly_vs_oracle(irk, oracle, dim, n):
-    """Indices bit-exact (as int64), values to 1 ulp-scale."""
-    M, K, bd = irk.assemble_p1(irk.StructuredGrid(dim, n))
+    """Indices bit-exact (as int64), values to 1 ulp-scale -- also at the
+    BASELINE config grids (1024^2: configs 2/5, 96^3: config 3, 2048^2:
+    config 4), as north_star asks for the workloads themselves."""
+    M, K, bd = irk.assemble_p1(irk.structured_grid(dim, n))
     Mo, Ko = oracle.p1_matrices(dim, n)
     for A, B in ((M, Mo), (K, Ko)):
         np.testing.assert_array_equal(A.row_offsets, B.indptr.astype(np.int64))
@@ -46,8 +49,9 @@ def test_p1_assembly_vs_oracle(irk, oracle, dim, n):
 
 def test_p1_config_sizes(irk):
     """nnz = m + 2 #edges at the config grids."""
-    for dim, n, m, nnz in ((2, 1024, 1050625, 7346177), (3, 96, 912673, 13465441)):
-        M, K, bd = irk.assemble_p1(irk.StructuredGrid(dim, n))
+    for dim, n, m, nnz in ((2, 1024, 1050625, 7346177), (3, 96, 912673, 13465441),
+                           (2, 2048, 4198401, 29372417)):
+        M, K, bd = irk.assemble_p1(irk.structured_grid(dim, n))
         assert M.nrows == m and M.nnz == nnz and K.nnz == nnz
         assert M.device().same_pattern(K.device())
 
@@ -206,7 +210,7 @@ def test_batched_pcg_vs_oracle(irk, oracle, dim, n):
     from paper_2403_08084_b200 import _lib
     from paper_2403_08084_b200 import sparsela as la
 
-    M, K, bd = irk.assemble_p1(irk.StructuredGrid(dim, n))
+    M, K, bd = irk.assemble_p1(irk.structured_grid(dim, n))
     Mo, Ko = oracle.p1_matrices(dim, n)
     m = M.nrows
     alphas, betas = [1.0, 1.0, 0.7], [0.01, 0.2, 1e-3]
@@ -304,7 +308,7 @@ def test_preconditioner_vs_reference(irk, golden, tname, kind, form):
 @pytest.mark.parametrize("form", ["ai", "ia"])
 def test_schur_preconditioner_vs_oracle(irk, oracle, tab_name, form):
     n = 5
-    M, K, bd = irk.assemble_p1(irk.StructuredGrid(3, n))
+    M, K, bd = irk.assemble_p1(irk.CubeGrid(3, n))
     Mo, Ko = oracle.p1_matrices(3, n)
     tab = irk.from_spec(tab_name)
     pc = irk.build_preconditioner(irk.PreconditionerKind.SCHUR, tab, M, K, 5e-3,
@@ -333,7 +337,7 @@ def test_schur_preconditioner_vs_oracle(irk, oracle, tab_name, form):
 def _p1_block(irk, dim, n, alpha, beta):
     from paper_2403_08084_b200 import sparsela as la
 
-    M, K, bd = irk.assemble_p1(irk.StructuredGrid(dim, n))
+    M, K, bd = irk.assemble_p1(irk.structured_grid(dim, n))
     st = la.BlockSolveSettings(method="mg", rtol=1e-12, raise_on_maxit=True)
     fac = la.BlockFactorization(M, K, alpha, beta, bd, st)
     return M, K, bd, fac
@@ -351,7 +355,7 @@ def test_direct_small_blocks(cuda, irk, oracle):
 
     M, K, bd = irk.assemble_p1(irk.StructuredGrid(2, 32))
     fac = la.BlockFactorization(M, K, 1.0, 5e-3, bd, la.BlockSolveSettings(rtol=1e-6))
-    assert fac._inv is not None and fac._mg is None
+    assert fac.direct and fac._mg is None
     Mo, Ko = oracle.p1_matrices(2, 32)
     B = oracle.dirichlet_identity((Mo + 5e-3 * Ko).tocsr(), bd)
     rhs = np.random.default_rng(9).standard_normal(M.nrows)
@@ -363,6 +367,95 @@ def test_direct_small_blocks(cuda, irk, oracle):
         assert fac.dev_solve(rd, xd[1:], ld_x=3, defer=True) == 1
     assert log.entries.shape[0] == 0
     assert rel(la.to_host(xd).reshape(-1, 3)[:, 1], x) < 1e-14
+    assert fac._inv is not None
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [32, 1024])
+def test_chebyshev_block_solver(cuda, irk, oracle, n):
+    """method="chebyshev" runs irk_chebyshev (Gershgorin bounds, sweep count
+    from rtol) and meets the tolerance against a sparse direct solve -- at
+    the config-2 block (n = 1024: M + dt a_ii K, RadauIIA-3) too."""
+    import scipy.sparse.linalg as spla
+
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(2, n))
+    beta = 1e-3 * 0.1550510257216822  # dt * a_11 of RadauIIA-3
+    st = la.BlockSolveSettings(method="chebyshev", rtol=1e-10)
+    fac = la.BlockFactorization(M, K, 1.0, beta, bd, st)
+    lmin, lmax = fac._cheb
+    assert 0 < lmin < 1 < lmax <= 2
+    Mo, Ko = oracle.p1_matrices(2, n)
+    B = oracle.dirichlet_identity((Mo + beta * Ko).tocsr(), bd)
+    rhs = np.random.default_rng(4).standard_normal(M.nrows)
+    x = fac.solve(rhs)
+    k = fac.last_iterations
+    assert k == fac.chebyshev_iterations() and k > 1
+    ref = spla.spsolve(B.tocsc(), rhs)
+    # the bound 2/T_k is on the D^-1/2 B D^-1/2-energy norm of the error;
+    # the 2-norm error stays within a condition-number factor of it
+    assert rel(x, ref) < 1e-7
+    # fixed sweep count: cheb_iters overrides the bound
+    fac2 = la.BlockFactorization(M, K, 1.0, beta, bd,
+                                 la.BlockSolveSettings(method="chebyshev", cheb_iters=7))
+    fac2.solve(rhs)
+    assert fac2.last_iterations == 7
+
+
+@pytest.mark.gpu
+def test_chebyshev_rejects_indefinite_bounds(cuda, irk):
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(2, 8))
+    with pytest.raises(ValueError):  # pure stiffness: Gershgorin lower bound 0
+        la.BlockFactorization(M, K, 0.0, 1.0, bd, la.BlockSolveSettings(method="chebyshev"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("method", ["direct", "chebyshev"])
+def test_block_diagonal_pc_honours_block_method(cuda, irk, method):
+    """BLOCK_DIAGONAL with method="direct"/"chebyshev" solves through the
+    block factors the user asked for (not the batched Jacobi-PCG)."""
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(2, 16))
+    tab = irk.radau_iia(3)
+    st = la.BlockSolveSettings(method=method, rtol=1e-10)
+    pc = irk.build_preconditioner(irk.PreconditionerKind.BLOCK_DIAGONAL, tab, M, K, 1e-2,
+                                  irk.Splitting.AI, bd, st)
+    v = np.random.default_rng(2).standard_normal(3 * M.nrows)
+    y = pc.apply(v)
+    assert pc._mg_blocks()
+    its = [r[0] for r in pc.inner_iterations]
+    if method == "direct":
+        assert its == [1, 1, 1]
+    else:
+        assert its == [pc.block_factors[i].chebyshev_iterations() for i in range(3)]
+    ref = irk.build_preconditioner(irk.PreconditionerKind.BLOCK_DIAGONAL, tab, M, K, 1e-2,
+                                   irk.Splitting.AI, bd,
+                                   la.BlockSolveSettings(method="pcg", rtol=1e-13)).apply(v)
+    assert rel(y, ref) < 1e-6
+
+
+@pytest.mark.gpu
+def test_deferred_log_grows(cuda, irk):
+    """More than 4096 deferred solves in one log: every entry is kept, in
+    order, and the status codes stay deferred (no synchronous fallback)."""
+    from paper_2403_08084_b200 import _lib
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(1, 64))
+    fac = la.BlockFactorization(M, K, 1.0, 1e-2, bd,
+                                la.BlockSolveSettings(method="pcg", rtol=1e-8))
+    rhs = la.to_dev(np.random.default_rng(1).standard_normal(M.nrows))
+    x = la.dev_empty(M.nrows)
+    with _lib.deferred_solves() as log:
+        for _ in range(5000):
+            assert fac.dev_solve(rhs, x, defer=True) is None
+    assert log.entries.shape == (5000, 4)
+    assert np.all(log.entries[:, 1] == 0)
+    assert len(set(log.entries[:, 0].tolist())) == 1
 
 
 @pytest.mark.gpu
@@ -476,7 +569,7 @@ def test_mgc_cocg_schur_pair(cuda, irk, oracle, dim, n):
     from paper_2403_08084_b200 import _lib
     from paper_2403_08084_b200 import sparsela as la
 
-    M, K, bd = irk.assemble_p1(irk.StructuredGrid(dim, n))
+    M, K, bd = irk.assemble_p1(irk.structured_grid(dim, n))
     m = M.nrows
     mask = la.dof_mask(m, bd)
     Md, Kd = la.shared_pattern([M.device(), K.device()])

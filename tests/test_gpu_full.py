@@ -34,7 +34,11 @@ def test_full_config_parity(cuda, oracle, k):
     st, prob = wl.stepper, wl.problem
     key = f"traj{k}_n{configs.GRID[k][1]}"
     P = oracle.sketch_rows(prob.m)
-    Ps = oracle.sketch_rows(prob.m * st.tableau.s, seed=77) if f"{key}_x0_proj" in g.files else None
+    s = st.tableau.s
+    assert f"{key}_x0_proj" in g.files, "the golden must record the stage vectors"
+    # DIRK (config 4): per-stage projections (an s*m Gaussian sketch is 3 GB)
+    per_stage = g[f"{key}_x0_proj"].ndim == 2
+    Ps = oracle.sketch_rows(prob.m if per_stage else prob.m * s, seed=77)
     worst_u = worst_x = 0.0
     for i in range(wl.steps):
         st.step_device(prob)
@@ -43,14 +47,17 @@ def test_full_config_parity(cuda, oracle, k):
         eu = max(np.linalg.norm(proj - g[f"{key}_u{i}_proj"]) / np.linalg.norm(g[f"{key}_u{i}_proj"]),
                  np.linalg.norm(samp - g[f"{key}_u{i}_sample"]) / np.linalg.norm(g[f"{key}_u{i}_sample"]))
         worst_u = max(worst_u, eu)
-        if Ps is not None and f"{key}_x{i}_proj" in g.files:
-            x = st._last_stages
-            px = Ps @ x
-            worst_x = max(worst_x, np.linalg.norm(px - g[f"{key}_x{i}_proj"])
-                          / np.linalg.norm(g[f"{key}_x{i}_proj"]))
+        x = st.stage_vectors
+        gx = g[f"{key}_x{i}_proj"]
+        px = np.stack([Ps @ xi for xi in x.reshape(s, -1)]) if per_stage else Ps @ x
+        ex = np.linalg.norm(px - gx) / np.linalg.norm(gx)
+        if f"{key}_x{i}_sample" in g.files:
+            gs = g[f"{key}_x{i}_sample"]
+            ex = max(ex, np.linalg.norm(x[:: max(1, len(x) // 4096)] - gs) / np.linalg.norm(gs))
+        worst_x = max(worst_x, ex)
     print(f"config {k}: worst state rel L2 {worst_u:.3e}, worst stage-vector rel L2 {worst_x:.3e}")
     assert worst_u < 1e-9
-    assert worst_x < 1e-9
+    assert 0.0 < worst_x < 1e-9
 
 
 def test_full_size_properties(cuda):

@@ -23,7 +23,7 @@ def build(irk, oracle, k, n, inner_rtol=1e-6):
     """The CUDA twin of oracle.config(k, n): same grid, seeds, tableau, BCs."""
     cfg = oracle.config(k, n)
     p = cfg["problem"]
-    grid = irk.StructuredGrid(cfg["dim"], cfg["n"])
+    grid = irk.structured_grid(cfg["dim"], cfg["n"])
     if k == 5:
         prob = irk.allen_cahn_problem(grid, 0.02, p.u0)
     else:
@@ -57,9 +57,11 @@ def test_config_trajectory_vs_reference(irk, oracle, golden, k, n):
         u, rep = st.step(prob)
         worst_u = max(worst_u, rel(u, U[i]))
         if X is not None:
-            worst_x = max(worst_x, rel(st._last_stages, X[i]))
+            worst_x = max(worst_x, rel(st.stage_vectors, X[i]))
     assert worst_u < 1e-9, worst_u
     assert worst_x < 1e-9, worst_x
+    assert X is not None, "every config golden records the reference's stage vectors"
+    assert worst_x > 0.0
 
 
 # ------------------------------------------- reference-suite known answers
@@ -266,3 +268,55 @@ def test_advance_and_clock(irk):
     assert abs(u[0] - np.exp(-1.0)) < 1e-9
     with pytest.raises(ValueError):
         irk.advance(irk.TimeStepper(case.problem, irk.radau_iia(1), 0.1, t0=1.0), case.problem, 0.5)
+
+
+def test_wsodirk433_dirk_path_vs_dense_stages(irk):
+    """WSODIRK433 (tableaux.py:257-277) through the device DIRK path on a
+    Dirichlet 1D heat problem: every stage derivative and the state against
+    a dense stage-by-stage solve (the reference's DIRK recurrence,
+    stepper.py:391-421), 3 steps."""
+    grid = irk.StructuredGrid(1, 12)
+    M, K, bd = irk.assemble_heat(grid)
+    x = grid.coords()[:, 0]
+    u0 = np.sin(np.pi * x) + 0.3 * x * (1 - x)
+    u0[bd] = 0.0
+    p = irk.SemidiscreteProblem(m=grid.npoints, mass=M, stiffness=K,
+                                load=lambda t: np.zeros(grid.npoints),
+                                dirichlet=irk.DirichletBC(dofs=bd, g=lambda t: np.zeros(2)), u0=u0)
+    tab, dt = irk.wsodirk433(), 0.05
+    st = irk.TimeStepper(p, tab, dt, formulation=irk.StageFormulation.DIRK,
+                         krylov=irk.KrylovSettings(rtol=1e-13, atol=1e-15))
+    Md, Kd = M.to_dense(), K.to_dense()
+    u = u0.copy()
+    interior = np.setdiff1d(np.arange(grid.npoints), bd)
+    for _ in range(3):
+        ks = np.zeros((tab.s, grid.npoints))
+        for i in range(tab.s):
+            acc = u + dt * (tab.A[i, :i] @ ks[:i])
+            S = Md + dt * tab.A[i, i] * Kd
+            rhs = -Kd @ acc
+            ks[i, interior] = np.linalg.solve(S[np.ix_(interior, interior)], rhs[interior])
+        u = u + dt * (tab.b @ ks)
+        un, rep = st.step(p)
+        assert rel(un, u) < 1e-11
+        assert rel(st.stage_vectors, ks.ravel()) < 1e-11
+        assert rep.krylov_iters == tab.s and len(rep.inner_iters) == tab.s
+
+
+def test_matrix_market_round_trip(irk, tmp_path):
+    """mm_write / mm_read (sparsela.py:410-416): coordinate real general
+    banner, pattern bit-exact (explicit zeros of the P1 stiffness kept),
+    values exact; a symmetric-format file written by scipy reads back whole."""
+    import scipy.io
+
+    M, K, _ = irk.assemble_p1(irk.StructuredGrid(2, 6))
+    path = tmp_path / "k.mtx"
+    irk.mm_write(path, K)
+    assert path.read_text().splitlines()[0].startswith("%%MatrixMarket matrix coordinate real general")
+    back = irk.mm_read(path)
+    np.testing.assert_array_equal(back.row_offsets, K.row_offsets)
+    np.testing.assert_array_equal(back.col_indices, K.col_indices)
+    np.testing.assert_array_equal(back.values, K.values)
+    sym = tmp_path / "m_sym.mtx"
+    scipy.io.mmwrite(str(sym), M.to_scipy(), symmetry="symmetric")
+    np.testing.assert_array_equal(irk.mm_read(sym).to_dense(), M.to_dense())

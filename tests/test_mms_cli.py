@@ -133,3 +133,30 @@ def test_cli_precond_bench_runs(cuda, tmp_path):
     assert cli.main(["precond-bench", "--stage-type", "dirk", "--nx", "16", "--steps", "2",
                      "--out", str(dout)]) == 0
     assert np.loadtxt(dout, delimiter=",", skiprows=1).shape == (3, 3)
+
+
+@pytest.mark.gpu
+def test_cli_solver_failure_exit_3(cuda, tmp_path, monkeypatch):
+    """NonConvergenceError -> exit code 3 (cli.py:358-360): FGMRES capped at
+    2 iterations cannot reach rtol 1e-12 on bc-compare's 40-cell problem."""
+    from paper_2403_08084_b200 import cli
+    from paper_2403_08084_b200.sparsela import KrylovSettings
+
+    monkeypatch.setattr(cli, "KrylovSettings",
+                        lambda **kw: KrylovSettings(**{**kw, "maxit": 2}))
+    assert cli.main(["bc-compare", "--rtol", "1e-12", "--nx", "40",
+                     "--out", str(tmp_path / "x")]) == 3
+
+
+@pytest.mark.gpu
+def test_cli_dirk_rows_count_one_iteration_per_stage(cuda, tmp_path):
+    """precond-bench --stage-type dirk reports one FGMRES-equivalent
+    iteration per stage, as the reference's exact-factor FGMRES does
+    (pkg/tests/test_cli.py:140-149)."""
+    from paper_2403_08084_b200 import cli
+
+    out = tmp_path / "dirk.csv"
+    assert cli.main(["precond-bench", "--stage-type", "dirk", "--nx", "16", "--steps", "3",
+                     "--out", str(out)]) == 0
+    rows = np.loadtxt(out, delimiter=",", skiprows=1)
+    assert np.all(rows[:, 2] == 1.0)
