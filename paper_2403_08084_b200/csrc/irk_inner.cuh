@@ -1289,7 +1289,43 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
       getenv("IRK_CG_PREFIX") ? std::max(0, atoi(getenv("IRK_CG_PREFIX")) & ~1) : 4;
   static const bool while_off = getenv("IRK_NO_WHILE") != nullptr;  // A/B: chunked graphs
   const int prefix = (prec && maxit > 0 && !graph_off && !while_off) ? prefix_env : 0;
-  {
+  // The key holds every launch argument of the loop kernels.
+  GraphKey key;
+  key.add((const void*)&k_cg_spmv<T, NB, HASB, MAXW>).add((const void*)&k_cg_update<T, NB>);
+  key.add(stencil).add(stencil_n).add(n_ext);
+  key.add(m).add(G).add(A).add(P).add(shift).add(mask).add(w).add(red);
+  key.add(maxit).add(prec ? prec->uid : (uint64_t)0);
+  int64_t body_kernels = 0;  // kernels per pass of the graph-resident loop
+  // CG iterations per WHILE pass: even, so every pass starts on parity 0
+  static const int body_its =
+      getenv("IRK_WHILE_BODY") ? 2 * std::max(1, atoi(getenv("IRK_WHILE_BODY")) / 2) : 2;
+  auto while_body = [&](cudaStream_t cs, cudaGraphConditionalHandle h) -> int {
+    // body_its is even: the loop kernels alternate the two state parities
+    IRK_TRY(chunk_body(cs, 0, body_its));
+    launch(k_cg_cond<T>, 1, 32, 0, cs, h, st0, st1);
+    IRK_CHECK_LAUNCH(ctx);
+    return IRK_OK;
+  };
+  static const bool split_while = getenv("IRK_SPLIT_WHILE") != nullptr;  // A/B: two graphs
+  bool looped = false;
+  if (maxit > 0 && !graph_off && !while_off && !split_while) {
+    // init + the first `prefix` iterations + the conditional WHILE loop in
+    // ONE graph (no second graph launch per solve)
+    GraphKey kc;
+    kc.add((const void*)&k_cg_init<T, NB, HASB>).add(m).add(G).add(A).add(P).add(shift);
+    kc.add(mask).add(w).add(red).add(cnt).add(rtol).add(atol);
+    kc.add(prec ? prec->uid : (uint64_t)0).add(prefix).add(stencil).add(maxit).add(n_ext);
+    kc.k += key.k;
+    kc.add(2).add(body_its);
+    IRK_TRY(graph_launch_prefix_while(
+        ctx, kc.k,
+        [&](cudaStream_t cs) -> int {
+          IRK_TRY(init_body(cs));
+          return chunk_body(cs, 0, prefix);
+        },
+        while_body, &body_kernels));
+    looped = true;
+  } else {
     GraphKey ki;
     ki.add((const void*)&k_cg_init<T, NB, HASB>).add(m).add(G).add(A).add(P).add(shift);
     ki.add(mask).add(w).add(red).add(cnt).add(rtol).add(atol);
@@ -1307,30 +1343,16 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
       }));
     }
   }
-  // The key holds every launch argument of the loop kernels.
-  GraphKey key;
-  key.add((const void*)&k_cg_spmv<T, NB, HASB, MAXW>).add((const void*)&k_cg_update<T, NB>);
-  key.add(stencil).add(stencil_n).add(n_ext);
-  key.add(m).add(G).add(A).add(P).add(shift).add(mask).add(w).add(red);
-  key.add(maxit).add(prec ? prec->uid : (uint64_t)0);
-  int64_t body_kernels = 0;  // kernels per pass of the graph-resident loop
-  if (maxit > 0 && !graph_off && !while_off) {
+  if (looped) {
+    // init, prefix and loop went out as one graph above
+  } else if (maxit > 0 && !graph_off && !while_off) {
     // The whole iteration loop is ONE graph: a conditional WHILE node whose
     // body runs two iterations (both parities) and then sets the loop
     // condition from the device state; termination never returns to the
     // host.  The body's kernels do nothing once the state is finished.
     GraphKey kw = key;
-    kw.add(1);
-    IRK_TRY(graph_launch_while(
-        ctx, kw.k,
-        [&](cudaStream_t cs, cudaGraphConditionalHandle h) -> int {
-          static const int body_its = getenv("IRK_WHILE_BODY") ? atoi(getenv("IRK_WHILE_BODY")) : 2;
-          IRK_TRY(chunk_body(cs, 0, body_its));
-          launch(k_cg_cond<T>, 1, 32, 0, cs, h, st0, st1);
-          IRK_CHECK_LAUNCH(ctx);
-          return IRK_OK;
-        },
-        &body_kernels));
+    kw.add(1).add(body_its);
+    IRK_TRY(graph_launch_while(ctx, kw.k, while_body, &body_kernels));
   } else {
     // Chunked issue with one chunk in flight ahead of the host check; full
     // chunks replay a cached CUDA graph (host launch cost once per chunk).

@@ -86,7 +86,8 @@ struct irk_ctx {
   struct GraphEntry {
     std::string key;
     cudaGraphExec_t exec;
-    int64_t kernels;
+    int64_t kernels;          // per launch (straight-line part)
+    int64_t body_kernels = 0;  // per pass of a conditional WHILE body
   };
   std::vector<GraphEntry> graphs;
   cudaStream_t cap_stream = nullptr;
@@ -253,6 +254,96 @@ int graph_launch_while(irk_ctx* ctx, const std::string& key, F&& body,
   ctx->graphs.push_back({key, exec, ctx->launches - l0});
   ctx->launches = l0;  // counted per executed body pass by the caller
   if (body_kernels) *body_kernels = ctx->graphs.back().kernels;
+  IRK_CUDA(cudaGraphLaunch(exec, ctx->stream));
+  return IRK_OK;
+}
+
+// One graph = a straight-line prefix `pre(stream)` followed by a conditional
+// WHILE node whose body is `body(stream, handle)`.  Replaces a prefix graph
+// launch + a separate WHILE-graph launch: measured on B200 inside the
+// multigrid-PCG solves, the second launch cost ~150 us of GPU idle per solve
+// (profiles/r02), a sequence in one graph costs a few us.  Cached like
+// graph_launch; the prefix kernels are counted per launch, *body_kernels
+// receives the kernel count of one body pass.
+template <class F, class B>
+int graph_launch_prefix_while(irk_ctx* ctx, const std::string& key, F&& pre, B&& body,
+                              int64_t* body_kernels) {
+  for (auto& g : ctx->graphs) {
+    if (g.key == key) {
+      IRK_CUDA(cudaGraphLaunch(g.exec, ctx->stream));
+      ctx->launches += g.kernels;
+      *body_kernels = g.body_kernels;
+      return IRK_OK;
+    }
+  }
+  if (!ctx->cap_stream)
+    IRK_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+  cudaGraph_t graph = nullptr;
+  IRK_CUDA(cudaGraphCreate(&graph, 0));
+  const int64_t l0 = ctx->launches;
+  cudaError_t e = cudaStreamBeginCaptureToGraph(ctx->cap_stream, graph, nullptr, nullptr, 0,
+                                                cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    IRK_CUDA(e);
+  }
+  int rc = pre(ctx->cap_stream);
+  // the conditional node joins the capture after the prefix's sink nodes
+  cudaGraphConditionalHandle h{};
+  cudaGraphNode_t node = nullptr;
+  cudaGraph_t bodyg = nullptr;
+  if (rc == IRK_OK) {
+    cudaStreamCaptureStatus cst;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    e = cudaStreamGetCaptureInfo(ctx->cap_stream, &cst, nullptr, nullptr, &deps, &ndeps);
+    if (e == cudaSuccess)
+      e = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    if (e == cudaSuccess) e = cudaGraphAddNode(&node, graph, deps, ndeps, &np);
+    if (e == cudaSuccess) {
+      bodyg = np.conditional.phGraph_out[0];
+      e = cudaStreamUpdateCaptureDependencies(ctx->cap_stream, &node, 1,
+                                              cudaStreamSetCaptureDependencies);
+    }
+  }
+  cudaGraph_t got = nullptr;
+  const cudaError_t ee = cudaStreamEndCapture(ctx->cap_stream, &got);
+  if (rc != IRK_OK || e != cudaSuccess || ee != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    if (rc != IRK_OK) return rc;
+    IRK_CUDA(e != cudaSuccess ? e : ee);
+  }
+  const int64_t pre_kernels = ctx->launches - l0;
+  e = cudaStreamBeginCaptureToGraph(ctx->cap_stream, bodyg, nullptr, nullptr, 0,
+                                    cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    IRK_CUDA(e);
+  }
+  rc = body(ctx->cap_stream, h);
+  e = cudaStreamEndCapture(ctx->cap_stream, &got);
+  if (rc != IRK_OK || e != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    if (rc != IRK_OK) return rc;
+    IRK_CUDA(e);
+  }
+  const int64_t bk = ctx->launches - l0 - pre_kernels;
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  IRK_CUDA(e);
+  if (ctx->graphs.size() >= 64) {
+    cudaGraphExecDestroy(ctx->graphs.front().exec);
+    ctx->graphs.erase(ctx->graphs.begin());
+  }
+  ctx->graphs.push_back({key, exec, pre_kernels, bk});
+  ctx->launches = l0 + pre_kernels;  // body passes are counted by the caller
+  *body_kernels = bk;
   IRK_CUDA(cudaGraphLaunch(exec, ctx->stream));
   return IRK_OK;
 }
