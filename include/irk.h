@@ -261,6 +261,32 @@ int irk_dot(irk_ctx* ctx, int64_t n, const double* x_dev, const double* y_dev, d
 /* 1 if every entry is finite (synchronous). */
 int irk_all_finite(irk_ctx* ctx, int64_t n, const double* x_dev, int* result_host);
 
+/* ------------------------------------------ device-resident FGMRES cycle
+ * The Arnoldi loop of fgmres (sparsela.py:355-403) without a host round trip
+ * per iteration: one CUDA graph runs a whole restart cycle (a conditional
+ * WHILE node; Givens rotations and the stop tests on the device).
+ * step_graph (a cudaGraph_t, cloned) computes w from v_j on fixed buffers:
+ * right preconditioning z_j = P v_j, w = A z_j (Z != NULL: Z_j = z_j is
+ * stored), or w = A v_j (Z == NULL, the solution update uses V).  work
+ * holds irk_fgmres_work_doubles(cycle) doubles, st_dev 8 ints.  The graph
+ * bakes in the context scratch: irk_fgmres_graph_run fails with
+ * IRK_EINVAL if that scratch was reallocated since (re-create it).
+ * irk_fgmres_graph_run: one cycle of at most cap <= cycle steps from the
+ * residual r (beta = ||r||): V_0 = r / beta, ..., x += Z y; writes the
+ * steps taken, the convergence flag (residual <= target or breakdown
+ * h_{j+1,j} < breakdown) and the residual estimates hist[0..k]
+ * (synchronous). */
+typedef struct irk_fgraph irk_fgraph;
+size_t irk_fgmres_work_doubles(int cycle);
+int irk_fgmres_graph_create(irk_ctx* ctx, void* step_graph, int64_t n, int cycle, int reorth,
+                            double* V, int64_t ldv, double* Z, int64_t ldz, double* vj,
+                            const double* zj, double* w, double* work, int* st_dev,
+                            irk_fgraph** out);
+int irk_fgmres_graph_run(irk_ctx* ctx, irk_fgraph* fg, int cap, const double* r, double beta,
+                         double target, double breakdown, double* x, int* k_host,
+                         int* conv_host, double* hist_host);
+int irk_fgmres_graph_destroy(irk_fgraph* fg);
+
 /* ------------------------------------------------------ inner block solves
  * Jacobi-preconditioned CG on nb independent SPD systems stored interleaved
  * (m-by-nb).  System k is

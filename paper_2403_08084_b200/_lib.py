@@ -101,11 +101,17 @@ _SIGS = {
     "irk_mgc_cocg": [_vp, _vp, _vp, _i64, _vp, _i64, _dbl, _dbl, _int, _vp, _vp],
     "irk_mg_info": [_vp, _vp, _vp],
     "irk_mg_pcg": [_vp, _vp, _vp, _i64, _vp, _i64, _dbl, _dbl, _int, _vp, _vp],
+    "irk_fgmres_work_doubles": [_int],
+    "irk_fgmres_graph_create": [_vp, _vp, _i64, _int, _int, _vp, _i64, _vp, _i64, _vp, _vp, _vp,
+                                _vp, _vp, C.POINTER(_vp)],
+    "irk_fgmres_graph_run": [_vp, _vp, _int, _vp, _dbl, _dbl, _dbl, _vp, _vp, _vp, _vp],
+    "irk_fgmres_graph_destroy": [_vp],
 }
 _RESTYPES = {
     "irk_last_error": C.c_char_p,
     "irk_version": C.c_char_p,
     "irk_ctx_launch_count": C.c_int64,
+    "irk_fgmres_work_doubles": C.c_size_t,
 }
 
 EXPORTED = tuple(_SIGS)

@@ -125,6 +125,8 @@ class StagePreconditioner:
         self._schur = None
         self.inner_iterations = []
         self.defer_solves = False  # set by the stepper around deferred_solves
+        self._serial = next(la._SERIAL)
+        self._last_apply = []  # inner_iterations entries of the latest apply
 
     # ------------------------------------------------------------ helpers
     def mask(self):
@@ -230,6 +232,7 @@ class StagePreconditioner:
         # it, so X needs no zeroing
         order, coefs = self._sweep_plan()
         tmp = la.dev_empty(m)
+        n0 = len(self.inner_iterations)
         for i in order:
             coef = coefs[i]
             if coef is not None:
@@ -244,8 +247,20 @@ class StagePreconditioner:
             st = fac.dev_solve(tmp, xi, ld_rhs=1, ld_x=s, settings=self.settings,
                                defer=self.defer_solves)
             self.inner_iterations.append([st])
+        self._last_apply = self.inner_iterations[n0:]
         return X
 
+    def _graph_key(self):
+        """Identity of a capturable application (graph-replayed inside the
+        device FGMRES cycles): the sequential sweep over blocks solved by a
+        fixed kernel sequence (direct inverses, fixed-sweep Chebyshev)."""
+        if self.kind is PreconditionerKind.SCHUR or self._shift is not None:
+            return None
+        if not self._mg_blocks():
+            return None
+        if not all(f.graph_safe(self.settings) for f in self.block_factors):
+            return None
+        return ("pc", self._serial)
     def _schur_plan(self):
         if self._schur is not None:
             return self._schur
@@ -358,6 +373,12 @@ class StagePreconditioner:
 
             def dev_apply(self, x, out):
                 pc.dev_apply(x, out)
+
+            def graph_key(self):
+                return pc._graph_key()
+
+            def account(self, applications):
+                pc.inner_iterations.extend(list(pc._last_apply) * applications)
 
         return _Op()
 

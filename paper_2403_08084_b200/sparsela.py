@@ -25,6 +25,11 @@ from dataclasses import dataclass
 from enum import Enum
 
 import ctypes as C
+import gc
+import itertools
+import os
+from collections import OrderedDict
+
 import numpy as np
 
 from . import _lib
@@ -170,13 +175,17 @@ def _like_input(dev_result, like):
 # ------------------------------------------------------------ device matrix
 
 
+_SERIAL = itertools.count(1)  # identities of device objects in graph keys
+
+
 class DeviceMatrix:
     """Owner of one libirk irk_mat (CSR + SELL-32, float64 values)."""
 
-    __slots__ = ("handle", "nrows", "ncols", "nnz", "_ccache", "__weakref__")
+    __slots__ = ("handle", "nrows", "ncols", "nnz", "_ccache", "serial", "__weakref__")
 
     def __init__(self, handle: C.c_void_p):
         self.handle = handle
+        self.serial = next(_SERIAL)  # graph-key identity (handles are reused addresses)
         self._ccache = {}
         r, c, z = C.c_int64(), C.c_int64(), C.c_int64()
         call("irk_mat_info", handle, C.byref(r), C.byref(c), C.byref(z))
@@ -475,6 +484,17 @@ class _DevOp:
     def dev_apply(self, x, out):  # pragma: no cover - interface
         raise NotImplementedError
 
+    def graph_key(self):
+        """Hashable identity of the exact kernel launches ``dev_apply`` makes
+        (fixed device objects and scalars, no host synchronisation), so that
+        one application can be captured in a CUDA graph and replayed; None
+        when it cannot (host callbacks, iterative solves that poll)."""
+        return None
+
+    def account(self, applications: int) -> None:
+        """Book-keeping of ``applications`` replays of a captured
+        application (the inner iteration counts a direct call records)."""
+
 
 class _SpmvOp(_DevOp):
     def __init__(self, A: SparseMatrix):
@@ -484,6 +504,9 @@ class _SpmvOp(_DevOp):
 
     def dev_apply(self, x, out):
         self._dm.spmv(x, out)
+
+    def graph_key(self):
+        return ("spmv", self._dm.serial)
 
 
 class _HostCallbackOp(_DevOp):
@@ -777,6 +800,7 @@ class BlockFactorization:
         if self.mask is not None:
             B = B.constrain(self.mask, 1.0)
         self._B = B
+        self._serial = next(_SERIAL)
         self._matrix = None
         self.last_iterations = 0
         self.last_relres = 0.0
@@ -945,6 +969,12 @@ class BlockFactorization:
         self._B.spmv(xd, y)
         return _like_input(y, x)
 
+    def graph_safe(self, settings: BlockSolveSettings | None = None) -> bool:
+        """dev_solve is a fixed kernel sequence without host synchronisation
+        (direct inverse or fixed-sweep Chebyshev): capturable in a graph."""
+        meth = (settings or self.settings).method
+        return (self.direct and meth in ("auto", "direct")) or meth == "chebyshev"
+
     def _dev_op(self):
         fac = self
 
@@ -953,6 +983,9 @@ class BlockFactorization:
 
             def dev_apply(self, x, out):
                 fac.dev_solve(x, out)
+
+            def graph_key(self):
+                return ("fac", fac._serial) if fac.graph_safe() else None
 
         return _Op()
 
@@ -1025,6 +1058,12 @@ class KroneckerStageOperator:
 
             def dev_apply(self, x, out):
                 op.dev_apply(x, out, mask)
+
+            def graph_key(self):
+                mats = [d.eliminated(mask) for d in op._device_mats()]
+                return ("kron", op.s, op.C1.tobytes(), op.C2.tobytes(), op.dt,
+                        tuple(d.serial for d in mats),
+                        mask.data_ptr() if mask is not None else 0)
 
         return _Op()
 
@@ -1123,6 +1162,118 @@ def _ev_rec():
     return e
 
 
+# ------------------------------------------- device-resident FGMRES cycles
+# Systems of at most this many unknowns whose operator and preconditioner
+# are graph-capturable run each restart cycle as ONE CUDA graph (libirk
+# irk_fgmres_graph_*: Arnoldi, Givens and the stop tests on the device);
+# larger ones keep the host Givens loop (its per-iteration round trip is a
+# small share of their iteration).  Env IRK_NO_DEVFGMRES: always the host loop.
+DEVFG_MAX_N = 1 << 16
+_DEVFG_OFF = bool(os.environ.get("IRK_NO_DEVFGMRES"))
+_FG_CACHE: "OrderedDict[tuple, _FgmresGraph]" = OrderedDict()
+_FG_SEEN: dict = {}
+
+
+class _FgmresGraph:
+    """Cached cycle graph for one (operator, preconditioner, n, restart):
+    the application w = A P v_j is captured once with torch.cuda.graph on
+    fixed buffers and embedded in libirk's WHILE-loop graph."""
+
+    def __init__(self, A: _DevOp, P: _DevOp | None, n: int, cycle: int, reorth: bool):
+        torch = _torch()
+        lib = _lib.load()
+        self.n, self.cycle, self.P = n, cycle, P
+        self.V = dev_empty((cycle + 1) * n)
+        self.Z = dev_empty(cycle * n) if P is not None else None
+        self.vj = dev_zeros(n)
+        self.zj = dev_zeros(n) if P is not None else None
+        self.w = dev_empty(n)
+        self.work = dev_zeros(int(lib.irk_fgmres_work_doubles(cycle)))
+        self.st = torch.zeros(8, dtype=torch.int32, device="cuda")
+        self.hist = np.zeros(cycle + 1)
+        self.k = C.c_int(0)
+        self.conv = C.c_int(0)
+        self.handle = None
+        self._step(A)  # lazy set-up (inverses, eliminated matrices) outside the capture
+        torch.cuda.synchronize()
+        self.tg = torch.cuda.CUDAGraph(keep_graph=True)
+        # no garbage collection inside the capture: a finalizer freeing device
+        # memory (cudaFree) would invalidate it
+        was = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.graph(self.tg, capture_error_mode="thread_local"):
+                self._step(A)
+        finally:
+            if was:
+                gc.enable()
+        h = C.c_void_p()
+        call("irk_fgmres_graph_create", ctx(), C.c_void_p(self.tg.raw_cuda_graph()), n, cycle,
+             1 if reorth else 0, ptr(self.V), n, ptr(self.Z), n, ptr(self.vj), ptr(self.zj),
+             ptr(self.w), ptr(self.work), ptr(self.st), C.byref(h))
+        self.handle = h
+
+    def _step(self, A):
+        if self.P is not None:
+            self.P.dev_apply(self.vj, self.zj)
+            A.dev_apply(self.zj, self.w)
+        else:
+            A.dev_apply(self.vj, self.w)
+
+    def run(self, cap, r, beta, target, breakdown, x):
+        """One cycle: (steps taken, converged, residual estimates 1..k)."""
+        status = _lib.load().irk_fgmres_graph_run(
+            ctx(), self.handle, int(cap), ptr(r), float(beta), float(target), float(breakdown),
+            ptr(x), C.byref(self.k), C.byref(self.conv), hptr(self.hist))
+        if status == _lib.IRK_EINVAL:
+            return None  # the context scratch moved: the caller rebuilds
+        _lib.check(status, "irk_fgmres_graph_run")
+        k = int(self.k.value)
+        if self.P is not None:
+            self.P.account(k)
+        return k, bool(self.conv.value), [float(v) for v in self.hist[1:k + 1]]
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.load().irk_fgmres_graph_destroy(self.handle)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+def _fgmres_graph(A, P, n, st, rebuild=False):
+    """The cached cycle graph for (A, P), or None (not capturable, too large,
+    or a key seen for the first time: one-off operators are not captured)."""
+    if _DEVFG_OFF or n > DEVFG_MAX_N or st.restart >= 64 or not st.right_pc:
+        return None
+    ka = A.graph_key()
+    kp = P.graph_key() if P is not None else ()
+    if ka is None or kp is None:
+        return None
+    key = (ka, kp, n, st.restart, bool(st.reorth))
+    g = None if rebuild else _FG_CACHE.get(key)
+    if g is not None:
+        _FG_CACHE.move_to_end(key)
+        return g
+    if not rebuild:
+        if len(_FG_SEEN) > 4096:
+            _FG_SEEN.clear()
+        _FG_SEEN[key] = _FG_SEEN.get(key, 0) + 1
+        if _FG_SEEN[key] < 2:
+            return None
+    try:
+        g = _FgmresGraph(A, P, n, st.restart, st.reorth)
+    except Exception:
+        # not capturable after all: the host loop from now on for this key
+        _FG_SEEN[key] = -(1 << 30)
+        _torch().cuda.synchronize()
+        return None
+    _FG_CACHE[key] = g
+    while len(_FG_CACHE) > 8:
+        _FG_CACHE.popitem(last=False)
+    return g
+
+
 def fgmres_device(A: _DevOp, b, P: _DevOp | None = None, settings: KrylovSettings | None = None,
                   x0=None) -> FgmresResult:
     """Restarted flexible GMRES on device vectors (control flow of
@@ -1163,6 +1314,30 @@ def fgmres_device(A: _DevOp, b, P: _DevOp | None = None, settings: KrylovSetting
     if residuals[0] <= target:
         return FgmresResult(x, 0, residuals)
     breakdown_tol = 1e-14 * normb
+    dg = None if left else _fgmres_graph(A, P, n, st)
+    if dg is not None:
+        # device-resident cycles: one graph launch and one host read per cycle
+        while True:
+            cycle = min(st.restart, st.maxit - iterations)
+            if cycle <= 0:
+                raise NonConvergenceError(
+                    f"fgmres: no convergence in {st.maxit} iterations "
+                    f"(residual {residuals[-1]:.3e}, target {target:.3e})", residuals)
+            beta = residuals[-1] if iterations == 0 else _norm(r)
+            out = dg.run(cycle, r, beta, target, breakdown_tol, x)
+            if out is None:
+                dg = _fgmres_graph(A, P, n, st, rebuild=True)
+                out = dg.run(cycle, r, beta, target, breakdown_tol, x)
+            k, conv, hist = out
+            iterations += k
+            residuals.extend(hist)
+            if conv or residuals[-1] <= target:
+                return FgmresResult(x, iterations, residuals)
+            if iterations >= st.maxit:
+                raise NonConvergenceError(
+                    f"fgmres: no convergence in {st.maxit} iterations "
+                    f"(residual {residuals[-1]:.3e}, target {target:.3e})", residuals)
+            r = residual_of(x)
     hbuf = dev_empty(128)
     tmp = dev_empty(n) if left else None
     while True:

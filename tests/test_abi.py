@@ -11,7 +11,7 @@ from conftest import ROOT
 
 def header_symbols():
     text = (ROOT / "include" / "irk.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(irk_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|size_t|const char\*)\s+(irk_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_core_entry_points():

@@ -694,3 +694,75 @@ def test_mg_hierarchy_1d_and_masks(cuda, irk, oracle):
     untagged = la.SparseMatrix.from_scipy(Mo)
     assert la.BlockFactorization(untagged, la.SparseMatrix.from_scipy(Ko), 1.0, 1e-3, bd)._mg is None
     assert la.dof_mask(M.nrows, bd) is la.dof_mask(M.nrows, np.array(bd))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("restart,reorth,pc", [(50, False, False), (4, False, True),
+                                               (7, True, True), (50, False, True)])
+def test_fgmres_device_cycle_matches_host_loop(cuda, irk, restart, reorth, pc):
+    """The device-resident FGMRES cycle (one CUDA graph per restart cycle:
+    Arnoldi, Givens rotations and stop tests on the device) reproduces the
+    host Givens loop: same iteration count, residual history and solution.
+    A recurring (operator, preconditioner) key is captured on its second
+    use; the first solve runs the host loop."""
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd = irk.assemble_p1(irk.structured_grid(2, 24))
+    op = irk.KroneckerStageOperator(np.eye(2), irk.radau_iia(2).A, M, [K], 0.01)
+    P = None
+    if pc:
+        fac = la.BlockFactorization(M, K, 1.0, 0.01 * 0.4, None, la.BlockSolveSettings())
+        assert fac.direct and fac.graph_safe()
+
+        class _BlockJacobi(la._DevOp):  # one direct solve per stage (interleaved)
+            n = op.n
+
+            def dev_apply(self, x, out):
+                for i in range(2):
+                    fac.dev_solve(x[i:], out[i:], ld_rhs=2, ld_x=2)
+
+            def graph_key(self):
+                return ("bj", fac._serial)
+
+        P = _BlockJacobi()
+    A = op._dev_op()
+    assert A.graph_key() is not None
+    b = la.to_dev(np.random.default_rng(11).standard_normal(op.n))
+    st = la.KrylovSettings(rtol=1e-12, restart=restart, reorth=reorth, maxit=400)
+    la._FG_CACHE.clear()
+    la._FG_SEEN.clear()
+    host = la.fgmres_device(A, b, P, st)
+    assert not la._FG_CACHE  # first use: host loop
+    dev = la.fgmres_device(A, b, P, st)
+    assert len(la._FG_CACHE) == 1  # second use: captured and replayed
+    assert dev.iterations == host.iterations
+    h, d = np.array(host.residuals), np.array(dev.residuals)
+    assert h.shape == d.shape
+    np.testing.assert_allclose(d, h, rtol=1e-8, atol=1e-14 * h[0])
+    x_h, x_d = host.x.cpu().numpy(), dev.x.cpu().numpy()
+    assert np.linalg.norm(x_d - x_h) <= 1e-11 * np.linalg.norm(x_h)
+    # a third solve replays the cached graph again
+    again = la.fgmres_device(A, b, P, st)
+    assert again.iterations == dev.iterations
+    assert np.array_equal(again.x.cpu().numpy(), x_d)  # deterministic
+
+
+@pytest.mark.gpu
+def test_fgmres_device_cycle_lucky_breakdown(cuda, irk):
+    """An exact preconditioner ends the device cycle after one step (lucky
+    breakdown / converged), as the host loop does."""
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd = irk.assemble_p1(irk.structured_grid(2, 12))
+    fac = la.BlockFactorization(M, K, 1.0, 0.05, None, la.BlockSolveSettings())
+    A = la._SpmvOp(fac.matrix)
+    P = fac._dev_op()
+    b = la.to_dev(np.random.default_rng(2).standard_normal(M.nrows))
+    st = la.KrylovSettings(rtol=1e-12)
+    la._FG_CACHE.clear()
+    la._FG_SEEN.clear()
+    r1 = la.fgmres_device(A, b, P, st)
+    r2 = la.fgmres_device(A, b, P, st)
+    assert len(la._FG_CACHE) == 1
+    assert r1.iterations == r2.iterations == 1
+    np.testing.assert_allclose(r2.x.cpu().numpy(), r1.x.cpu().numpy(), rtol=1e-12, atol=1e-14)
