@@ -230,6 +230,13 @@ int irk_bc_scatter(irk_ctx* ctx, int s, int64_t nb, const int64_t* idx_dev,
 int irk_bc_gather(irk_ctx* ctx, int64_t nb, const int64_t* idx_dev, const double* x_dev,
                   double* v_dev);
 int irk_bc_zero(irk_ctx* ctx, int s, int64_t nb, const int64_t* idx_dev, double* X_dev);
+/* DAE stage boundary values from the device state (stage_bc_values,
+ * bcs.py:76-87): out[i*nb+k] = (G[i*nb+k] - u[idx[k]]) / dt (Ainv_host NULL:
+ * the W unknowns), or sum_j Ainv[i][j] (G[j*nb+k] - u[idx[k]]) / dt (the
+ * stage derivatives; Ainv row-major s x s on the host). */
+int irk_bc_dae_values(irk_ctx* ctx, int s, int64_t nb, const int64_t* idx_dev,
+                      const double* G_dev, const double* u_dev, double dt,
+                      const double* Ainv_host, double* out_dev);
 /* mask_dev[idx[k]] = 1, others 0 (length m). */
 int irk_bc_mask(irk_ctx* ctx, int64_t m, int64_t nb, const int64_t* idx_dev, uint8_t* mask_dev);
 

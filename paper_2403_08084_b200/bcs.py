@@ -17,7 +17,7 @@ from typing import Callable, Optional
 import numpy as np
 
 from . import sparsela as la
-from ._lib import call, ctx, ptr
+from ._lib import call, ctx, hptr, ptr
 
 
 class BcMethod(Enum):
@@ -100,6 +100,20 @@ def stage_bc_values(method: BcMethod, tab, bc: DirichletBC, u_n, t: float, dt: f
         G = np.stack([_values_at(bc.g, ti, shape) for ti in stage_t])
         if unknown is StageUnknown.VALUE:
             return G  # independent of u_n: no device read-back
+        if la.is_torch(u_n) and u_n.device.type == "cuda":
+            # from the device state without a host round trip: (s, |Gamma|)
+            # device array, consumed by stage_values_dev
+            if unknown is not StageUnknown.W and not tab.invertible:
+                raise ValueError(
+                    "DAE boundary conditions on stage derivatives need an invertible "
+                    f"tableau, got {tab.name!r}")
+            out = la.dev_empty(G.size)
+            ainv = (None if unknown is StageUnknown.W
+                    else np.ascontiguousarray(_tableau_inverse(tab), dtype=np.float64))
+            call("irk_bc_dae_values", ctx(), tab.s, shape[0], ptr(bc.dofs_dev()),
+                 ptr(la.to_dev(np.ascontiguousarray(G).reshape(-1))), ptr(u_n), float(dt),
+                 hptr(ainv) if ainv is not None else None, ptr(out))
+            return out.reshape(tab.s, -1)
         ub = _boundary_state(u_n, bc.dofs)
         W = (G - ub[None, :]) / dt
         if unknown is StageUnknown.W:

@@ -661,6 +661,28 @@ __global__ void k_bc_gather(int64_t nb, const int64_t* __restrict__ idx,
     v[k] = x[idx[k]];
 }
 
+// DAE boundary values of the stage unknowns from the boundary state on the
+// device (bcs.py:58-96): W[i,k] = (G[i,k] - u[idx[k]]) / dt, out = W (W
+// unknowns) or A^-1 W (derivative unknowns; Ainv row-major s x s, by value)
+__global__ void k_bc_dae(int s, int64_t nb, const int64_t* __restrict__ idx,
+                         const double* __restrict__ G, const double* __restrict__ u, double dt,
+                         Mat8 Ainv, int derivative, double* __restrict__ out) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nb;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double ub = u[idx[k]];
+    double w[kMaxStages];
+    for (int i = 0; i < s; ++i) w[i] = (G[(int64_t)i * nb + k] - ub) / dt;
+    for (int i = 0; i < s; ++i) {
+      double v = w[i];
+      if (derivative) {
+        v = 0.0;
+        for (int j = 0; j < s; ++j) v += Ainv.q[i * kMaxStages + j] * w[j];
+      }
+      out[(int64_t)i * nb + k] = v;
+    }
+  }
+}
+
 __global__ void k_bc_zero(int s, int64_t nb, const int64_t* __restrict__ idx,
                           double* __restrict__ X) {
   int64_t n = nb * s;
@@ -1097,6 +1119,21 @@ int irk_bc_gather(irk_ctx* ctx, int64_t nb, const int64_t* idx_dev, const double
   IRK_REQUIRE(ctx, "irk_bc_gather: bad argument");
   if (nb == 0) return IRK_OK;
   k_bc_gather<<<grid_for(ctx, nb), kBlock, 0, ctx->stream>>>(nb, idx_dev, x_dev, v_dev);
+  IRK_CHECK_LAUNCH(ctx);
+  return IRK_OK;
+}
+
+int irk_bc_dae_values(irk_ctx* ctx, int s, int64_t nb, const int64_t* idx_dev,
+                      const double* G_dev, const double* u_dev, double dt,
+                      const double* Ainv_host, double* out_dev) {
+  IRK_REQUIRE(ctx && s >= 1 && s <= kMaxStages && dt != 0.0, "irk_bc_dae_values: bad argument");
+  if (nb == 0) return IRK_OK;
+  Mat8 Ai{};
+  if (Ainv_host)
+    for (int i = 0; i < s; ++i)
+      for (int j = 0; j < s; ++j) Ai.q[i * kMaxStages + j] = Ainv_host[i * s + j];
+  k_bc_dae<<<grid_for(ctx, nb), kBlock, 0, ctx->stream>>>(s, nb, idx_dev, G_dev, u_dev, dt, Ai,
+                                                          Ainv_host ? 1 : 0, out_dev);
   IRK_CHECK_LAUNCH(ctx);
   return IRK_OK;
 }

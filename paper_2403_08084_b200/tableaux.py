@@ -85,7 +85,12 @@ class ButcherTableau:
 
     @property
     def invertible(self) -> bool:
-        return is_invertible(self)
+        # A is read-only: the LU test runs once per tableau (steppers ask every step)
+        hit = self.__dict__.get("_invertible")
+        if hit is None:
+            hit = is_invertible(self)
+            object.__setattr__(self, "_invertible", hit)
+        return hit
 
     def __repr__(self):
         return f"ButcherTableau({self.name!r}, s={self.s}, order={self.formal_order})"
