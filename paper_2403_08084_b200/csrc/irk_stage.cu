@@ -397,6 +397,41 @@ static bool stencil_layout(const std::vector<int>& sd, StLayout& L) {
   return true;
 }
 
+#include "irk_stage_bulk.cuh"
+
+// launch k_stage_apply_bulk<s, W, KT> on a persistent grid (resident CTAs
+// per SM from the occupancy API, queried once per instantiation)
+template <int S, int W, int KT>
+static void launch_bulk_s(irk_ctx* ctx, int64_t m, int64_t ns, int64_t ntiles,
+                          const BulkLayout& BL, size_t sm, const Pattern* P, const double* mv,
+                          const double* kv, const Coef2& cf, double dt, const uint8_t* mask,
+                          const double* Y, double* Out) {
+  static int occ = 0;
+  static size_t occ_sm = 0;
+  if (!occ || occ_sm != sm) {
+    cudaFuncSetAttribute(k_stage_apply_bulk<S, W, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_apply_bulk<S, W, KT>, KT * 32, sm);
+    occ = std::max(occ, 1);
+    occ_sm = sm;
+  }
+  const unsigned gb = (unsigned)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * occ);
+  k_stage_apply_bulk<S, W, KT><<<gb, KT * 32, sm, ctx->stream>>>(
+      m, ns, ntiles, BL, P->sell_col, P->colhdr, mv, kv, cf, dt, mask, Y, Out);
+}
+template <int W, int KT>
+static void launch_bulk(irk_ctx* ctx, int s, int64_t m, int64_t ns, int64_t ntiles,
+                        const BulkLayout& BL, size_t sm, const Pattern* P, const double* mv,
+                        const double* kv, const Coef2& cf, double dt, const uint8_t* mask,
+                        const double* Y, double* Out) {
+  switch (s) {
+    case 1: launch_bulk_s<1, W, KT>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
+    case 2: launch_bulk_s<2, W, KT>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
+    case 3: launch_bulk_s<3, W, KT>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
+    default: launch_bulk_s<4, W, KT>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
+  }
+}
+
 // Semilinear per-stage Jacobian K_i = kscale K + M diag(D_i):
 // Out_r,i = (C1 (M Y))_i + dt*kscale (C2 (K Y))_i + dt (M (D_i o (C2 Y)_i))_r
 template <int S>
@@ -871,6 +906,33 @@ int irk_stage_apply(irk_ctx* ctx, int s, const double* C1_host, const double* C2
         for (int w = SL.nwin; w < 16; ++w) {
           SL.wbase[w] = 1 << 30;
           SL.wstart[w] = 0;
+        }
+        // bulk-asynchronous tiles (k_stage_apply_bulk); env IRK_NO_BULK: the
+        // per-warp window copies of k_stage_apply_std
+        static const bool bulk_off = getenv("IRK_NO_BULK") != nullptr;
+        // (2D stencils: with the 15-point 3D stencil a tile's two stages fill
+        // the shared memory of one 4-warp CTA per SM, slower than the per-warp
+        // copies: 116 vs 80 us at config 3)
+        if (!bulk_off && P->ellw == 7) {
+          const int kT = P->ellw == 15 ? 4 : 8;
+          BulkLayout BL;
+          const int ymis = (int)(((uintptr_t)Y_dev & 15) / 8);
+          if (bulk_layout(SL, P->ellw, s, kT, ymis, BL)) {
+            const size_t sm =
+                2 * ((size_t)2 * kT * P->ellw * kSlice + kT * kSlice / 8 + (size_t)BL.rows_total * s) *
+                sizeof(double);
+            if (sm <= 200 * 1024) {
+              const int64_t ntiles = (ns + kT - 1) / kT;
+              if (P->ellw == 7)
+                launch_bulk<7, 8>(ctx, s, m, ns, ntiles, BL, sm, P, M->val, kp.k[0], cf, dt,
+                                  rowmask_dev, Y_dev, Out_dev);
+              else
+                launch_bulk<15, 4>(ctx, s, m, ns, ntiles, BL, sm, P, M->val, kp.k[0], cf, dt,
+                                   rowmask_dev, Y_dev, Out_dev);
+              IRK_CHECK_LAUNCH(ctx);
+              return IRK_OK;
+            }
+          }
         }
         if (P->ellw == 7 && SL.nwin <= 3) {
           IRK_LAUNCH_STD(7, 3)

@@ -43,7 +43,21 @@ def main():
             dev.dev_apply(Y, Out)
         e1.record()
         torch.cuda.synchronize()
+        t_eager = e0.elapsed_time(e1) / 1e3 / reps
+        # device time: the applies replayed from one captured CUDA graph (the
+        # eager loop can be bound by the host's ~35 us per Python call)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(reps):
+                dev.dev_apply(Y, Out)
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / 1e3 / reps
+        print(f"   (eager loop {t_eager * 1e6:.2f} us per apply)")
         algo = nnz * 20 + (m + 1) * 4 + 2 * s * m * 8
         peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
         print(f"config {k} stage apply masked={masked}: {t * 1e6:.2f} us, "

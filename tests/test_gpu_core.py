@@ -766,3 +766,42 @@ def test_fgmres_device_cycle_lucky_breakdown(cuda, irk):
     assert len(la._FG_CACHE) == 1
     assert r1.iterations == r2.iterations == 1
     np.testing.assert_allclose(r2.x.cpu().numpy(), r1.x.cpu().numpy(), rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("s,shift", [(3, 0), (3, 1), (2, 0), (4, 0), (1, 1)])
+def test_stage_apply_bulk_tiles_vs_oracle(cuda, irk, oracle, s, shift):
+    """K2 on a 2D stencil grid large enough for the bulk-asynchronous tiles
+    (k_stage_apply_bulk: interior tiles by cp.async.bulk, the first / last
+    tiles by gathers), masked and unmasked, with the stage vector 16-byte
+    aligned or 8 bytes off (shift = 1: a Krylov basis row of odd length)."""
+    from paper_2403_08084_b200 import sparsela as la
+
+    n = 160
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(2, n))
+    Mo, Ko = oracle.p1_matrices(2, n)
+    tab = irk.radau_iia(s)
+    m = M.nrows
+    op = irk.KroneckerStageOperator(np.eye(s), tab.A, M, [K], 1e-3)
+    rng = np.random.default_rng(40 + s)
+    v = rng.standard_normal(s * m)
+    ref = oracle.kron_apply(np.eye(s), tab.A, Mo, [Ko], 1e-3, v)
+    idx = oracle.stage_index(s, m, bd)
+    refc = oracle.constrained(lambda w: oracle.kron_apply(np.eye(s), tab.A, Mo, [Ko], 1e-3, w),
+                              idx)(v)
+    import torch
+
+    for masked, want in ((False, ref), (True, refc)):
+        dev = (irk.ConstrainedStageOperator(op, bd) if masked else op)._dev_op()
+        buf = la.dev_zeros(s * m + 2)
+        Y = buf[shift: shift + s * m]
+        Y.copy_(la.to_dev(_to_il(v, m, s)))
+        out = la.dev_empty(s * m)
+        dev.dev_apply(Y, out)
+        got = out.cpu().numpy().reshape(m, s).T.reshape(-1)
+        assert rel(got, want) < 1e-14, (masked, shift)
+    torch.cuda.synchronize()
+
+
+def _to_il(v, m, s):
+    return np.ascontiguousarray(np.asarray(v).reshape(s, m).T).reshape(-1)
