@@ -742,27 +742,35 @@ __global__ void __launch_bounds__(1024, 1)
   double* fx = sm;       // fine x2 (zero outside the interior)
   double* fr = sm + mf;  // fine residual
   double* buf[2] = {sm + 2 * mf, sm + 2 * mf + m};
-  for (int g = threadIdx.x; g < mf; g += 1024) {
-    const int gx = g % n1f, gy = g / n1f;
-    const bool in = interior2(gx, gy, Nf);
-    fx[g] = in ? x2f[g] : 0.0;
-    fr[g] = in ? bf[g] : 0.0;
-  }
+  // row-wise mapping (warp = row, lane = column): no runtime div/mod per point
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int gy = warp; gy < n1f; gy += 32)
+    for (int gx = lane; gx < n1f; gx += 32) {
+      const int g = gy * n1f + gx;
+      const bool in = interior2(gx, gy, Nf);
+      fx[g] = in ? x2f[g] : 0.0;
+      fr[g] = in ? bf[g] : 0.0;
+    }
   for (int g = threadIdx.x; g < 2 * m; g += 1024) buf[0][g] = 0.0;
   __syncthreads();
-  for (int g = threadIdx.x; g < mf; g += 1024) {
-    const int gx = g % n1f, gy = g / n1f;
-    if (interior2(gx, gy, Nf)) fr[g] -= sten_apply<F9>(Sf, fx, g, n1f);
-  }
+  for (int gy = 1 + warp; gy < Nf; gy += 32)
+    for (int gx = 1 + lane; gx < Nf; gx += 32) {
+      const int g = gy * n1f + gx;
+      fr[g] -= sten_apply<F9>(Sf, fx, g, n1f);
+    }
   __syncthreads();
+  // the coarse points of this thread, once: index, or -1 off the interior
   double bi[PPT], xi[PPT], di[PPT];
+  int gi[PPT];
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     const int g = threadIdx.x + p * 1024;
     double v = 0.0;
+    gi[p] = -1;
     if (g < m) {
       const int cx = g % n1, cy = g / n1;
       if (interior2(cx, cy, N)) {
+        gi[p] = g;
         const int i = 2 * cy * n1f + 2 * cx;
         v = fr[i] + 0.5 * (fr[i - 1] + fr[i + 1] + fr[i - n1f] + fr[i + n1f] + fr[i - n1f - 1] +
                            fr[i + n1f + 1]);
@@ -778,10 +786,8 @@ __global__ void __launch_bounds__(1024, 1)
     double* xo = buf[cur ^ 1];
 #pragma unroll
     for (int p = 0; p < PPT; ++p) {
-      const int g = threadIdx.x + p * 1024;
-      if (g >= m) continue;
-      const int gx = g % n1, gy = g / n1;
-      if (!interior2(gx, gy, N)) continue;  // b_c = 0 there: x stays 0
+      const int g = gi[p];
+      if (g < 0) continue;  // b_c = 0 there: x stays 0
       const double res = bi[p] - (k ? sten_apply<F9>(S, xs, g, n1) : 0.0);
       const double dn = (k ? C.cd[k] * di[p] : 0.0) + C.cr[k] * S.dinv * res;
       di[p] = dn;
@@ -820,6 +826,12 @@ __global__ void __launch_bounds__(1024, 1)
     di[p] = 0.0;
   }
   for (int g = threadIdx.x; g < 2 * m; g += 1024) sm[g] = 0.0;
+  bool inp[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int g = threadIdx.x + p * 1024;
+    inp[p] = g < m && interior2(g % n1, g / n1, N);
+  }
   __syncthreads();
   int cur = 0;
   for (int k = 0; k < C.n; ++k) {
@@ -829,8 +841,7 @@ __global__ void __launch_bounds__(1024, 1)
     for (int p = 0; p < PPT; ++p) {
       const int g = threadIdx.x + p * 1024;
       if (g >= m) continue;
-      const int gx = g % n1, gy = g / n1;
-      if (!interior2(gx, gy, N)) {
+      if (!inp[p]) {
         xi[p] = bi[p];
         continue;  // stays 0 in the shared iterate (eliminated column)
       }
