@@ -391,6 +391,14 @@ int irk_mg_info(const irk_mg* mg, int* nlev, int* structured);
 int irk_mg_pcg(irk_ctx* ctx, irk_mg* mg, const double* rhs_dev, int64_t ld_rhs, double* x_dev,
                int64_t ld_x, double rtol, double atol, int maxit, int* its_host,
                double* relres_host);
+/* n independent block solves (system k: mgs[k], rhs_dev + k*rhs_step,
+ * x_dev + k*x_step; steps in doubles): the block-Jacobi preconditioner's
+ * diagonal blocks (precond.py:97-117 with no coupling terms).  Deferred
+ * solves run concurrently on auxiliary streams (see irk_mgc_cocg_multi). */
+int irk_mg_pcg_multi(irk_ctx* ctx, int n, irk_mg* const* mgs, const double* rhs_dev,
+                     int64_t ld_rhs, int64_t rhs_step, double* x_dev, int64_t ld_x,
+                     int64_t x_step, double rtol, double atol, int maxit, int* its_host,
+                     double* relres_host);
 
 /* ---- complex multigrid for the Schur-pair blocks ------------------------
  * alpha M + beta K with complex alpha, beta (the 2x2 real-Schur pairs of the
@@ -417,6 +425,16 @@ int irk_mgc_info(const irk_mgc* mg, int* nlev, int* structured);
 int irk_mgc_cocg(irk_ctx* ctx, irk_mgc* mg, const double* rhs_dev, int64_t ld_rhs,
                  double* x_dev, int64_t ld_x, double rtol, double atol, int maxit,
                  int* its_host, double* relres_host);
+/* n independent pair solves (system k: mgs[k], rhs_dev + k*rhs_step,
+ * x_dev + k*x_step; steps in doubles, even): the transformed
+ * block-diagonal preconditioner's pair blocks (precond.py:120-157 solves its
+ * blocks one by one).  Deferred solves (NULL its/relres, log enabled) run
+ * concurrently on auxiliary streams forked from and joined into the context
+ * stream; otherwise one after another.  its_host/relres_host: n entries. */
+int irk_mgc_cocg_multi(irk_ctx* ctx, int n, irk_mgc* const* mgs, const double* rhs_dev,
+                       int64_t ld_rhs, int64_t rhs_step, double* x_dev, int64_t ld_x,
+                       int64_t x_step, double rtol, double atol, int maxit, int* its_host,
+                       double* relres_host);
 
 #ifdef __cplusplus
 }

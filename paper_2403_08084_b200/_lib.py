@@ -100,6 +100,10 @@ _SIGS = {
     "irk_mgc_info": [_vp, _vp, _vp],
     "irk_mgc_cocg": [_vp, _vp, _vp, _i64, _vp, _i64, _dbl, _dbl, _int, _vp, _vp],
     "irk_mg_info": [_vp, _vp, _vp],
+    "irk_mg_pcg_multi": [_vp, _int, _vp, _vp, _i64, _i64, _vp, _i64, _i64, _dbl, _dbl, _int, _vp,
+                         _vp],
+    "irk_mgc_cocg_multi": [_vp, _int, _vp, _vp, _i64, _i64, _vp, _i64, _i64, _dbl, _dbl, _int,
+                           _vp, _vp],
     "irk_mg_pcg": [_vp, _vp, _vp, _i64, _vp, _i64, _dbl, _dbl, _int, _vp, _vp],
     "irk_bc_dae_values": [_vp, _int, _i64, _vp, _vp, _vp, _dbl, _vp, _vp],
     "irk_fgmres_work_doubles": [_int],

@@ -103,8 +103,12 @@ int irk_ctx_destroy(irk_ctx* ctx) {
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
+  for (irk_ctx* a : ctx->aux) irk_ctx_destroy(a);
   if (ctx->solve_log) cudaFree(ctx->solve_log);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+  if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
   delete ctx;
   return IRK_OK;
 }
@@ -126,11 +130,12 @@ int64_t irk_ctx_launch_count(const irk_ctx* ctx) { return ctx ? ctx->launches : 
 }  // extern "C"
 
 namespace irk {
-// Room for one more deferred-solve entry: the log doubles when full (a rare,
+// Room for n more deferred-solve entries: the log doubles when full (a rare,
 // synchronous event; entries already written are carried over in order).
-int log_reserve(irk_ctx* ctx) {
-  if (ctx->log_n < ctx->log_cap) return IRK_OK;
-  const int cap = ctx->log_cap * 2;
+int log_reserve(irk_ctx* ctx, int n) {
+  if (ctx->log_n + n <= ctx->log_cap) return IRK_OK;
+  int cap = ctx->log_cap * 2;
+  while (ctx->log_n + n > cap) cap *= 2;
   int* fresh = nullptr;
   IRK_CUDA(cudaMalloc(&fresh, (size_t)cap * 4 * sizeof(int)));
   IRK_CUDA(cudaMemcpyAsync(fresh, ctx->solve_log, (size_t)ctx->log_n * 4 * sizeof(int),
@@ -139,6 +144,24 @@ int log_reserve(irk_ctx* ctx) {
   IRK_CUDA(cudaFree(ctx->solve_log));
   ctx->solve_log = fresh;
   ctx->log_cap = cap;
+  return IRK_OK;
+}
+
+int aux_ctx(irk_ctx* ctx, int k, irk_ctx** out) {
+  while ((int)ctx->aux.size() <= k) {
+    irk_ctx* a = nullptr;
+    IRK_TRY(irk_ctx_create(ctx->device, &a));
+    if (cudaStreamCreateWithFlags(&a->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a->join_ev, cudaEventDisableTiming) != cudaSuccess) {
+      irk_ctx_destroy(a);
+      set_error("aux_ctx: stream/event creation failed");
+      return IRK_ECUDA;
+    }
+    a->stream = a->own_stream;
+    ctx->aux.push_back(a);
+  }
+  if (!ctx->fork_ev) IRK_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+  *out = ctx->aux[k];
   return IRK_OK;
 }
 }  // namespace irk

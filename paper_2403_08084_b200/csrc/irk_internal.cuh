@@ -99,6 +99,13 @@ struct irk_ctx {
   int* solve_log = nullptr;  // 4 ints per entry
   int log_cap = 0;
   int64_t log_n = 0;
+  // Independent inner solves run concurrently (irk::run_forked): system
+  // k >= 1 on auxiliary context aux[k-1] (own stream, workspace, reduction
+  // scratch and graph cache), forked from and joined into `stream`.
+  std::vector<irk_ctx*> aux;
+  cudaStream_t own_stream = nullptr;  // created by and owned by this context
+  cudaEvent_t fork_ev = nullptr;
+  cudaEvent_t join_ev = nullptr;
 };
 
 namespace irk {
@@ -145,7 +152,61 @@ constexpr int kNumCounters = 16;
 int ensure_red(irk_ctx* ctx, size_t doubles);
 int ensure_work(irk_ctx* ctx, size_t bytes);
 int ensure_pinned(irk_ctx* ctx, size_t bytes);
-int log_reserve(irk_ctx* ctx);
+int log_reserve(irk_ctx* ctx, int n = 1);
+// auxiliary context k (lazily created, own non-blocking stream)
+int aux_ctx(irk_ctx* ctx, int k, irk_ctx** out);
+
+// Run fn(k, c) for the n independent systems k = 0..n-1.  Concurrent when
+// `concurrent` (deferred solves: no host round trip inside fn) and the
+// stream is not being captured: system k >= 1 runs on auxiliary context
+// k-1, whose stream waits on an event of ctx->stream and is joined back
+// into it; system 0 runs on ctx.  The latency-bound coarse levels of one
+// system's V-cycles then overlap with the other systems' kernels.  Deferred
+// log entries land in ctx's log in system order, launches are counted on
+// ctx.  Sequential otherwise.
+template <typename F>
+int run_forked(irk_ctx* ctx, int n, bool concurrent, F&& fn) {
+  static const bool fork_off = getenv("IRK_NO_FORK") != nullptr;  // A/B: one by one
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (fork_off) concurrent = false;
+  if (concurrent && n > 1) {
+    if (cudaStreamIsCapturing(ctx->stream, &cap) != cudaSuccess) cap = cudaStreamCaptureStatusActive;
+  }
+  if (!concurrent || n <= 1 || cap != cudaStreamCaptureStatusNone) {
+    for (int k = 0; k < n; ++k) IRK_TRY(fn(k, ctx));
+    return IRK_OK;
+  }
+  if (ctx->log_on) IRK_TRY(log_reserve(ctx, n));
+  irk_ctx* a = nullptr;
+  IRK_TRY(aux_ctx(ctx, n - 2, &a));
+  IRK_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
+  const int64_t base = ctx->log_n;
+  int status = IRK_OK;
+  int forked = 0;
+  for (int k = 1; k < n && status == IRK_OK; ++k, ++forked) {
+    a = ctx->aux[k - 1];
+    IRK_CUDA(cudaStreamWaitEvent(a->stream, ctx->fork_ev, 0));
+    a->log_on = ctx->log_on;
+    a->solve_log = ctx->solve_log;
+    a->log_cap = ctx->log_cap;
+    a->log_n = base + k;
+    const int64_t l0 = a->launches;
+    status = fn(k, a);
+    ctx->launches += a->launches - l0;
+    a->solve_log = nullptr;
+    a->log_on = 0;
+    a->log_n = 0;
+    IRK_CUDA(cudaEventRecord(a->join_ev, a->stream));
+  }
+  if (status == IRK_OK) {
+    ctx->log_n = base;
+    status = fn(0, ctx);
+    ctx->log_n = base + n;
+  }
+  for (int k = 0; k < forked; ++k)
+    IRK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux[k]->join_ev, 0));
+  return status;
+}
 // Byte-string key builder for the graph cache.
 struct GraphKey {
   std::string k;

@@ -1478,4 +1478,17 @@ int irk_mg_pcg(irk_ctx* ctx, irk_mg* mg, const double* rhs_dev, int64_t ld_rhs, 
 #undef IRK_MGRUN
 }
 
+int irk_mg_pcg_multi(irk_ctx* ctx, int n, irk_mg* const* mgs, const double* rhs_dev,
+                     int64_t ld_rhs, int64_t rhs_step, double* x_dev, int64_t ld_x,
+                     int64_t x_step, double rtol, double atol, int maxit, int* its_host,
+                     double* relres_host) {
+  IRK_REQUIRE(ctx && mgs && n >= 0, "irk_mg_pcg_multi: NULL argument");
+  const bool deferred = !its_host && !relres_host && ctx->log_on;
+  return run_forked(ctx, n, deferred, [&](int k, irk_ctx* c) {
+    return irk_mg_pcg(c, mgs[k], rhs_dev + k * rhs_step, ld_rhs, x_dev + k * x_step, ld_x, rtol,
+                      atol, maxit, its_host ? its_host + k : nullptr,
+                      relres_host ? relres_host + k : nullptr);
+  });
+}
+
 }  // extern "C"

@@ -1011,4 +1011,18 @@ int irk_mgc_cocg(irk_ctx* ctx, irk_mgc* mg, const double* rhs_dev, int64_t ld_rh
 #undef IRK_MGCRUN
 }
 
+int irk_mgc_cocg_multi(irk_ctx* ctx, int n, irk_mgc* const* mgs, const double* rhs_dev,
+                       int64_t ld_rhs, int64_t rhs_step, double* x_dev, int64_t ld_x,
+                       int64_t x_step, double rtol, double atol, int maxit, int* its_host,
+                       double* relres_host) {
+  IRK_REQUIRE(ctx && mgs && n >= 0, "irk_mgc_cocg_multi: NULL argument");
+  IRK_REQUIRE(rhs_step % 2 == 0 && x_step % 2 == 0, "irk_mgc_cocg_multi: odd system step");
+  const bool deferred = !its_host && !relres_host && ctx->log_on;
+  return run_forked(ctx, n, deferred, [&](int k, irk_ctx* c) {
+    return irk_mgc_cocg(c, mgs[k], rhs_dev + k * rhs_step, ld_rhs, x_dev + k * x_step, ld_x, rtol,
+                        atol, maxit, its_host ? its_host + k : nullptr,
+                        relres_host ? relres_host + k : nullptr);
+  });
+}
+
 }  // extern "C"

@@ -182,6 +182,15 @@ class StagePreconditioner:
             return False
         return all(f._mg is not None or f.direct for f in facs)
 
+    def _concurrent_blocks(self, coefs) -> bool:
+        """Independent multigrid block solves that may overlap: no coupling
+        terms, deferred status, every block on its hierarchy."""
+        if not self.defer_solves or self.settings.raise_on_maxit or self.s < 2:
+            return False
+        if any(c is not None for c in coefs) or self.settings.method not in ("auto", "mg"):
+            return False
+        return all(f._mg is not None and not f.direct for f in self.block_factors)
+
     def _block_coefs(self):
         s = self.s
         if self.form is Splitting.IA:
@@ -231,8 +240,21 @@ class StagePreconditioner:
         # solve writes its whole stage column of X before a later block reads
         # it, so X needs no zeroing
         order, coefs = self._sweep_plan()
-        tmp = la.dev_empty(m)
         n0 = len(self.inner_iterations)
+        if self._concurrent_blocks(coefs):
+            # block Jacobi on multigrid blocks, deferred: the s independent
+            # solves read their stage columns of R in place and run
+            # concurrently (one auxiliary stream per block after the first)
+            st = self.settings
+            hs = (C.c_void_p * s)(*[f._mg.handle.value for f in self.block_factors])
+            status = _lib.load().irk_mg_pcg_multi(
+                ctx(), s, hs, ptr(R), s, 1, ptr(X), s, 1, float(st.rtol), float(st.atol),
+                int(st.maxit), None, None)
+            _lib.check(status, "deferred block solves")
+            self.inner_iterations.extend([[None]] * s)
+            self._last_apply = self.inner_iterations[n0:]
+            return X
+        tmp = la.dev_empty(m)
         for i in order:
             coef = coefs[i]
             if coef is not None:
@@ -336,7 +358,16 @@ class StagePreconditioner:
         if mgc is not None:
             # one multigrid-preconditioned COCG per pair block (complex V-cycle)
             defer = self.defer_solves and not st.raise_on_maxit
-            for k in range(npairs):
+            if defer:
+                # the pair solves are independent: concurrent on auxiliary
+                # streams, status to the deferred log
+                hs = (C.c_void_p * npairs)(*[h.handle.value for h in mgc])
+                status = _lib.load().irk_mgc_cocg_multi(
+                    ctx(), npairs, hs, ptr(W), sp_, 2, ptr(Z), sp_, 2, float(st.rtol),
+                    float(st.atol), int(st.maxit), None, None)
+                _lib.check(status, "deferred pair solves")
+                self.inner_iterations.extend([[None]] * npairs)
+            for k in range(0 if defer else npairs):
                 its = np.zeros(1, dtype=np.int32)
                 rel = np.zeros(1)
                 status = _lib.load().irk_mgc_cocg(

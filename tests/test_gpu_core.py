@@ -674,6 +674,69 @@ def test_mg_pcg_cap_and_deferred_log(cuda, irk):
 
 
 @pytest.mark.gpu
+def test_forked_block_and_pair_solves_match_sequential(cuda, irk):
+    """irk_mg_pcg_multi / irk_mgc_cocg_multi: deferred independent solves
+    run concurrently on auxiliary streams and give bit-identical solutions,
+    iteration counts and log order to the one-by-one synchronous solves."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2403_08084_b200 import _lib
+    from paper_2403_08084_b200 import sparsela as la
+
+    lib = _lib.load()
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(2, 128))
+    m, s = M.nrows, 3
+    st = la.BlockSolveSettings(method="mg", rtol=1e-8)
+    facs = [la.BlockFactorization(M, K, 1.0, b, bd, st) for b in (2e-3, 5e-3, 1e-2)]
+    assert all(f._mg is not None for f in facs)
+    R = la.to_dev(np.random.default_rng(5).standard_normal(s * m))
+    X_seq = la.dev_zeros(s * m)
+    its_seq = []
+    for k, f in enumerate(facs):
+        its_seq.append(f.dev_solve(R[k:], X_seq[k:], ld_rhs=s, ld_x=s, settings=st))
+    hs = (C.c_void_p * s)(*[f._mg.handle.value for f in facs])
+    X_par = la.dev_zeros(s * m)
+    with _lib.deferred_solves() as log:
+        assert lib.irk_mg_pcg_multi(_lib.ctx(), s, hs, _lib.ptr(R), s, 1, _lib.ptr(X_par), s, 1,
+                                    1e-8, 0.0, 500, None, None) == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    assert log.entries.shape == (s, 4)
+    assert list(log.entries[:, 0]) == its_seq and not log.entries[:, 1].any()
+    assert torch.equal(X_par, X_seq)
+
+    # complex Schur-pair blocks (two pairs, interleaved with ld 4)
+    M3, K3, bd3 = irk.assemble_p1(irk.structured_grid(3, 16))
+    m3 = M3.nrows
+    mask = la.dof_mask(m3, bd3)
+    Md, Kd = la.shared_pattern([M3.device(), K3.device()])
+    Md, Kd = Md.eliminated(mask), Kd.eliminated(mask)
+    hs3 = [la._MgcHierarchy.build(M3, K3, Md, Kd, 1.0 + 0j, b, mask,
+                                  la.BlockSolveSettings(rtol=1e-10))
+           for b in (0.01 * (0.09 + 0.12j), 0.01 * (0.2 + 0.05j))]
+    assert all(h is not None for h in hs3)
+    W = la.to_dev(np.random.default_rng(6).standard_normal(4 * m3))
+    Z_seq = la.dev_zeros(4 * m3)
+    its_c = []
+    for k, h in enumerate(hs3):
+        its = np.zeros(1, dtype=np.int32)
+        rel_ = np.zeros(1)
+        assert lib.irk_mgc_cocg(_lib.ctx(), h.handle, _lib.ptr(W[2 * k:]), 4,
+                                _lib.ptr(Z_seq[2 * k:]), 4, 1e-10, 0.0, 500, _lib.hptr(its),
+                                _lib.hptr(rel_)) == 0
+        its_c.append(int(its[0]))
+    Z_par = la.dev_zeros(4 * m3)
+    hh = (C.c_void_p * 2)(*[h.handle.value for h in hs3])
+    with _lib.deferred_solves() as log:
+        assert lib.irk_mgc_cocg_multi(_lib.ctx(), 2, hh, _lib.ptr(W), 4, 2, _lib.ptr(Z_par), 4,
+                                      2, 1e-10, 0.0, 500, None, None) == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    assert list(log.entries[:, 0]) == its_c and not log.entries[:, 1].any()
+    assert torch.equal(Z_par, Z_seq)
+
+
+@pytest.mark.gpu
 def test_mg_hierarchy_1d_and_masks(cuda, irk, oracle):
     """1D P1 blocks get a hierarchy; a non-boundary Dirichlet set or a
     missing grid tag falls back to Jacobi-PCG; the mask cache returns one
