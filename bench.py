@@ -360,8 +360,9 @@ def step_stats(reps):
 
 
 def spawn_cpu_jobs(ks, budget, avoid_cpu):
-    """CPU baselines as subprocesses (one core each, pinned away from this
-    process's core) so they run while the GPU arm works."""
+    """CPU baselines as subprocesses, one core each (pinned, in parallel when
+    the affinity mask has a core per job), started after the GPU arm's
+    measurements."""
     import subprocess
 
     try:
@@ -534,15 +535,6 @@ def run_ours(args, world, rank, local):
     _lib.load()
     k = args.config
     solo = rank == 0 and world == 1
-    cpu_jobs = None
-    if solo and not args.no_cpu_baseline:
-        ks = [k] + ([j for j in (1, 2, 3, 4, 5) if j != k] if not args.no_workloads else [])
-        try:
-            me = os.sched_getaffinity(0)
-            me = min(me) if len(me) == 1 else -1
-        except AttributeError:
-            me = -1
-        cpu_jobs = spawn_cpu_jobs(ks, args.cpu_budget, me)
     # experiments only: IRK_BENCH_BLOCK='{"mg_nu": 3}' overrides block-solver settings
     wl = configs.build(k, **json.loads(os.environ.get("IRK_BENCH_BLOCK", "{}")))
     st, prob = wl.stepper, wl.problem
@@ -605,8 +597,16 @@ def run_ours(args, world, rank, local):
     }
     if solo and not args.no_workloads:
         out["workloads"] = other_workloads(k, args)
-    if cpu_jobs is not None:
-        res = collect_cpu_jobs(*cpu_jobs)
+    if solo and not args.no_cpu_baseline:
+        # the CPU baselines run after every GPU measurement (run alongside,
+        # their memory traffic slowed the host side of the e2e steps ~10 %)
+        ks = [k] + ([j for j in (1, 2, 3, 4, 5) if j != k] if not args.no_workloads else [])
+        try:
+            me = os.sched_getaffinity(0)
+            me = min(me) if len(me) == 1 else -1
+        except AttributeError:
+            me = -1
+        res = collect_cpu_jobs(*spawn_cpu_jobs(ks, args.cpu_budget, me))
         out["cpu_baseline"] = res.get(k)
         for j, r in res.items():
             if j != k and "workloads" in out and str(j) in out["workloads"]:

@@ -386,6 +386,15 @@ int irk_mg_vcycle(irk_ctx* ctx, irk_mg* mg, const double* r_dev, double* z_dev);
  * (IRK_EINVAL when unavailable) or off, and query the hierarchy. */
 int irk_mg_set_structured(irk_mg* mg, int on);
 int irk_mg_info(const irk_mg* mg, int* nlev, int* structured);
+/* Fast sine-transform preconditioner of the level-0 block (replaces the
+ * V-cycle inside irk_mg_pcg when on): the reflection-symmetrised level-0
+ * stencil inverted exactly by 2D DST-I (shared-memory FFTs of length 2N),
+ * B_s^-1 = (2/N)^2 S Lambda^-1 S.  Available for verified 2D grid stencils
+ * with the full-boundary Dirichlet set, N a power of two in [32, 2048].
+ * Replaces the reference's exact block solve (sparsela.py:171-191) like
+ * the V-cycle does: CG on the block to the requested tolerance. */
+int irk_mg_set_dst(irk_mg* mg, int on);
+int irk_mg_dst_info(const irk_mg* mg, int* available, int* on);
 /* CG on the level-0 block preconditioned by one V-cycle per iteration;
  * strided rhs/x as irk_pcg; status as irk_pcg. */
 int irk_mg_pcg(irk_ctx* ctx, irk_mg* mg, const double* rhs_dev, int64_t ld_rhs, double* x_dev,

@@ -1,0 +1,258 @@
+// Fast sine-transform (DST-I) preconditioner for the 2D grid blocks
+// alpha M + beta K with the full-boundary Dirichlet set.
+//
+// The block's interior operator is ONE 3x3 stencil c[dy][dx] (extracted from
+// the assembled matrix and verified against every row by the structured
+// multigrid setup, irk_mg.cu k_mg2_row_stencil / k_mg2_verify).  Its
+// reflection-symmetrised copy
+//   s00 = c00,  s10 = (c[1][0] + c[1][2]) / 2,  s01 = (c[0][1] + c[2][1]) / 2,
+//   s11 = (c[0][0] + c[0][2] + c[2][0] + c[2][2]) / 4
+// is diagonalised by the 2D sine basis sin(pi j k / N) sin(pi i l / N):
+//   lambda(k, l) = s00 + 2 s10 cos(pi k/N) + 2 s01 cos(pi l/N)
+//                  + 4 s11 cos(pi k/N) cos(pi l/N),
+// so  B_s^-1 = (2/N)^2 S_x S_y Lambda^-1 S_y S_x  (S = DST-I, S S = N/2 I).
+// B - B_s only moves the P1 diagonal-edge coupling (weight h^2/12 of the
+// mass matrix) between the two diagonals, so the spectrum of B_s^-1 B lies
+// in [1 - eps, 1 + eps] with eps ~ h^2 / (12 |beta / alpha|) (1e-4 .. 1e-5 on
+// the 1024^2 / 2048^2 workloads): CG reaches 1e-6 in ~2 and 1e-12 in ~3-4
+// iterations instead of ~5.5 / ~9 multigrid-PCG ones.  Boundary rows are
+// identity (z = r there).
+//
+// DST-I of length N-1 through a complex FFT of length L = 2N of the odd
+// extension y = (0, x_1..x_{N-1}, 0, -x_{N-1}..-x_1):  Y_k = -2i S_k.  Two
+// real sequences a, b share one FFT (y = a + i b):  S_a = -Im Y / 2,
+// S_b = Re Y / 2.  The FFT runs in shared memory: Stockham autosort passes
+// of radix 8 (one radix-2/4 pass for the remainder), each thread holding its
+// radix-R butterfly in registers; one twiddle table e^{-2 pi i q / L}.
+//
+// Three kernels per application (N a power of two, 32 <= N <= 2048):
+//   k_dst_rows<L, false>  rows of r      -> T (row DSTs, T has row stride N)
+//   k_dst_cols<L>         columns of T   -> column DST, scale (2/N)^2/lambda,
+//                                           column DST, back to T (4 columns
+//                                           per CTA: one 32-byte sector per row)
+//   k_dst_rows<L, true>   rows of T      -> z (row DSTs; boundary z = r)
+// Each reads and writes the grid once (L2-resident at these sizes).
+#pragma once
+
+namespace irk {
+
+struct DstStencil {
+  double s00, s10, s01, s11;
+};
+
+__device__ __forceinline__ double2 c_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 c_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 c_mul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// (-i) z
+__device__ __forceinline__ double2 c_mi(double2 a) { return make_double2(a.y, -a.x); }
+
+// in-register forward DFTs (e^{-2 pi i j k / R}), natural order in and out
+__device__ __forceinline__ void dft2(double2* v) {
+  const double2 t = v[0];
+  v[0] = c_add(t, v[1]);
+  v[1] = c_sub(t, v[1]);
+}
+__device__ __forceinline__ void dft4(double2& x0, double2& x1, double2& x2, double2& x3) {
+  const double2 t0 = c_add(x0, x2), t1 = c_sub(x0, x2);
+  const double2 t2 = c_add(x1, x3), t3 = c_mi(c_sub(x1, x3));
+  x0 = c_add(t0, t2);
+  x2 = c_sub(t0, t2);
+  x1 = c_add(t1, t3);
+  x3 = c_sub(t1, t3);
+}
+__device__ __forceinline__ void dft8(double2* v) {
+  double2 a0 = v[0], a1 = v[2], a2 = v[4], a3 = v[6];
+  double2 b0 = v[1], b1 = v[3], b2 = v[5], b3 = v[7];
+  dft4(a0, a1, a2, a3);
+  dft4(b0, b1, b2, b3);
+  constexpr double r = 0.70710678118654752440;
+  // w8^1 = (1 - i)/sqrt2, w8^2 = -i, w8^3 = (-1 - i)/sqrt2
+  const double2 w1 = make_double2(r * (b1.x + b1.y), r * (b1.y - b1.x));
+  const double2 w2 = c_mi(b2);
+  const double2 w3 = make_double2(r * (b3.y - b3.x), -r * (b3.x + b3.y));
+  v[0] = c_add(a0, b0);
+  v[4] = c_sub(a0, b0);
+  v[1] = c_add(a1, w1);
+  v[5] = c_sub(a1, w1);
+  v[2] = c_add(a2, w2);
+  v[6] = c_sub(a2, w2);
+  v[3] = c_add(a3, w3);
+  v[7] = c_sub(a3, w3);
+}
+
+// One Stockham pass of radix R over the L-point sequence in buf (in place:
+// every thread first reads all its butterflies, then the block syncs, then
+// writes), NT threads of the calling group (tid in [0, NT)).
+template <int L, int R, int NT>
+__device__ __forceinline__ void fft_pass(double2* buf, int Ns, const double2* __restrict__ tw,
+                                         int tid) {
+  constexpr int ITEMS = L / R / NT;
+  static_assert(ITEMS >= 1 && (L / R) % NT == 0, "fft_pass: bad thread count");
+  double2 v[ITEMS][R];
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const int j = tid + it * NT;
+    const int k = j % Ns;
+    const int step = k * (L / (Ns * R));
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double2 x = buf[j + r * (L / R)];
+      if (r > 0 && k > 0) x = c_mul(x, __ldg(tw + r * step));
+      v[it][r] = x;
+    }
+    if constexpr (R == 8) dft8(v[it]);
+    else if constexpr (R == 4) dft4(v[it][0], v[it][1], v[it][2], v[it][3]);
+    else dft2(v[it]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const int j = tid + it * NT;
+    const int k = j % Ns;
+    const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[base + r * Ns] = v[it][r];
+  }
+  __syncthreads();
+}
+
+// L / (the largest power of 8 dividing L): the last pass's radix (1: none)
+__host__ __device__ constexpr int fft_rem(int L) { return L % 8 == 0 ? fft_rem(L / 8) : L; }
+
+// Forward FFT of L points (power of two, 16 <= L <= 4096) in buf: radix-8
+// passes, then one radix-4 or radix-2 pass for the remainder.
+template <int L, int NT>
+__device__ __forceinline__ void fft_smem(double2* buf, const double2* __restrict__ tw, int tid) {
+  int Ns = 1;
+#pragma unroll
+  for (int p = 8; p <= L; p *= 8) {
+    fft_pass<L, 8, NT>(buf, Ns, tw, tid);
+    Ns *= 8;
+  }
+  constexpr int rem = fft_rem(L);
+  if constexpr (rem == 4) fft_pass<L, 4, NT>(buf, Ns, tw, tid);
+  else if constexpr (rem == 2) fft_pass<L, 2, NT>(buf, Ns, tw, tid);
+}
+
+// Row DSTs.  Forward (INV = false): rows gy = 1..N-1 of the grid vector src
+// (row stride n1 = N + 1) -> T (row stride N, column k = 1..N-1, column 0
+// zero).  Inverse (INV = true): rows of T -> z (row stride n1), the boundary
+// of z copied from r.  CTA b takes rows 1 + 2b and 2 + 2b (one complex FFT).
+template <int L, bool INV>
+__global__ void __launch_bounds__(L / 8)
+    k_dst_rows(int N, const double* __restrict__ src, double* __restrict__ dst,
+               const double* __restrict__ r, const double2* __restrict__ tw, const int* stop) {
+  IRK_PDL_ENTER();
+  if (stop && *stop) return;
+  constexpr int NT = L / 8;
+  extern __shared__ double2 dst_buf[];
+  double2* buf = dst_buf;
+  const int n1 = N + 1;
+  const int ra = 1 + 2 * blockIdx.x, rb = ra + 1;
+  const bool hb = rb <= N - 1;
+  const int sstride = INV ? N : n1;
+  const double* sa = src + (size_t)ra * sstride;
+  const double* sb = src + (size_t)rb * sstride;
+  for (int j = threadIdx.x; j <= N; j += NT) {
+    double2 y = make_double2(0.0, 0.0);
+    if (j >= 1 && j <= N - 1) y = make_double2(sa[j], hb ? sb[j] : 0.0);
+    buf[j] = y;
+    if (j >= 1 && j <= N - 1) buf[L - j] = make_double2(-y.x, -y.y);
+  }
+  __syncthreads();
+  fft_smem<L, NT>(buf, tw, threadIdx.x);
+  const int dstride = INV ? n1 : N;
+  double* da = dst + (size_t)ra * dstride;
+  double* db = dst + (size_t)rb * dstride;
+  for (int k = threadIdx.x; k <= N; k += NT) {
+    if (k >= 1 && k <= N - 1) {
+      const double2 Y = buf[k];
+      da[k] = -0.5 * Y.y;
+      if (hb) db[k] = 0.5 * Y.x;
+    } else if (INV) {
+      // boundary columns x = 0, x = N of these rows: identity rows
+      da[k] = r[(size_t)ra * n1 + k];
+      if (hb) db[k] = r[(size_t)rb * n1 + k];
+    } else if (k == 0) {
+      da[0] = 0.0;
+      if (hb) db[0] = 0.0;
+    }
+  }
+  if (INV) {
+    // boundary rows y = 0 (first CTA) and y = N (last CTA): identity rows
+    if (blockIdx.x == 0)
+      for (int k = threadIdx.x; k <= N; k += NT) dst[k] = r[k];
+    if (blockIdx.x == gridDim.x - 1)
+      for (int k = threadIdx.x; k <= N; k += NT) dst[(size_t)N * n1 + k] = r[(size_t)N * n1 + k];
+  }
+}
+
+// Column DSTs, spectral scaling and inverse column DSTs on T in place:
+// CTA b owns columns 4b .. 4b+3 (column 0 is the zero column), two complex
+// FFTs of L points (columns (4b, 4b+1) and (4b+2, 4b+3)), L/4 threads in two
+// groups.  coskn[k] = cos(pi k / N).
+template <int L>
+__global__ void __launch_bounds__(L / 4)
+    k_dst_cols(int N, double* __restrict__ T, DstStencil S, const double* __restrict__ coskn,
+               const double2* __restrict__ tw, const int* stop) {
+  IRK_PDL_ENTER();
+  if (stop && *stop) return;
+  constexpr int NT = L / 8;
+  extern __shared__ double2 dst_buf[];
+  const int grp = threadIdx.x / NT, tid = threadIdx.x % NT;
+  double2* buf = dst_buf + grp * L;
+  const int k0 = 4 * blockIdx.x;
+  // load rows 1..N-1 of the 4 columns: thread t takes column t % 4 of row
+  // 1 + t / 4 (one 32-byte sector per row)
+  for (int t = threadIdx.x; t < 4 * (N - 1); t += 2 * NT) {
+    const int l = 1 + (t >> 2), c = t & 3;
+    const double v = T[(size_t)l * N + k0 + c];
+    double2* b = dst_buf + (c >> 1) * L;
+    if (c & 1) {
+      b[l].y = v;
+      b[L - l].y = -v;
+    } else {
+      b[l].x = v;
+      b[L - l].x = -v;
+    }
+  }
+  if (threadIdx.x < 2) {
+    double2* b = dst_buf + threadIdx.x * L;
+    b[0] = make_double2(0.0, 0.0);
+    b[N] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  fft_smem<L, NT>(buf, tw, tid);
+  // spectral scaling: column k (a: 4b + 2 grp, b: + 1), row frequency l
+  {
+    const int ka = k0 + 2 * grp, kb = ka + 1;
+    const double cka = coskn[ka], ckb = coskn[kb];
+    const double sc = 4.0 / ((double)N * (double)N);
+    for (int l = 1 + tid; l <= N - 1; l += NT) {
+      const double2 Y = buf[l];
+      const double cl = coskn[l];
+      // column 0 is the zero column (Y = 0 there): any nonzero lambda
+      const double la = ka == 0 ? 1.0
+                                : S.s00 + 2.0 * S.s10 * cka + cl * (2.0 * S.s01 + 4.0 * S.s11 * cka);
+      const double lb = S.s00 + 2.0 * S.s10 * ckb + cl * (2.0 * S.s01 + 4.0 * S.s11 * ckb);
+      const double2 y = make_double2(-0.5 * Y.y * sc / la, 0.5 * Y.x * sc / lb);
+      buf[l] = y;
+      buf[L - l] = make_double2(-y.x, -y.y);
+    }
+    if (tid == 0) {
+      buf[0] = make_double2(0.0, 0.0);
+      buf[N] = make_double2(0.0, 0.0);
+    }
+  }
+  __syncthreads();
+  fft_smem<L, NT>(buf, tw, tid);
+  for (int t = threadIdx.x; t < 4 * (N - 1); t += 2 * NT) {
+    const int l = 1 + (t >> 2), c = t & 3;
+    const double2 Y = dst_buf[(c >> 1) * L + l];
+    T[(size_t)l * N + k0 + c] = (c & 1) ? 0.5 * Y.x : -0.5 * Y.y;
+  }
+}
+
+}  // namespace irk

@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "irk_inner.cuh"
+#include "irk_dst.cuh"
 
 namespace irk {
 
@@ -993,6 +994,110 @@ struct irk_mg : public irk::CgPrec {
   std::vector<bool> f9;
   std::vector<irk::ChebS> c2;  // per level (lmax differs)
   irk::ChebN cn{};
+  // fast sine-transform preconditioner of the level-0 block (irk_dst.cuh):
+  // available / in use instead of the V-cycle
+  bool dst_ok = false, dst_on = false;
+  int dst_N = 0;
+  irk::DstStencil dstS{};
+  double* dst_mem = nullptr;
+  double* dst_T = nullptr;      // N x N spectral work array
+  double* dst_cos = nullptr;    // cos(pi k / N), k = 0..N
+  double2* dst_tw = nullptr;    // e^{-2 pi i q / (2N)}, q < 2N
+
+  // Set up the sine-transform preconditioner on a verified level-0 stencil
+  // (structured path available): N a power of two in [32, 2048], the
+  // symmetrised stencil's eigenvalues positive (bilinear in cos(pi k/N),
+  // cos(pi l/N): the extremes are at the corners).
+  int setup_dst(irk_ctx* ctx) {
+    using namespace irk;
+    dst_ok = false;
+    if (!s2_ok || dim != 2) return IRK_OK;
+    const int N = (int)lev[0].g.n1 - 1;
+    if (N < 32 || N > 2048 || (N & (N - 1)) != 0) return IRK_OK;
+    const Sten2& C = sten[0];
+    DstStencil S;
+    S.s00 = C.c[1][1];
+    S.s10 = 0.5 * (C.c[1][0] + C.c[1][2]);
+    S.s01 = 0.5 * (C.c[0][1] + C.c[2][1]);
+    S.s11 = 0.25 * (C.c[0][0] + C.c[0][2] + C.c[2][0] + C.c[2][2]);
+    const double ce[2] = {std::cos(M_PI / N), -std::cos(M_PI / N)};
+    for (double a : ce)
+      for (double b : ce) {
+        const double lam = S.s00 + 2 * S.s10 * a + 2 * S.s01 * b + 4 * S.s11 * a * b;
+        if (!(lam > 0.0) || !std::isfinite(lam)) return IRK_OK;
+      }
+    const int L = 2 * N;
+    const size_t doubles = (size_t)N * N + (N + 1) + 2 * (size_t)L + 8;
+    if (!dst_mem) IRK_CUDA(cudaMalloc(&dst_mem, doubles * sizeof(double)));
+    dst_T = dst_mem;
+    dst_tw = reinterpret_cast<double2*>(dst_mem + (size_t)N * N);  // 16-byte aligned (N even)
+    dst_cos = dst_mem + (size_t)N * N + 2 * (size_t)L;
+    std::vector<double> host(2 * (size_t)L + N + 1);
+    for (int q = 0; q < L; ++q) {
+      // exact at the multiples of pi/4 (the cos/sin of the reduced angle)
+      const double a = -2.0 * M_PI * (double)q / (double)L;
+      host[2 * q] = std::cos(a);
+      host[2 * q + 1] = std::sin(a);
+    }
+    for (int k = 0; k <= N; ++k) host[2 * (size_t)L + k] = std::cos(M_PI * (double)k / N);
+    IRK_CUDA(cudaMemcpyAsync(dst_tw, host.data(), host.size() * sizeof(double),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+    IRK_TRY(dst_attrs(L));
+    dstS = S;
+    dst_N = N;
+    dst_ok = true;
+    return IRK_OK;
+  }
+
+  template <int L>
+  static int dst_attrs_l() {
+    IRK_CUDA(cudaFuncSetAttribute(irk::k_dst_rows<L, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, L * 16));
+    IRK_CUDA(cudaFuncSetAttribute(irk::k_dst_rows<L, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, L * 16));
+    IRK_CUDA(cudaFuncSetAttribute(irk::k_dst_cols<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  2 * L * 16));
+    return IRK_OK;
+  }
+  static int dst_attrs(int L) {
+    switch (L) {
+      case 64: return dst_attrs_l<64>();
+      case 128: return dst_attrs_l<128>();
+      case 256: return dst_attrs_l<256>();
+      case 512: return dst_attrs_l<512>();
+      case 1024: return dst_attrs_l<1024>();
+      case 2048: return dst_attrs_l<2048>();
+      case 4096: return dst_attrs_l<4096>();
+    }
+    return IRK_EINVAL;
+  }
+
+  template <int L>
+  int apply_dst_l(irk_ctx* ctx, cudaStream_t s, const double* r, double* z, const int* stop) {
+    using namespace irk;
+    const int N = dst_N;
+    launch(k_dst_rows<L, false>, N / 2, L / 8, (size_t)L * 16, s, N, r, dst_T, r, dst_tw, stop);
+    launch(k_dst_cols<L>, N / 4, L / 4, (size_t)2 * L * 16, s, N, dst_T, dstS, dst_cos, dst_tw,
+           stop);
+    launch(k_dst_rows<L, true>, N / 2, L / 8, (size_t)L * 16, s, N, dst_T, z, r, dst_tw, stop);
+    ctx->launches += 3;
+    return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
+  }
+  // z = B_s^-1 r (r != z)
+  int apply_dst(irk_ctx* ctx, cudaStream_t s, const double* r, double* z, const int* stop) {
+    switch (2 * dst_N) {
+      case 64: return apply_dst_l<64>(ctx, s, r, z, stop);
+      case 128: return apply_dst_l<128>(ctx, s, r, z, stop);
+      case 256: return apply_dst_l<256>(ctx, s, r, z, stop);
+      case 512: return apply_dst_l<512>(ctx, s, r, z, stop);
+      case 1024: return apply_dst_l<1024>(ctx, s, r, z, stop);
+      case 2048: return apply_dst_l<2048>(ctx, s, r, z, stop);
+      case 4096: return apply_dst_l<4096>(ctx, s, r, z, stop);
+    }
+    irk::set_error("irk_mg: no sine-transform plan");
+    return IRK_EINVAL;
+  }
 
   // Chebyshev coefficients (cd_k, cr_k) of steps k = 0..n-1 on [lo, hi]
   static void cheb(double lo, double hi, int n, std::vector<double>& cd, std::vector<double>& cr) {
@@ -1268,7 +1373,7 @@ struct irk_mg : public irk::CgPrec {
   // top-level post-smoother's CTAs write the r.z partials
   int fused_rz_count() override {
     static const bool off = getenv("IRK_MG_NOFUSE") || getenv("IRK_CG_NOFUSE");
-    if (off || !s2_on || lev.size() < 2) return 0;
+    if (off || !s2_on || dst_on || lev.size() < 2) return 0;
     const int N = (int)lev[0].g.n1 - 1;
     return N >= 512 ? ((N + irk::kBTX - 1) / irk::kBTX) * ((N + irk::kBTY - 1) / irk::kBTY)
                     : ((N + 31) / 32) * ((N + 7) / 8);
@@ -1287,6 +1392,14 @@ struct irk_mg : public irk::CgPrec {
 
   int apply(irk_ctx* ctx, cudaStream_t s, const double* r, double* z,
             const int* stop) override {
+    if (dst_on) {
+      const int e = apply_dst(ctx, s, r, z, stop);
+      if (e != IRK_OK || cudaGetLastError() != cudaSuccess) {
+        irk::set_error("irk_mg: sine-transform preconditioner launch failed");
+        return IRK_ECUDA;
+      }
+      return IRK_OK;
+    }
     if (s2_on) {
       const int e = vcycle2(ctx, s, 0, r, z, stop);
       if (e != IRK_OK || cudaGetLastError() != cudaSuccess) {
@@ -1305,6 +1418,7 @@ struct irk_mg : public irk::CgPrec {
 
   ~irk_mg() override {
     if (mem) cudaFree(mem);
+    if (dst_mem) cudaFree(dst_mem);
   }
 };
 
@@ -1406,6 +1520,11 @@ int irk_mg_create(irk_ctx* ctx, int dim, int nlev, const int64_t* N_host,
     }
     static const bool generic = getenv("IRK_MG_GENERIC") != nullptr;
     mg->s2_on = mg->s2_ok && !generic;
+    const int ed = mg->setup_dst(ctx);
+    if (ed != IRK_OK) {
+      delete mg;
+      return ed;
+    }
     if (mg->s2_ok) {
       // dynamic shared memory of the single-CTA coarsest kernel (2 buffers)
       const int sh4 = 2 * 4 * 1024 * (int)sizeof(double);
@@ -1437,6 +1556,26 @@ int irk_mg_set_structured(irk_mg* mg, int on) {
     mg->s2_on = on != 0;
     mg->uid = g_mg_uid.fetch_add(1);  // cached graphs hold the other kernel sequence
   }
+  return IRK_OK;
+}
+
+int irk_mg_set_dst(irk_mg* mg, int on) {
+  IRK_REQUIRE(mg, "irk_mg_set_dst: NULL argument");
+  IRK_REQUIRE(!on || mg->dst_ok,
+              "irk_mg_set_dst: no sine-transform preconditioner for this block (needs a verified "
+              "2D grid stencil with the full-boundary Dirichlet set, N a power of two in "
+              "[32, 2048], positive symmetrised eigenvalues)");
+  if ((on != 0) != mg->dst_on) {
+    mg->dst_on = on != 0;
+    mg->uid = g_mg_uid.fetch_add(1);  // cached graphs hold the other kernel sequence
+  }
+  return IRK_OK;
+}
+
+int irk_mg_dst_info(const irk_mg* mg, int* available, int* on) {
+  IRK_REQUIRE(mg, "irk_mg_dst_info: NULL argument");
+  if (available) *available = mg->dst_ok ? 1 : 0;
+  if (on) *on = mg->dst_on ? 1 : 0;
   return IRK_OK;
 }
 

@@ -171,7 +171,7 @@ class StagePreconditioner:
             return False
         if meth in ("direct", "chebyshev"):
             return True
-        if meth not in ("auto", "mg"):
+        if meth not in ("auto", "mg", "dst"):
             return False
         facs = list(self.block_factors)
         if all(f.direct for f in facs):
@@ -187,7 +187,7 @@ class StagePreconditioner:
         terms, deferred status, every block on its hierarchy."""
         if not self.defer_solves or self.settings.raise_on_maxit or self.s < 2:
             return False
-        if any(c is not None for c in coefs) or self.settings.method not in ("auto", "mg"):
+        if any(c is not None for c in coefs) or self.settings.method not in ("auto", "mg", "dst"):
             return False
         return all(f._mg is not None and not f.direct for f in self.block_factors)
 
@@ -448,7 +448,7 @@ def build_preconditioner(kind: PreconditionerKind, tab: ButcherTableau, M: Spars
         # the pair blocks are complex symmetric: COCG (multigrid or Jacobi)
         raise ValueError(f"block method {st.method!r} is not available for the Schur "
                          "preconditioner's complex pair blocks (use 'auto', 'mg' or 'pcg')")
-    if shift is not None and st.method in ("direct", "chebyshev", "mg"):
+    if shift is not None and st.method in ("direct", "chebyshev", "mg", "dst"):
         raise ValueError(f"block method {st.method!r} cannot include the diagonal shift of "
                          "the semilinear surrogate blocks (use 'auto' or 'pcg')")
 

@@ -578,9 +578,13 @@ DIRECT_MAX = 2048
 class BlockSolveSettings:
     """Inner diagonal-block solver (replaces SuperLU, sparsela.py:149-191).
 
-    method: "auto" (a direct solve for blocks of at most DIRECT_MAX rows,
-    multigrid-preconditioned CG for larger blocks of P1 grid operators,
-    Jacobi-PCG otherwise), "direct" (the block inverse, formed once on the
+    method: "auto" (a direct solve for blocks of at most DIRECT_MAX rows;
+    for larger blocks of P1 grid operators CG preconditioned by the fast
+    sine transform where it applies (2D, full-boundary Dirichlet set, N a
+    power of two <= 2048: the symmetrised grid stencil inverted exactly by
+    DST-I, ~2 iterations to 1e-6), else by a multigrid V-cycle;
+    Jacobi-PCG otherwise), "dst" (sine-transform-preconditioned CG
+    required), "direct" (the block inverse, formed once on the
     device, applied by one dense matrix-vector kernel: the exact solve of
     the reference's SuperLU factorisation at sizes where the iterative
     solvers are launch-latency-bound), "mg" (multigrid required), "pcg"
@@ -607,10 +611,13 @@ class BlockSolveSettings:
     mg_coarse_ratio: float = 0.5
 
     def __post_init__(self):
-        if self.method not in ("auto", "pcg", "mg", "chebyshev", "direct"):
+        if self.method not in ("auto", "pcg", "mg", "dst", "chebyshev", "direct"):
             raise ValueError(f"unknown block solver {self.method!r}")
         if self.rtol < 0 or self.atol < 0 or self.maxit < 0 or self.cheb_iters < 0:
             raise ValueError("block solver tolerances must be non-negative")
+
+
+_DST_OFF = bool(os.environ.get("IRK_NO_DST"))  # A/B: multigrid V-cycle under "auto"
 
 
 class _MgHierarchy:
@@ -694,6 +701,24 @@ class _MgHierarchy:
     def structured(self, on: bool):
         call("irk_mg_set_structured", self.handle, int(bool(on)))
 
+    @property
+    def dst_available(self) -> bool:
+        ok = C.c_int()
+        call("irk_mg_dst_info", self.handle, C.byref(ok), None)
+        return bool(ok.value)
+
+    @property
+    def dst(self) -> bool:
+        """True when CG is preconditioned by the fast sine transform of the
+        level-0 block (irk_dst.cuh) instead of the V-cycle."""
+        on = C.c_int()
+        call("irk_mg_dst_info", self.handle, None, C.byref(on))
+        return bool(on.value)
+
+    @dst.setter
+    def dst(self, on: bool):
+        call("irk_mg_set_dst", self.handle, int(bool(on)))
+
 
 class _MgcHierarchy:
     """Complex multigrid of a Schur-pair block alpha*M + beta*K (complex
@@ -734,7 +759,7 @@ class _MgcHierarchy:
         grid = getattr(M, "_p1_grid", None)
         if grid is None or getattr(K, "_p1_grid", None) != grid or abs(alpha) == 0:
             return None
-        if settings.method not in ("auto", "mg"):
+        if settings.method not in ("auto", "mg", "dst"):
             return None
         dim, N = grid
         torch = _torch()
@@ -819,12 +844,19 @@ class BlockFactorization:
             self._cheb = self._chebyshev_bounds()
         elif self.direct:
             pass
-        elif meth in ("auto", "mg"):
+        elif meth in ("auto", "mg", "dst"):
             self._mg = _MgHierarchy.build(M, K, self.alpha, self.beta, self.mask, B,
                                           self.settings)
-            if self._mg is None and self.settings.method == "mg":
-                raise ValueError("multigrid block solver needs M, K from assemble_p1 "
+            if self._mg is None and meth != "auto":
+                raise ValueError(f"{meth!r} block solver needs M, K from assemble_p1 "
                                  "(nested structured-grid P1 operators)")
+            if self._mg is not None and meth in ("auto", "dst") and not _DST_OFF:
+                if self._mg.dst_available:
+                    self._mg.dst = True
+                elif meth == "dst":
+                    raise ValueError("sine-transform block solver needs a 2D P1 grid block with "
+                                     "the full-boundary Dirichlet set and N a power of two in "
+                                     "[32, 2048]")
 
     def _chebyshev_bounds(self):
         """[lmin, lmax] of D^-1 B from Gershgorin discs (irk_mat_absrowsum):
@@ -926,7 +958,7 @@ class BlockFactorization:
         one = np.ones(8)
         defer = defer and (checked or not st.raise_on_maxit)
         its_p, rel_p = (None, None) if defer else (hptr(its), hptr(rel))
-        if self._mg is not None and st.method in ("auto", "mg"):
+        if self._mg is not None and st.method in ("auto", "mg", "dst"):
             status = _lib.load().irk_mg_pcg(
                 ctx(), self._mg.handle, ptr(rhs), int(ld_rhs), ptr(x), int(ld_x),
                 float(st.rtol), float(st.atol), int(st.maxit), its_p, rel_p)

@@ -736,6 +736,72 @@ def test_forked_block_and_pair_solves_match_sequential(cuda, irk):
     assert torch.equal(Z_par, Z_seq)
 
 
+def _dst_prec_host(B, N, r):
+    """Host restatement of the sine-transform preconditioner (irk_dst.cuh):
+    the reflection-symmetrised interior stencil of B inverted by 2D DST-I,
+    boundary rows identity."""
+    from scipy.fft import dst
+
+    n1 = N + 1
+    c = (N // 2) * n1 + N // 2
+    st = {(dx, dy): B[c, c + dx + dy * n1] for dx in (-1, 0, 1) for dy in (-1, 0, 1)}
+    s00 = st[(0, 0)]
+    s10 = (st[(1, 0)] + st[(-1, 0)]) / 2
+    s01 = (st[(0, 1)] + st[(0, -1)]) / 2
+    s11 = (st[(1, 1)] + st[(-1, -1)] + st[(1, -1)] + st[(-1, 1)]) / 4
+    cs = np.cos(np.pi * np.arange(1, N) / N)
+    lam = s00 + 2 * s10 * cs[None, :] + 2 * s01 * cs[:, None] + 4 * s11 * np.outer(cs, cs)
+    R = r.reshape(n1, n1)
+    T = dst(dst(R[1:N, 1:N], type=1, axis=1), type=1, axis=0) / 4  # scipy DST-I = 2 sum
+    Z = R.copy()
+    Z[1:N, 1:N] = dst(dst(T / lam, type=1, axis=1), type=1, axis=0) / 4 * (2.0 / N) ** 2
+    return Z.reshape(-1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,beta", [(32, 2e-2), (64, 5e-3), (256, 3e-4), (2048, 4.4e-4)])
+def test_dst_preconditioner(cuda, irk, oracle, n, beta):
+    """Fast sine-transform preconditioner (k_dst_rows / k_dst_cols) against
+    its scipy DST-I restatement, and the sine-transform-preconditioned CG
+    block solve against a sparse direct solve, in a handful of iterations."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+
+    from paper_2403_08084_b200 import _lib
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(2, n))
+    m = M.nrows
+    fac = la.BlockFactorization(M, K, 1.0, beta, bd,
+                                la.BlockSolveSettings(method="dst", rtol=1e-10,
+                                                      raise_on_maxit=True))
+    assert fac._mg is not None and fac._mg.dst
+    Mo, Ko = oracle.p1_matrices(2, n)
+    keep = np.ones(m)
+    keep[bd] = 0.0
+    D, I = sp.diags(keep), sp.diags(1.0 - keep)
+    A = (D @ (Mo + beta * Ko) @ D + I).tocsr()
+    rng = np.random.default_rng(n)
+    r = rng.standard_normal(m)
+    z = la.dev_empty(m)
+    assert _lib.load().irk_mg_vcycle(_lib.ctx(), fac._mg.handle, _lib.ptr(la.to_dev(r)),
+                                     _lib.ptr(z)) == 0, _lib.last_error()
+    z_ref = _dst_prec_host(A, n, r)
+    assert np.linalg.norm(la.to_host(z) - z_ref) <= 1e-12 * np.linalg.norm(z_ref)
+    if n > 256:
+        return
+    x = fac.solve(r)
+    ref = spla.spsolve(A.tocsc(), r)
+    assert np.linalg.norm(x - ref) <= 1e-8 * np.linalg.norm(ref)
+    assert fac.last_iterations <= (12 if n <= 64 else 5), fac.last_iterations
+    if m <= la.DIRECT_MAX:
+        return  # "auto" solves small blocks directly
+    # "auto" picks it, "mg" keeps the V-cycle
+    assert la.BlockFactorization(M, K, 1.0, beta, bd)._mg.dst
+    assert not la.BlockFactorization(M, K, 1.0, beta, bd,
+                                     la.BlockSolveSettings(method="mg"))._mg.dst
+
+
 @pytest.mark.gpu
 def test_mg_hierarchy_1d_and_masks(cuda, irk, oracle):
     """1D P1 blocks get a hierarchy; a non-boundary Dirichlet set or a
