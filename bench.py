@@ -206,7 +206,12 @@ def inner_solve_profile(wl, peak, reps=20):
       SpMV on slot-uniform values): 80*m for the CG vectors (SpMV reads z,
       p_old, writes p_new, q: 32 B; update reads p, q, x, r, writes x, r:
       48 B) + per V-cycle level 62*m_l (pre 16, restriction 20, post 26) and
-      16*m_L on the single-CTA coarsest level."""
+      16*m_L on the single-CTA coarsest level.
+      sine-transform-preconditioned CG (2D real): the 80*m of the CG vectors
+      + 3 transform kernels reading and writing the grid once (48*m).
+      sine-transform-preconditioned COCG (3D complex pair blocks, config 3):
+      160*m for the complex CG vectors + 5 line-transform kernels reading
+      and writing the complex grid once (160*m)."""
     import torch
 
     from paper_2403_08084_b200 import sparsela as la
@@ -220,8 +225,10 @@ def inner_solve_profile(wl, peak, reps=20):
         sett = fac.settings
     else:
         pc = st._preconditioner(_SPLIT[st.formulation], prob)
-        if pc is None or pc.kind.name == "SCHUR":
+        if pc is None:
             return None
+        if pc.kind.name == "SCHUR":
+            return pair_solve_profile(pc, prob, peak, reps)
         fac = pc.block_factors[0]
         sett = pc.settings
     if fac.direct:
@@ -242,7 +249,10 @@ def inner_solve_profile(wl, peak, reps=20):
     per_it = t / max(its / reps, 1)
     mg = getattr(fac, "_mg", None)
     nnz = prob.mass.nnz
-    if mg is not None and mg.structured:
+    if mg is not None and mg.dst:
+        b_it = 80 * m + 48 * m
+        kind = "sine-transform-preconditioned CG (2D DST-I of the symmetrised stencil)"
+    elif mg is not None and mg.structured:
         dim, N = prob.mass._p1_grid
         ms = [((N >> l) + 1) ** dim for l in range(mg.levels)]
         b_it = 80 * m + sum(62 * v for v in ms[:-1]) + 16 * ms[-1]
@@ -261,9 +271,72 @@ def inner_solve_profile(wl, peak, reps=20):
             "bound": "hbm", "algorithmic_bytes_per_iteration": int(b_it),
             "achieved": b_it / per_it / 1e9, "peak": peak, "unit": "GB/s",
             "frac": b_it / per_it / 1e9 / peak,
-            "note": "per CG iteration incl. one V-cycle; the working set (<= 8 vectors of "
+            "note": "per CG iteration incl. one preconditioner application; the working set (<= 8 vectors of "
                     f"{m * 8 / 1e6:.1f} MB) is largely L2-resident, so HBM is an upper "
                     "bound on the traffic, not the binding limit"}
+    return out
+
+
+def pair_solve_profile(pc, prob, peak, reps=20):
+    """Config 3: one COCG solve of the first Gauss-Legendre Schur-pair block
+    (complex alpha M + beta K) to the preconditioner's inner tolerance, timed
+    like inner_solve_profile (irk_mgc_cocg through the C ABI)."""
+    import torch
+
+    from paper_2403_08084_b200 import _lib
+    from paper_2403_08084_b200 import sparsela as la
+
+    plan = pc._schur_plan()
+    if not plan["np"]:
+        return None
+    Md, Kd = [d.eliminated(pc.mask()) for d in pc._device_mats()]
+    mgc = pc._schur_mg(plan, Md, Kd)
+    if mgc is None:
+        return None
+    h = mgc[0]
+    m = prob.m
+    sett = pc.settings
+    b = la.to_dev(np.random.default_rng(1).standard_normal(2 * m))
+    x = la.dev_empty(2 * m)
+    its = np.zeros(1, dtype=np.int32)
+    rel = np.zeros(1)
+    lib = _lib.load()
+
+    def solve():
+        st = lib.irk_mgc_cocg(_lib.ctx(), h.handle, _lib.ptr(b), 2, _lib.ptr(x), 2,
+                              float(sett.rtol), float(sett.atol), int(sett.maxit),
+                              _lib.hptr(its), _lib.hptr(rel))
+        if st not in (0, _lib.IRK_ENOCONV):
+            raise RuntimeError(_lib.last_error())
+        return int(its[0])
+
+    solve()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    n_it = sum(solve() for _ in range(reps))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 1e3 / reps
+    per_it = t / max(n_it / reps, 1)
+    if h.dst:
+        kind = "sine-transform-preconditioned COCG (3D complex DST-I of the symmetrised stencil)"
+        b_it = 160 * m + 160 * m
+    else:
+        kind = ("multigrid-COCG (structured 3D complex V-cycle)" if h.structured else
+                "multigrid-COCG (generic complex V-cycle)")
+        b_it = None
+    out = dict(m=m, iterations_per_solve=n_it / reps, rtol=sett.rtol, method=kind,
+               mg_levels=h.levels, us_per_solve=t * 1e6, us_per_iteration=per_it * 1e6)
+    if b_it is not None:
+        out["roofline"] = {
+            "bound": "hbm", "algorithmic_bytes_per_iteration": int(b_it),
+            "achieved": b_it / per_it / 1e9, "peak": peak, "unit": "GB/s",
+            "frac": b_it / per_it / 1e9 / peak,
+            "note": "per COCG iteration incl. one preconditioner application; the working "
+                    f"set (complex vectors of {m * 16 / 1e6:.1f} MB) is largely L2-resident, "
+                    "so HBM is an upper bound on the traffic, not the binding limit"}
     return out
 
 

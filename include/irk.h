@@ -428,6 +428,21 @@ int irk_mgc_destroy(irk_mgc* mg);
  * or off, and query the hierarchy. */
 int irk_mgc_set_structured(irk_mgc* mg, int on);
 int irk_mgc_info(const irk_mgc* mg, int* nlev, int* structured);
+/* Fast sine-transform preconditioner of the level-0 pair block (replaces the
+ * complex V-cycle inside irk_mgc_cocg when on): the level-0 3x3x3 stencil,
+ * averaged over the reflections of every offset, inverted exactly by 3D
+ * DST-I (shared-memory mixed-radix FFTs of length 2N, five line-transform
+ * launches), B_s^-1 = (2/N)^3 F Lambda^-1 F with complex Lambda.  Available
+ * for verified 3D grid stencils with the full-boundary Dirichlet set and
+ * 2N = 2^a or 3 * 2^a in [24, 384].  Stands where the reference's exact
+ * block solve does (sparsela.py:171-191): COCG on the block to the requested
+ * tolerance. */
+int irk_mgc_set_dst(irk_mgc* mg, int on);
+/* One application z = P^-1 r of the pair block's preconditioner (the V-cycle,
+ * or the sine transform when on); r, z interleaved complex, contiguous,
+ * 16-byte aligned, r != z. */
+int irk_mgc_vcycle(irk_ctx* ctx, irk_mgc* mg, const double* r_dev, double* z_dev);
+int irk_mgc_dst_info(const irk_mgc* mg, int* available, int* on);
 /* COCG on the level-0 block preconditioned by one complex V-cycle per
  * iteration; rhs/x interleaved complex (re, im) with leading dimensions in
  * doubles (even), 16-byte aligned; status and deferred logging as irk_pcg. */

@@ -102,6 +102,9 @@ _SIGS = {
     "irk_mg_info": [_vp, _vp, _vp],
     "irk_mg_set_dst": [_vp, _int],
     "irk_mg_dst_info": [_vp, _vp, _vp],
+    "irk_mgc_set_dst": [_vp, _int],
+    "irk_mgc_vcycle": [_vp, _vp, _vp, _vp],
+    "irk_mgc_dst_info": [_vp, _vp, _vp],
     "irk_mg_pcg_multi": [_vp, _int, _vp, _vp, _i64, _i64, _vp, _i64, _i64, _dbl, _dbl, _int, _vp,
                          _vp],
     "irk_mgc_cocg_multi": [_vp, _int, _vp, _vp, _i64, _i64, _vp, _i64, _i64, _dbl, _dbl, _int,

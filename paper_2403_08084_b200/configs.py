@@ -21,12 +21,13 @@ DESCRIPTIONS = {
     1: "2D heat P1 32x32, RadauIIA s=2, stage-derivative (AI), dt=1/32, 10 steps, "
        "GMRES 1e-12, block-Jacobi",
     2: "2D heat P1 1024x1024 (~1.05M DOFs), RadauIIA s=3, stage-value, dt=1e-3, 20 steps, "
-       "GMRES 1e-12, block-Gauss-Seidel, inner multigrid-PCG 1e-6 (SuperLU blocks in the "
-       "reference)",
+       "GMRES 1e-12, block-Gauss-Seidel, inner sine-transform-preconditioned CG 1e-6 "
+       "(SuperLU blocks in the reference)",
     3: "3D heat P1 96^3 Kuhn tets (~0.91M DOFs), Gauss-Legendre s=4, DAE Dirichlet "
-       "exp(-t)sin(pi x), dt=5e-3, 10 steps, GMRES 1e-12, real-Schur block-diagonal",
+       "exp(-t)sin(pi x), dt=5e-3, 10 steps, GMRES 1e-12, real-Schur block-diagonal, inner "
+       "sine-transform-preconditioned COCG 1e-6 on the complex pair blocks",
     4: "2D heat P1 2048x2048 (~4.2M DOFs), Alexander SDIRK, dt=1e-3, 50 steps, one reused "
-       "stage operator, multigrid-PCG 1e-12",
+       "stage operator, sine-transform-preconditioned CG 1e-12",
     5: "Allen-Cahn eps=0.02 P1 1024x1024, Neumann, RadauIIA s=3, AI, dt=1e-3, 20 steps, "
        "Newton atol 1e-10, GMRES 1e-10, block-Jacobi (surrogate blocks, inner Jacobi-PCG 1e-2)",
 }

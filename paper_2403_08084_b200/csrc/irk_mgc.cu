@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "irk_inner.cuh"
+#include "irk_dst3.cuh"
 
 namespace irk {
 namespace {
@@ -604,6 +605,79 @@ struct irk_mgc : public irk::CgPrec {
   bool s3_on = false, s3_ok = false;
   std::vector<irk::Sten3> s3;
   std::vector<irk::Cheb2c> c3;
+  // fast sine-transform preconditioner of the level-0 block (irk_dst3.cu):
+  // available / in use instead of the V-cycle
+  bool dst_ok = false, dst_on = false;
+  irk::Dst3Plan dstP{};
+  void* dst_mem = nullptr;
+
+  // Set up the sine-transform preconditioner on the verified level-0 stencil
+  // (structured path available): the stencil averaged over the reflections
+  // of every offset, its eigenvalues bounded away from zero on all modes.
+  int setup_dst3(irk_ctx* ctx) {
+    using namespace irk;
+    dst_ok = false;
+    if (!s3_ok || dim != 3) return IRK_OK;
+    const int N = (int)lev[0].g.n1 - 1;
+    if (!dst3_supported(N)) return IRK_OK;
+    Dst3Coef C{};
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const cplx c = s3[0].c[(dz + 1) * 9 + (dy + 1) * 3 + dx + 1];
+          const int a = dx != 0, b = dy != 0, e = dz != 0;
+          const double w = 1.0 / (double)(1 << (a + b + e));
+          C.s[a + 2 * b + 4 * e].x += w * c.re;
+          C.s[a + 2 * b + 4 * e].y += w * c.im;
+        }
+    C.sc = 8.0 / ((double)N * (double)N * (double)N);
+    std::vector<double> ck(N + 1);
+    for (int k = 0; k <= N; ++k) ck[k] = std::cos(M_PI * (double)k / N);
+    double lo = INFINITY, hi = 0.0;
+    for (int kz = 1; kz < N; ++kz)
+      for (int ky = 1; ky < N; ++ky) {
+        const double tz = 2 * ck[kz], ty = 2 * ck[ky];
+        double pr[2], qr[2];
+        for (int c = 0; c < 2; ++c) {
+          auto S = [&](int i) { return c == 0 ? C.s[i].x : C.s[i].y; };
+          pr[c] = S(0) + S(2) * ty + S(4) * tz + S(6) * ty * tz;
+          qr[c] = S(1) + S(3) * ty + S(5) * tz + S(7) * ty * tz;
+        }
+        for (int kx = 1; kx < N; ++kx) {
+          const double tx = 2 * ck[kx];
+          const double re = pr[0] + qr[0] * tx, im = pr[1] + qr[1] * tx;
+          const double a2 = re * re + im * im;
+          lo = std::fmin(lo, a2);
+          hi = std::fmax(hi, a2);
+        }
+      }
+    if (!(lo > 1e-24 * hi) || !std::isfinite(hi)) return IRK_OK;
+    const int L = 2 * N;
+    const size_t n1 = (size_t)N + 1;
+    const size_t bytes = (n1 * n1 * n1 + (size_t)L) * sizeof(double2) + (n1 + 8) * sizeof(double);
+    if (!dst_mem) IRK_CUDA(cudaMalloc(&dst_mem, bytes));
+    double2* T = reinterpret_cast<double2*>(dst_mem);
+    double2* tw = T + n1 * n1 * n1;
+    double* cosk = reinterpret_cast<double*>(tw + L);
+    std::vector<double> host(2 * (size_t)L + n1);
+    for (int q = 0; q < L; ++q) {
+      const double a = -2.0 * M_PI * (double)q / (double)L;
+      host[2 * q] = std::cos(a);
+      host[2 * q + 1] = std::sin(a);
+    }
+    for (int k = 0; k <= N; ++k) host[2 * (size_t)L + k] = ck[k];
+    IRK_CUDA(cudaMemcpyAsync(tw, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    IRK_CUDA(cudaStreamSynchronize(ctx->stream));
+    IRK_TRY(dst3_prepare(N));
+    dstP.N = N;
+    dstP.C = C;
+    dstP.T = T;
+    dstP.tw = tw;
+    dstP.cosk = cosk;
+    dst_ok = true;
+    return IRK_OK;
+  }
 
   int setup_s3(irk_ctx* ctx) {
     using namespace irk;
@@ -843,6 +917,15 @@ struct irk_mgc : public irk::CgPrec {
   }
 
   int apply(irk_ctx* ctx, cudaStream_t s, const double* r, double* z, const int* stop) override {
+    if (dst_on) {
+      const int e = irk::dst3_apply(ctx, s, dstP, reinterpret_cast<const double2*>(r),
+                                    reinterpret_cast<double2*>(z), stop);
+      if (e != IRK_OK || cudaGetLastError() != cudaSuccess) {
+        irk::set_error("irk_mgc: sine-transform preconditioner launch failed");
+        return IRK_ECUDA;
+      }
+      return IRK_OK;
+    }
     if (s3_on) {
       const int e = vcycle3(ctx, s, 0, reinterpret_cast<const irk::cplx*>(r),
                             reinterpret_cast<irk::cplx*>(z), stop);
@@ -864,6 +947,7 @@ struct irk_mgc : public irk::CgPrec {
 
   ~irk_mgc() override {
     if (mem) cudaFree(mem);
+    if (dst_mem) cudaFree(dst_mem);
   }
 };
 
@@ -958,7 +1042,34 @@ int irk_mgc_create(irk_ctx* ctx, int dim, int nlev, const int64_t* N_host,
     L.lmax = mx;
   }
   IRK_TRY(mg->setup_s3(ctx));
+  {
+    const int ed = mg->setup_dst3(ctx);
+    if (ed != IRK_OK) {
+      delete mg;
+      return ed;
+    }
+  }
   *out = mg;
+  return IRK_OK;
+}
+
+int irk_mgc_set_dst(irk_mgc* mg, int on) {
+  IRK_REQUIRE(mg, "irk_mgc_set_dst: NULL argument");
+  IRK_REQUIRE(!on || mg->dst_ok,
+              "irk_mgc_set_dst: no sine-transform preconditioner for this block (needs a verified "
+              "3D grid stencil with the full-boundary Dirichlet set and 2N = 2^a or 3 * 2^a in "
+              "[24, 384])");
+  if ((on != 0) != mg->dst_on) {
+    mg->dst_on = on != 0;
+    mg->uid = g_mgc_uid.fetch_add(1);  // cached graphs hold the other kernel sequence
+  }
+  return IRK_OK;
+}
+
+int irk_mgc_dst_info(const irk_mgc* mg, int* available, int* on) {
+  IRK_REQUIRE(mg, "irk_mgc_dst_info: NULL argument");
+  if (available) *available = mg->dst_ok ? 1 : 0;
+  if (on) *on = mg->dst_on ? 1 : 0;
   return IRK_OK;
 }
 
@@ -979,6 +1090,14 @@ int irk_mgc_info(const irk_mgc* mg, int* nlev, int* structured) {
   if (nlev) *nlev = (int)mg->lev.size();
   if (structured) *structured = mg->s3_on ? 1 : 0;
   return IRK_OK;
+}
+
+int irk_mgc_vcycle(irk_ctx* ctx, irk_mgc* mg, const double* r_dev, double* z_dev) {
+  IRK_REQUIRE(ctx && mg && r_dev && z_dev, "irk_mgc_vcycle: NULL argument");
+  IRK_REQUIRE(r_dev != z_dev, "irk_mgc_vcycle: r and z must differ");
+  IRK_REQUIRE(((uintptr_t)r_dev % 16) == 0 && ((uintptr_t)z_dev % 16) == 0,
+              "irk_mgc_vcycle: r/z must be 16-byte aligned");
+  return mg->apply(ctx, ctx->stream, r_dev, z_dev, nullptr);
 }
 
 int irk_mgc_destroy(irk_mgc* mg) {

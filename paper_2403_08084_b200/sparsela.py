@@ -752,6 +752,24 @@ class _MgcHierarchy:
     def structured(self, on: bool):
         call("irk_mgc_set_structured", self.handle, int(bool(on)))
 
+    @property
+    def dst_available(self) -> bool:
+        ok = C.c_int()
+        call("irk_mgc_dst_info", self.handle, C.byref(ok), None)
+        return bool(ok.value)
+
+    @property
+    def dst(self) -> bool:
+        """True when COCG is preconditioned by the 3D fast sine transform of
+        the level-0 block (irk_dst3.cu) instead of the V-cycle."""
+        on = C.c_int()
+        call("irk_mgc_dst_info", self.handle, None, C.byref(on))
+        return bool(on.value)
+
+    @dst.setter
+    def dst(self, on: bool):
+        call("irk_mgc_set_dst", self.handle, int(bool(on)))
+
     @staticmethod
     def build(M, K, Md, Kd, alpha: complex, beta: complex, mask, settings):
         """M, K: the SparseMatrix pair (grid-tagged); Md, Kd: their device
@@ -802,7 +820,15 @@ class _MgcHierarchy:
              C.cast(hk, C.c_void_p), C.cast(mp, C.c_void_p), float(alpha.real),
              float(alpha.imag), float(beta.real), float(beta.imag), nu,
              int(settings.mg_coarse_steps), C.byref(h))
-        return _MgcHierarchy(h, (ms, ks, masks))
+        hier = _MgcHierarchy(h, (ms, ks, masks))
+        if settings.method in ("auto", "dst") and not _DST_OFF:
+            if hier.dst_available:
+                hier.dst = True
+            elif settings.method == "dst":
+                raise ValueError("sine-transform pair-block solver needs a 3D P1 grid block with "
+                                 "the full-boundary Dirichlet set and 2N = 2^a or 3*2^a in "
+                                 "[24, 384]")
+        return hier
 
 
 class BlockFactorization:
