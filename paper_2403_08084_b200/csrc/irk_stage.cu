@@ -910,11 +910,12 @@ int irk_stage_apply(irk_ctx* ctx, int s, const double* C1_host, const double* C2
         // bulk-asynchronous tiles (k_stage_apply_bulk); env IRK_NO_BULK: the
         // per-warp window copies of k_stage_apply_std
         static const bool bulk_off = getenv("IRK_NO_BULK") != nullptr;
-        // (2D stencils: with the 15-point 3D stencil a tile's two stages fill
-        // the shared memory of one 4-warp CTA per SM, slower than the per-warp
-        // copies: 116 vs 80 us at config 3)
-        if (!bulk_off && P->ellw == 7) {
-          const int kT = P->ellw == 15 ? 4 : 8;
+        // (the 15-point 3D stencil: tiles of IRK_BULK3_KT slices, 4 or 6;
+        // IRK_NO_BULK3 keeps the per-warp copies there)
+        static const bool bulk3_off = getenv("IRK_NO_BULK3") != nullptr;
+        static const int bulk3_kt = getenv("IRK_BULK3_KT") ? atoi(getenv("IRK_BULK3_KT")) : 4;
+        if (!bulk_off && (P->ellw == 7 || (P->ellw == 15 && !bulk3_off))) {
+          const int kT = P->ellw == 15 ? (bulk3_kt == 6 ? 6 : 4) : 8;
           BulkLayout BL;
           const int ymis = (int)(((uintptr_t)Y_dev & 15) / 8);
           if (bulk_layout(SL, P->ellw, s, kT, ymis, BL)) {
@@ -926,6 +927,9 @@ int irk_stage_apply(irk_ctx* ctx, int s, const double* C1_host, const double* C2
               if (P->ellw == 7)
                 launch_bulk<7, 8>(ctx, s, m, ns, ntiles, BL, sm, P, M->val, kp.k[0], cf, dt,
                                   rowmask_dev, Y_dev, Out_dev);
+              else if (kT == 6)
+                launch_bulk<15, 6>(ctx, s, m, ns, ntiles, BL, sm, P, M->val, kp.k[0], cf, dt,
+                                   rowmask_dev, Y_dev, Out_dev);
               else
                 launch_bulk<15, 4>(ctx, s, m, ns, ntiles, BL, sm, P, M->val, kp.k[0], cf, dt,
                                    rowmask_dev, Y_dev, Out_dev);

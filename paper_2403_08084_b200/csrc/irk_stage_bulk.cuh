@@ -133,20 +133,52 @@ __global__ void __launch_bounds__(KT * 32)
       const int d = lane < W ? __ldg(colhdr + sl * W + lane) : 0;
       const bool std_slice = __all_sync(0xffffffffu, lane >= W || d == BL.sd[lane < W ? lane : 0]);
       if (std_slice) {
+        // Even S: a row of the window buffer is S*8 bytes (a bulk copy cannot
+        // pad it), so lanes reading stage q of consecutive rows would hit the
+        // same banks 2 (S = 2) or 4 (S = 4) at a time.  Lane l reads its
+        // stages rotated by rot(l) instead (register q holds stage
+        // (q + rot) % S): the 16 lanes of a 64-bit shared-load phase then
+        // cover 16 distinct bank pairs.  The sums are un-rotated below.
+        constexpr bool ROT = S % 2 == 0;
+        const int rot = ROT ? (S == 4 ? (lane >> 2) & 3 : (lane >> 3) & 1) : 0;
+        const double* yq[S];
+#pragma unroll
+        for (int q = 0; q < S; ++q) yq[q] = yb + (ROT ? ((q + rot) & (S - 1)) : q);
 #pragma unroll
         for (int k = 0; k < W; ++k) {
           const double mk = mv[k * kSlice], kk = kv[k * kSlice];
-          const double* yr = yb + (size_t)BL.krow[k] * S;
+          const int ko = BL.krow[k] * S;
 #pragma unroll
           for (int q = 0; q < S; ++q) {
-            const double y = yr[q];
+            const double y = yq[q][ko];
             a[q] += mk * y;
             b[q] += kk * y;
           }
         }
-        const double* yr = yb + (size_t)BL.krow[BL.kc] * S;
+        const int kco = BL.krow[BL.kc] * S;
 #pragma unroll
-        for (int q = 0; q < S; ++q) yc[q] = yr[q];
+        for (int q = 0; q < S; ++q) yc[q] = yq[q][kco];
+        if constexpr (ROT) {
+          // register q holds stage (q + rot) % S: rotate right by rot
+#pragma unroll
+          for (int sh = 1; sh < S; sh <<= 1) {
+            if (rot & sh) {
+              double ta[S], tb[S], tc[S];
+#pragma unroll
+              for (int q = 0; q < S; ++q) {
+                ta[(q + sh) & (S - 1)] = a[q];
+                tb[(q + sh) & (S - 1)] = b[q];
+                tc[(q + sh) & (S - 1)] = yc[q];
+              }
+#pragma unroll
+              for (int q = 0; q < S; ++q) {
+                a[q] = ta[q];
+                b[q] = tb[q];
+                yc[q] = tc[q];
+              }
+            }
+          }
+        }
         done_row = true;
       } else if (r < m) {
 #pragma unroll
