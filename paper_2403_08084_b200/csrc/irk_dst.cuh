@@ -82,25 +82,54 @@ __device__ __forceinline__ void dft8(double2* v) {
   v[7] = c_sub(a3, w3);
 }
 
-// One Stockham pass of radix R over the L-point sequence in buf (in place:
-// every thread first reads all its butterflies, then the block syncs, then
-// writes), NT threads of the calling group (tid in [0, NT)).
-template <int L, int R, int NT>
-__device__ __forceinline__ void fft_pass(double2* buf, int Ns, const double2* __restrict__ tw,
-                                         int tid) {
+// Shared-memory layout of an FFT buffer: element i lives at fpad(i) =
+// i + i / 8 (one 16-byte pad per 8 elements).  A Stockham pass writes its
+// radix-R outputs at stride Ns elements; unpadded, the strided 16-byte
+// stores of the first passes (Ns = 1: lane stride 8 elements = 128 bytes)
+// fall on the same 4 banks (32-way conflict).  With the pad the 8 lanes of a
+// quarter-warp phase cover 8 distinct bank quads in every pass, and the
+// unit-stride reads stay conflict-free.  A buffer of L elements takes
+// fpad_len(L) = L + L / 8 elements.
+__host__ __device__ constexpr int fpad(int i) { return i + (i >> 3); }
+__host__ __device__ constexpr int fpad_len(int L) { return L + (L >> 3); }
+
+// One Stockham pass of radix R, Ns = the product of the earlier radices
+// (compile time), over the L-point sequence in buf (in place: every thread
+// first reads all its butterflies, then the block syncs, then writes), NT
+// threads of the calling group (tid in [0, NT)).  Twiddles: ONE table load
+// w = e^{-2 pi i k / (Ns R)} per butterfly, its powers w^2 .. w^{R-1} by
+// complex multiplications (the R-1 scattered 16-byte loads per butterfly
+// they replace were the kernels' bottleneck: 7 uncoalesced requests per
+// thread and pass).
+template <int L, int R, int NT, int NS>
+__device__ __forceinline__ void fft_pass(double2* buf, const double2* __restrict__ tw, int tid) {
   constexpr int ITEMS = L / R / NT;
   static_assert(ITEMS >= 1 && (L / R) % NT == 0, "fft_pass: bad thread count");
   double2 v[ITEMS][R];
 #pragma unroll
   for (int it = 0; it < ITEMS; ++it) {
     const int j = tid + it * NT;
-    const int k = j % Ns;
-    const int step = k * (L / (Ns * R));
+    const int k = j % NS;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      double2 x = buf[j + r * (L / R)];
-      if (r > 0 && k > 0) x = c_mul(x, __ldg(tw + r * step));
-      v[it][r] = x;
+    for (int r = 0; r < R; ++r) v[it][r] = buf[fpad(j + r * (L / R))];
+    if constexpr (NS > 1) {
+      const double2 w1 = __ldg(tw + k * (L / (NS * R)));
+      if constexpr (R == 2) {
+        v[it][1] = c_mul(v[it][1], w1);
+      } else {
+        const double2 w2 = c_mul(w1, w1), w3 = c_mul(w2, w1);
+        v[it][1] = c_mul(v[it][1], w1);
+        v[it][2] = c_mul(v[it][2], w2);
+        v[it][3] = c_mul(v[it][3], w3);
+        if constexpr (R == 8) {
+          const double2 w4 = c_mul(w2, w2), w5 = c_mul(w4, w1), w6 = c_mul(w3, w3),
+                        w7 = c_mul(w4, w3);
+          v[it][4] = c_mul(v[it][4], w4);
+          v[it][5] = c_mul(v[it][5], w5);
+          v[it][6] = c_mul(v[it][6], w6);
+          v[it][7] = c_mul(v[it][7], w7);
+        }
+      }
     }
     if constexpr (R == 8) dft8(v[it]);
     else if constexpr (R == 4) dft4(v[it][0], v[it][1], v[it][2], v[it][3]);
@@ -110,10 +139,10 @@ __device__ __forceinline__ void fft_pass(double2* buf, int Ns, const double2* __
 #pragma unroll
   for (int it = 0; it < ITEMS; ++it) {
     const int j = tid + it * NT;
-    const int k = j % Ns;
-    const int base = (j / Ns) * Ns * R + k;
+    const int k = j % NS;
+    const int base = (j / NS) * NS * R + k;
 #pragma unroll
-    for (int r = 0; r < R; ++r) buf[base + r * Ns] = v[it][r];
+    for (int r = 0; r < R; ++r) buf[fpad(base + r * NS)] = v[it][r];
   }
   __syncthreads();
 }
@@ -121,32 +150,75 @@ __device__ __forceinline__ void fft_pass(double2* buf, int Ns, const double2* __
 // L / (the largest power of 8 dividing L): the last pass's radix (1: none)
 __host__ __device__ constexpr int fft_rem(int L) { return L % 8 == 0 ? fft_rem(L / 8) : L; }
 
-// Forward FFT of L points (power of two, 16 <= L <= 4096) in buf: radix-8
-// passes, then one radix-4 or radix-2 pass for the remainder.
-template <int L, int NT>
+// Forward FFT of L points (power of two, 16 <= L <= 4096) in buf (padded
+// layout): radix-8 passes, then one radix-4 or radix-2 pass for the rest.
+template <int L, int NT, int NS = 1>
 __device__ __forceinline__ void fft_smem(double2* buf, const double2* __restrict__ tw, int tid) {
-  int Ns = 1;
-#pragma unroll
-  for (int p = 8; p <= L; p *= 8) {
-    fft_pass<L, 8, NT>(buf, Ns, tw, tid);
-    Ns *= 8;
+  if constexpr (NS * 8 <= L) {
+    fft_pass<L, 8, NT, NS>(buf, tw, tid);
+    fft_smem<L, NT, NS * 8>(buf, tw, tid);
+  } else if constexpr (L / NS == 4) {
+    fft_pass<L, 4, NT, NS>(buf, tw, tid);
+  } else if constexpr (L / NS == 2) {
+    fft_pass<L, 2, NT, NS>(buf, tw, tid);
   }
-  constexpr int rem = fft_rem(L);
-  if constexpr (rem == 4) fft_pass<L, 4, NT>(buf, Ns, tw, tid);
-  else if constexpr (rem == 2) fft_pass<L, 2, NT>(buf, Ns, tw, tid);
 }
 
+#ifdef IRK_DST_2D  // the 2D kernels (irk_mg.cu, after irk_inner.cuh: SkipCtl, cg_skip_pred)
 // Row DSTs.  Forward (INV = false): rows gy = 1..N-1 of the grid vector src
 // (row stride n1 = N + 1) -> T (row stride N, column k = 1..N-1, column 0
 // zero).  Inverse (INV = true): rows of T -> z (row stride n1), the boundary
 // of z copied from r.  CTA b takes rows 1 + 2b and 2 + 2b (one complex FFT).
+//
+// Fused CG (SkipCtl / rz_part, blocks of at least kBlock threads): the
+// forward kernel takes the skip decision of k_cg_skip itself (every CTA
+// reduces the update kernel's ||r||^2 partials in reduce_partials' order and
+// CTA 0 publishes it for the other transform kernels); the inverse kernel
+// writes one r.z partial per CTA (rz_part[blockIdx.x]) of the rows it
+// writes, so k_cg_dot_rz is not launched.
+template <int NT>
+__device__ __forceinline__ double dst_reduce_rr(const double* part, int G) {
+  static_assert(NT >= kBlock, "dst_reduce_rr: block smaller than kBlock");
+  __shared__ double pred[kBlock / 32];
+  __shared__ double tot;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < kBlock) {
+    double v = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int b = threadIdx.x + c * kBlock;
+      if (b < G) v += __ldcg(part + b);
+    }
+    v = warp_sum(v);
+    if (lane == 0) pred[warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kBlock / 32; ++w) t += pred[w];
+    tot = t;
+  }
+  __syncthreads();
+  return tot;
+}
+
 template <int L, bool INV>
 __global__ void __launch_bounds__(L / 8)
     k_dst_rows(int N, const double* __restrict__ src, double* __restrict__ dst,
-               const double* __restrict__ r, const double2* __restrict__ tw, const int* stop) {
+               const double* __restrict__ r, const double2* __restrict__ tw, const int* stop,
+               SkipCtl sk, double* __restrict__ rz_part) {
   IRK_PDL_ENTER();
-  if (stop && *stop) return;
   constexpr int NT = L / 8;
+  if constexpr (!INV && NT >= kBlock) {
+    if (sk.st) {
+      const double rr = dst_reduce_rr<NT>(sk.rr, sk.G);
+      const bool skip = cg_skip_pred<double>(sk.st, rr, sk.maxit);
+      if (blockIdx.x == 0 && threadIdx.x == 0) sk.st->skip = skip ? 1 : 0;
+      if (skip) return;
+      stop = nullptr;
+    }
+  }
+  if (stop && *stop) return;
   extern __shared__ double2 dst_buf[];
   double2* buf = dst_buf;
   const int n1 = N + 1;
@@ -158,23 +230,36 @@ __global__ void __launch_bounds__(L / 8)
   for (int j = threadIdx.x; j <= N; j += NT) {
     double2 y = make_double2(0.0, 0.0);
     if (j >= 1 && j <= N - 1) y = make_double2(sa[j], hb ? sb[j] : 0.0);
-    buf[j] = y;
-    if (j >= 1 && j <= N - 1) buf[L - j] = make_double2(-y.x, -y.y);
+    buf[fpad(j)] = y;
+    if (j >= 1 && j <= N - 1) buf[fpad(L - j)] = make_double2(-y.x, -y.y);
   }
   __syncthreads();
   fft_smem<L, NT>(buf, tw, threadIdx.x);
   const int dstride = INV ? n1 : N;
   double* da = dst + (size_t)ra * dstride;
   double* db = dst + (size_t)rb * dstride;
+  double rz = 0.0;  // r.z of the points this thread writes (INV, fused CG)
+  const bool want_rz = INV && rz_part != nullptr;
   for (int k = threadIdx.x; k <= N; k += NT) {
     if (k >= 1 && k <= N - 1) {
-      const double2 Y = buf[k];
-      da[k] = -0.5 * Y.y;
-      if (hb) db[k] = 0.5 * Y.x;
+      const double2 Y = buf[fpad(k)];
+      const double za = -0.5 * Y.y, zb = 0.5 * Y.x;
+      da[k] = za;
+      if (hb) db[k] = zb;
+      if (want_rz) {
+        rz += r[(size_t)ra * n1 + k] * za;
+        if (hb) rz += r[(size_t)rb * n1 + k] * zb;
+      }
     } else if (INV) {
       // boundary columns x = 0, x = N of these rows: identity rows
-      da[k] = r[(size_t)ra * n1 + k];
-      if (hb) db[k] = r[(size_t)rb * n1 + k];
+      const double va = r[(size_t)ra * n1 + k];
+      da[k] = va;
+      rz += va * va;
+      if (hb) {
+        const double vb = r[(size_t)rb * n1 + k];
+        db[k] = vb;
+        rz += vb * vb;
+      }
     } else if (k == 0) {
       da[0] = 0.0;
       if (hb) db[0] = 0.0;
@@ -183,9 +268,30 @@ __global__ void __launch_bounds__(L / 8)
   if (INV) {
     // boundary rows y = 0 (first CTA) and y = N (last CTA): identity rows
     if (blockIdx.x == 0)
-      for (int k = threadIdx.x; k <= N; k += NT) dst[k] = r[k];
+      for (int k = threadIdx.x; k <= N; k += NT) {
+        const double v = r[k];
+        dst[k] = v;
+        rz += v * v;
+      }
     if (blockIdx.x == gridDim.x - 1)
-      for (int k = threadIdx.x; k <= N; k += NT) dst[(size_t)N * n1 + k] = r[(size_t)N * n1 + k];
+      for (int k = threadIdx.x; k <= N; k += NT) {
+        const double v = r[(size_t)N * n1 + k];
+        dst[(size_t)N * n1 + k] = v;
+        rz += v * v;
+      }
+    if (want_rz) {
+      // fixed-order block sum (warp trees, then the warps in order)
+      __shared__ double wred[NT / 32 > 0 ? NT / 32 : 1];
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      rz = warp_sum(rz);
+      if (lane == 0) wred[warp] = rz;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < NT / 32; ++w) t += wred[w];
+        rz_part[blockIdx.x] = t;
+      }
+    }
   }
 }
 
@@ -202,26 +308,27 @@ __global__ void __launch_bounds__(L / 4)
   constexpr int NT = L / 8;
   extern __shared__ double2 dst_buf[];
   const int grp = threadIdx.x / NT, tid = threadIdx.x % NT;
-  double2* buf = dst_buf + grp * L;
+  constexpr int LP = fpad_len(L);
+  double2* buf = dst_buf + grp * LP;
   const int k0 = 4 * blockIdx.x;
   // load rows 1..N-1 of the 4 columns: thread t takes column t % 4 of row
   // 1 + t / 4 (one 32-byte sector per row)
   for (int t = threadIdx.x; t < 4 * (N - 1); t += 2 * NT) {
     const int l = 1 + (t >> 2), c = t & 3;
     const double v = T[(size_t)l * N + k0 + c];
-    double2* b = dst_buf + (c >> 1) * L;
+    double2* b = dst_buf + (c >> 1) * LP;
     if (c & 1) {
-      b[l].y = v;
-      b[L - l].y = -v;
+      b[fpad(l)].y = v;
+      b[fpad(L - l)].y = -v;
     } else {
-      b[l].x = v;
-      b[L - l].x = -v;
+      b[fpad(l)].x = v;
+      b[fpad(L - l)].x = -v;
     }
   }
   if (threadIdx.x < 2) {
-    double2* b = dst_buf + threadIdx.x * L;
-    b[0] = make_double2(0.0, 0.0);
-    b[N] = make_double2(0.0, 0.0);
+    double2* b = dst_buf + threadIdx.x * LP;
+    b[fpad(0)] = make_double2(0.0, 0.0);
+    b[fpad(N)] = make_double2(0.0, 0.0);
   }
   __syncthreads();
   fft_smem<L, NT>(buf, tw, tid);
@@ -231,28 +338,30 @@ __global__ void __launch_bounds__(L / 4)
     const double cka = coskn[ka], ckb = coskn[kb];
     const double sc = 4.0 / ((double)N * (double)N);
     for (int l = 1 + tid; l <= N - 1; l += NT) {
-      const double2 Y = buf[l];
+      const double2 Y = buf[fpad(l)];
       const double cl = coskn[l];
       // column 0 is the zero column (Y = 0 there): any nonzero lambda
       const double la = ka == 0 ? 1.0
                                 : S.s00 + 2.0 * S.s10 * cka + cl * (2.0 * S.s01 + 4.0 * S.s11 * cka);
       const double lb = S.s00 + 2.0 * S.s10 * ckb + cl * (2.0 * S.s01 + 4.0 * S.s11 * ckb);
       const double2 y = make_double2(-0.5 * Y.y * sc / la, 0.5 * Y.x * sc / lb);
-      buf[l] = y;
-      buf[L - l] = make_double2(-y.x, -y.y);
+      buf[fpad(l)] = y;
+      buf[fpad(L - l)] = make_double2(-y.x, -y.y);
     }
     if (tid == 0) {
-      buf[0] = make_double2(0.0, 0.0);
-      buf[N] = make_double2(0.0, 0.0);
+      buf[fpad(0)] = make_double2(0.0, 0.0);
+      buf[fpad(N)] = make_double2(0.0, 0.0);
     }
   }
   __syncthreads();
   fft_smem<L, NT>(buf, tw, tid);
   for (int t = threadIdx.x; t < 4 * (N - 1); t += 2 * NT) {
     const int l = 1 + (t >> 2), c = t & 3;
-    const double2 Y = dst_buf[(c >> 1) * L + l];
+    const double2 Y = dst_buf[(c >> 1) * LP + fpad(l)];
     T[(size_t)l * N + k0 + c] = (c & 1) ? 0.5 * Y.x : -0.5 * Y.y;
   }
 }
+
+#endif  // IRK_DST_2D
 
 }  // namespace irk

@@ -1037,6 +1037,9 @@ struct CgPrec {
   // skip decision itself and publishes it in st->skip for the others; the
   // last kernel writes fused_rz_count() partials of r.z to rz_part.
   virtual int fused_rz_count() { return 0; }
+  // CG iterations worth issuing straight-line with the init sequence (the
+  // iterations a typical solve needs; < 0: the default, IRK_CG_PREFIX)
+  virtual int prefix_iters() { return -1; }
   virtual int apply_fused(irk_ctx* ctx, cudaStream_t s, const double* r, double* z,
                           const SkipCtl& sk, double* rz_part) {
     return IRK_EINVAL;
@@ -1288,7 +1291,10 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   static const int prefix_env =
       getenv("IRK_CG_PREFIX") ? std::max(0, atoi(getenv("IRK_CG_PREFIX")) & ~1) : 4;
   static const bool while_off = getenv("IRK_NO_WHILE") != nullptr;  // A/B: chunked graphs
-  const int prefix = (prec && maxit > 0 && !graph_off && !while_off) ? prefix_env : 0;
+  const int prefix_hint = prec && !getenv("IRK_CG_PREFIX") ? prec->prefix_iters() : -1;
+  const int prefix = (prec && maxit > 0 && !graph_off && !while_off)
+                         ? (prefix_hint >= 0 ? (prefix_hint & ~1) : prefix_env)
+                         : 0;
   // The key holds every launch argument of the loop kernels.
   GraphKey key;
   key.add((const void*)&k_cg_spmv<T, NB, HASB, MAXW>).add((const void*)&k_cg_update<T, NB>);

@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "irk_inner.cuh"
+#define IRK_DST_2D
 #include "irk_dst.cuh"
 
 namespace irk {
@@ -1053,11 +1054,13 @@ struct irk_mg : public irk::CgPrec {
   template <int L>
   static int dst_attrs_l() {
     IRK_CUDA(cudaFuncSetAttribute(irk::k_dst_rows<L, false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, L * 16));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  irk::fpad_len(L) * 16));
     IRK_CUDA(cudaFuncSetAttribute(irk::k_dst_rows<L, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, L * 16));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  irk::fpad_len(L) * 16));
     IRK_CUDA(cudaFuncSetAttribute(irk::k_dst_cols<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  2 * L * 16));
+                                  2 * irk::fpad_len(L) * 16));
     return IRK_OK;
   }
   static int dst_attrs(int L) {
@@ -1074,26 +1077,32 @@ struct irk_mg : public irk::CgPrec {
   }
 
   template <int L>
-  int apply_dst_l(irk_ctx* ctx, cudaStream_t s, const double* r, double* z, const int* stop) {
+  int apply_dst_l(irk_ctx* ctx, cudaStream_t s, const double* r, double* z, const int* stop,
+                  const irk::SkipCtl& sk, double* rz_part) {
     using namespace irk;
     const int N = dst_N;
-    launch(k_dst_rows<L, false>, N / 2, L / 8, (size_t)L * 16, s, N, r, dst_T, r, dst_tw, stop);
-    launch(k_dst_cols<L>, N / 4, L / 4, (size_t)2 * L * 16, s, N, dst_T, dstS, dst_cos, dst_tw,
-           stop);
-    launch(k_dst_rows<L, true>, N / 2, L / 8, (size_t)L * 16, s, N, dst_T, z, r, dst_tw, stop);
+    // fused CG: the forward row kernel decides the skip (sk) and publishes
+    // it in sk.st->skip for the other two; the inverse one writes rz_part
+    constexpr size_t kBuf = (size_t)fpad_len(L) * 16;  // one padded FFT buffer
+    launch(k_dst_rows<L, false>, N / 2, L / 8, kBuf, s, N, r, dst_T, r, dst_tw, stop, sk,
+           (double*)nullptr);
+    launch(k_dst_cols<L>, N / 4, L / 4, 2 * kBuf, s, N, dst_T, dstS, dst_cos, dst_tw, stop);
+    launch(k_dst_rows<L, true>, N / 2, L / 8, kBuf, s, N, dst_T, z, r, dst_tw, stop, SkipCtl{},
+           rz_part);
     ctx->launches += 3;
     return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
   }
   // z = B_s^-1 r (r != z)
-  int apply_dst(irk_ctx* ctx, cudaStream_t s, const double* r, double* z, const int* stop) {
+  int apply_dst(irk_ctx* ctx, cudaStream_t s, const double* r, double* z, const int* stop,
+                const irk::SkipCtl& sk = irk::SkipCtl{}, double* rz_part = nullptr) {
     switch (2 * dst_N) {
-      case 64: return apply_dst_l<64>(ctx, s, r, z, stop);
-      case 128: return apply_dst_l<128>(ctx, s, r, z, stop);
-      case 256: return apply_dst_l<256>(ctx, s, r, z, stop);
-      case 512: return apply_dst_l<512>(ctx, s, r, z, stop);
-      case 1024: return apply_dst_l<1024>(ctx, s, r, z, stop);
-      case 2048: return apply_dst_l<2048>(ctx, s, r, z, stop);
-      case 4096: return apply_dst_l<4096>(ctx, s, r, z, stop);
+      case 64: return apply_dst_l<64>(ctx, s, r, z, stop, sk, rz_part);
+      case 128: return apply_dst_l<128>(ctx, s, r, z, stop, sk, rz_part);
+      case 256: return apply_dst_l<256>(ctx, s, r, z, stop, sk, rz_part);
+      case 512: return apply_dst_l<512>(ctx, s, r, z, stop, sk, rz_part);
+      case 1024: return apply_dst_l<1024>(ctx, s, r, z, stop, sk, rz_part);
+      case 2048: return apply_dst_l<2048>(ctx, s, r, z, stop, sk, rz_part);
+      case 4096: return apply_dst_l<4096>(ctx, s, r, z, stop, sk, rz_part);
     }
     irk::set_error("irk_mg: no sine-transform plan");
     return IRK_EINVAL;
@@ -1373,15 +1382,30 @@ struct irk_mg : public irk::CgPrec {
   // top-level post-smoother's CTAs write the r.z partials
   int fused_rz_count() override {
     static const bool off = getenv("IRK_MG_NOFUSE") || getenv("IRK_CG_NOFUSE");
-    if (off || !s2_on || dst_on || lev.size() < 2) return 0;
+    // sine-transform preconditioner: one partial per CTA of the inverse row
+    // kernel (row-kernel blocks of at least kBlock threads: N >= 1024)
+    if (dst_on) return (!off && 2 * dst_N / 8 >= irk::kBlock) ? dst_N / 2 : 0;
+    if (off || !s2_on || lev.size() < 2) return 0;
     const int N = (int)lev[0].g.n1 - 1;
     return N >= 512 ? ((N + irk::kBTX - 1) / irk::kBTX) * ((N + irk::kBTY - 1) / irk::kBTY)
                     : ((N + 31) / 32) * ((N + 7) / 8);
   }
 
+  // the sine-transform-preconditioned CG reaches 1e-6 in 2 iterations (3-4
+  // at 1e-12): issue 2 with the init sequence, the rest from the loop
+  int prefix_iters() override { return dst_on ? 2 : -1; }
+
   int apply_fused(irk_ctx* ctx, cudaStream_t s, const double* r, double* z,
                   const irk::SkipCtl& sk, double* rz_part) override {
     const int* stop = sk.st ? &sk.st->skip : nullptr;
+    if (dst_on) {
+      const int e = apply_dst(ctx, s, r, z, stop, sk, rz_part);
+      if (e != IRK_OK || cudaGetLastError() != cudaSuccess) {
+        irk::set_error("irk_mg: fused sine-transform preconditioner launch failed");
+        return IRK_ECUDA;
+      }
+      return IRK_OK;
+    }
     const int e = vcycle2(ctx, s, 0, r, z, stop, sk, rz_part);
     if (e != IRK_OK || cudaGetLastError() != cudaSuccess) {
       irk::set_error("irk_mg: fused structured V-cycle launch failed");

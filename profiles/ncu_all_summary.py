@@ -14,6 +14,7 @@ from collections import defaultdict
 PEAK = 6546.9  # GB/s, MEASURED_PEAKS.json copy bandwidth (B200 pool)
 _SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9,
           "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "%": 1.0, "": 1.0,
+          "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0,
           "register/thread": 1.0}
 
 
