@@ -58,7 +58,7 @@ int64_t irk_ctx_launch_count(const irk_ctx* ctx);
 /* Deferred inner-solve status.  While enabled, irk_pcg / irk_cocg /
  * irk_mg_pcg called with its_host == relres_host == NULL return IRK_OK
  * without synchronising and append (iterations, code 0 ok / 1 cap /
- * 2 breakdown, loop iterations, kernels per loop pass) to a device log;
+ * 2 breakdown, executed loop passes, kernels per loop pass) to a device log;
  * irk_ctx_log_take copies the entries in call order (synchronous) and
  * clears the log.  Enabling also clears it.  The log grows on demand;
  * irk_ctx_log_size reports the number of pending entries. */

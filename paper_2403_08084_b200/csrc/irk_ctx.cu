@@ -195,8 +195,8 @@ int irk_ctx_log_take(irk_ctx* ctx, int* out_host, int max_entries, int* n_out) {
   }
   IRK_CUDA(cudaStreamSynchronize(ctx->stream));
   for (int i = 0; i < n; ++i) {
-    // kernels executed by graph-resident loops: per pass, (iterations / 2 + 1) passes
-    ctx->launches += (int64_t)out_host[4 * i + 3] * (out_host[4 * i + 2] / 2 + 1);
+    // kernels executed by graph-resident loops: kernels per pass x passes
+    ctx->launches += (int64_t)out_host[4 * i + 3] * out_host[4 * i + 2];
   }
   *n_out = n;
   ctx->log_n = 0;

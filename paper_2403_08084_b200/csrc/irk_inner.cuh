@@ -460,11 +460,13 @@ template <typename T, int NB>
 __device__ __forceinline__ bool cg_enter_a(const SysState<T>* sin, SysState<T>* sout,
                                            double* red, int c, int maxit,
                                            T (&beta)[NB], bool (&act)[NB],
-                                           const double* ext_rz = nullptr, int n_ext = 0) {
+                                           const double* ext_rz = nullptr, int n_ext = 0,
+                                           int G_loop = 0) {
   __shared__ SysState<T> S;
   __shared__ T smu[NB], srz[NB];
   __shared__ double srr[NB];
-  const int G = gridDim.x;
+  // G_loop: the loop kernels' grid when called from another grid (k_cg_settle)
+  const int G = G_loop > 0 ? G_loop : (int)gridDim.x;
   state_copy(&S, sin);
   {
     // issued together with the state loads (unused when the state is fresh
@@ -547,6 +549,34 @@ __device__ __forceinline__ bool cg_enter_a(const SysState<T>* sin, SysState<T>* 
   }
   __syncthreads();
   return done;
+}
+
+// Loop condition with early settlement (external-preconditioner solves, at
+// a parity-0 boundary: after the straight-line prefix iterations and after
+// every WHILE pass).  When the preconditioner application of the last
+// iteration was skipped (sin->skip: the next A kernel will end the solve),
+// this one-CTA kernel takes that A kernel's state transition itself
+// (cg_enter_a over the loop grid's partials: sin -> sout, idempotent) and
+// clears the loop condition, so a finished solve does not run one more
+// WHILE pass of no-op kernels.
+template <typename T, int NB>
+__global__ void __launch_bounds__(kBlock)
+    k_cg_settle(cudaGraphConditionalHandle h, const SysState<T>* sin, SysState<T>* sout,
+                double* red, int G, int maxit, const double* ext_rz, int n_ext) {
+  IRK_PDL_ENTER();
+  __shared__ int sflag[2];
+  if (threadIdx.x == 0) {
+    sflag[0] = __ldcg(&sin->done) || __ldcg(&sout->done);
+    sflag[1] = __ldcg(&sin->skip);
+  }
+  __syncthreads();
+  bool finished = sflag[0] != 0;
+  if (!finished && sflag[1]) {
+    T beta[NB];
+    bool act[NB];
+    finished = cg_enter_a<T, NB>(sin, sout, red, 0, maxit, beta, act, ext_rz, n_ext, G);
+  }
+  if (threadIdx.x == 0) cudaGraphSetConditional(h, finished ? 0u : 1u);
 }
 
 // Prologue of B_k: alpha = rho / mu from A_k's partials; true when finished.
@@ -998,7 +1028,7 @@ __global__ void k_cg_cond(cudaGraphConditionalHandle h, const SysState<T>* a,
 // loop iteration count) of one solve into the context's solve log.
 template <typename T>
 __global__ void k_cg_log(const SysState<T>* a, const SysState<T>* b, int nb, int body_kernels,
-                         int* out) {
+                         int prefix, int settle, int* out) {
   IRK_PDL_ENTER();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const SysState<T>* f = (a->done != b->done) ? (a->done ? a : b) : (a->iter >= b->iter ? a : b);
@@ -1012,7 +1042,10 @@ __global__ void k_cg_log(const SysState<T>* a, const SysState<T>* b, int nb, int
   }
   out[0] = its;
   out[1] = code;
-  out[2] = f->iter;
+  // passes of the graph-resident loop: iterations in pairs after the prefix;
+  // without the settling condition one more pass observes the finished state
+  const int rest = max(f->iter - prefix, 0);
+  out[2] = settle ? (rest + 1) / 2 : rest / 2 + 1;
   out[3] = body_kernels;
 }
 
@@ -1305,12 +1338,23 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   // CG iterations per WHILE pass: even, so every pass starts on parity 0
   static const int body_its =
       getenv("IRK_WHILE_BODY") ? 2 * std::max(1, atoi(getenv("IRK_WHILE_BODY")) / 2) : 2;
+  // the loop condition at a parity-0 boundary: with an external
+  // preconditioner the settling kernel (IRK_NO_SETTLE: the plain condition)
+  static const bool settle_off = getenv("IRK_NO_SETTLE") != nullptr;
+  const bool settle = prec != nullptr && !settle_off;
+  auto launch_cond = [&](cudaStream_t cs, cudaGraphConditionalHandle h) -> int {
+    if (settle)
+      launch(k_cg_settle<T, NB>, 1, kBlock, 0, cs, h, (const SysState<T>*)st1, st0, red, (int)G,
+             maxit, n_ext ? red + red_base + (size_t)n_ext : (const double*)nullptr, n_ext);
+    else
+      launch(k_cg_cond<T>, 1, 32, 0, cs, h, st0, st1);
+    IRK_CHECK_LAUNCH(ctx);
+    return IRK_OK;
+  };
   auto while_body = [&](cudaStream_t cs, cudaGraphConditionalHandle h) -> int {
     // body_its is even: the loop kernels alternate the two state parities
     IRK_TRY(chunk_body(cs, 0, body_its));
-    launch(k_cg_cond<T>, 1, 32, 0, cs, h, st0, st1);
-    IRK_CHECK_LAUNCH(ctx);
-    return IRK_OK;
+    return launch_cond(cs, h);
   };
   static const bool split_while = getenv("IRK_SPLIT_WHILE") != nullptr;  // A/B: two graphs
   bool looped = false;
@@ -1322,12 +1366,15 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
     kc.add(mask).add(w).add(red).add(cnt).add(rtol).add(atol);
     kc.add(prec ? prec->uid : (uint64_t)0).add(prefix).add(stencil).add(maxit).add(n_ext);
     kc.k += key.k;
-    kc.add(2).add(body_its);
+    kc.add(2).add(body_its).add(settle);
     IRK_TRY(graph_launch_prefix_while(
         ctx, kc.k,
-        [&](cudaStream_t cs) -> int {
+        [&](cudaStream_t cs, cudaGraphConditionalHandle h) -> int {
           IRK_TRY(init_body(cs));
-          return chunk_body(cs, 0, prefix);
+          IRK_TRY(chunk_body(cs, 0, prefix));
+          // a solve that finished inside the prefix skips the loop
+          if (settle && prefix > 0) return launch_cond(cs, h);
+          return IRK_OK;
         },
         while_body, &body_kernels));
     looped = true;
@@ -1399,8 +1446,8 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   if (!its_host && !relres_host && ctx->log_on) {
     // deferred status: log the outcome on the device, no host round trip
     IRK_TRY(log_reserve(ctx));
-    launch(k_cg_log<T>, 1, 32, 0, s, st0, st1, NB, (int)body_kernels,
-                                 ctx->solve_log + 4 * ctx->log_n);
+    launch(k_cg_log<T>, 1, 32, 0, s, st0, st1, NB, (int)body_kernels, prefix,
+                                 (int)(settle && looped), ctx->solve_log + 4 * ctx->log_n);
     IRK_CHECK_LAUNCH(ctx);
     ctx->log_n++;
     launch(k_cg_store<T, NB>, grid_for(ctx, m), kBlock, 0, s, m, w.x, xout, ld_x);
@@ -1416,8 +1463,10 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
                           : (hst[0].iter >= hst[1].iter ? hst[0] : hst[1]);
   // body passes executed by the graph-resident loop: iterations in pairs,
   // plus the pass in which the finished state was observed
-  if (body_kernels)
-    ctx->launches += body_kernels * ((int64_t)std::max(fs.iter - prefix, 0) / 2 + 1);
+  if (body_kernels) {
+    const int64_t rest = std::max(fs.iter - prefix, 0);
+    ctx->launches += body_kernels * ((settle && looped) ? (rest + 1) / 2 : rest / 2 + 1);
+  }
   int status = IRK_OK;
   for (int k = 0; k < NB; ++k) {
     if (its_host) its_host[k] = fs.its[k];

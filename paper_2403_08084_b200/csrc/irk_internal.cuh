@@ -325,7 +325,8 @@ int graph_launch_while(irk_ctx* ctx, const std::string& key, F&& body,
 // multigrid-PCG solves, the second launch cost ~150 us of GPU idle per solve
 // (profiles/r02), a sequence in one graph costs a few us.  Cached like
 // graph_launch; the prefix kernels are counted per launch, *body_kernels
-// receives the kernel count of one body pass.
+// receives the kernel count of one body pass.  `pre(stream, handle)` may
+// launch a kernel that sets the loop condition (default 1 at every launch).
 template <class F, class B>
 int graph_launch_prefix_while(irk_ctx* ctx, const std::string& key, F&& pre, B&& body,
                               int64_t* body_kernels) {
@@ -348,9 +349,12 @@ int graph_launch_prefix_while(irk_ctx* ctx, const std::string& key, F&& pre, B&&
     cudaGraphDestroy(graph);
     IRK_CUDA(e);
   }
-  int rc = pre(ctx->cap_stream);
-  // the conditional node joins the capture after the prefix's sink nodes
+  // the handle exists before the prefix is captured: its last kernel may
+  // clear the condition (a solve that finished inside the prefix)
   cudaGraphConditionalHandle h{};
+  e = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault);
+  int rc = e == cudaSuccess ? pre(ctx->cap_stream, h) : IRK_ECUDA;
+  // the conditional node joins the capture after the prefix's sink nodes
   cudaGraphNode_t node = nullptr;
   cudaGraph_t bodyg = nullptr;
   if (rc == IRK_OK) {
@@ -358,8 +362,6 @@ int graph_launch_prefix_while(irk_ctx* ctx, const std::string& key, F&& pre, B&&
     const cudaGraphNode_t* deps = nullptr;
     size_t ndeps = 0;
     e = cudaStreamGetCaptureInfo(ctx->cap_stream, &cst, nullptr, nullptr, &deps, &ndeps);
-    if (e == cudaSuccess)
-      e = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault);
     cudaGraphNodeParams np = {};
     np.type = cudaGraphNodeTypeConditional;
     np.conditional.handle = h;
