@@ -54,12 +54,13 @@ __device__ __forceinline__ void dft3(double2* v) {
   v[2] = c_sub(m, t);
 }
 
-// One Stockham pass of radix R over the L-point sequence in buf, NT threads
-// per sequence (tid in [0, NT)); L / R need not be a multiple of NT.  All
-// threads of the CTA call it together (block-wide barriers).
-template <int L, int R, int NT>
-__device__ __forceinline__ void fft_pass_g(double2* buf, int Ns, const double2* __restrict__ tw,
-                                           int tid) {
+// One Stockham pass of radix R (NS = the product of the earlier radices)
+// over the L-point sequence in buf (padded layout fpad of irk_dst.cuh), NT
+// threads per sequence (tid in [0, NT)); L / R need not be a multiple of NT.
+// All threads of the CTA call it together (block-wide barriers).  One
+// twiddle load per butterfly, its powers by complex multiplications.
+template <int L, int R, int NT, int NS>
+__device__ __forceinline__ void fft_pass_g(double2* buf, const double2* __restrict__ tw, int tid) {
   constexpr int NB = L / R;
   constexpr int ITEMS = (NB + NT - 1) / NT;
   double2 v[ITEMS][R];
@@ -67,13 +68,28 @@ __device__ __forceinline__ void fft_pass_g(double2* buf, int Ns, const double2* 
   for (int it = 0; it < ITEMS; ++it) {
     const int j = tid + it * NT;
     if (j < NB) {
-      const int k = j % Ns;
-      const int step = k * (L / (Ns * R));
+      const int k = j % NS;
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        double2 x = buf[j + r * NB];
-        if (r > 0 && k > 0) x = c_mul(x, __ldg(tw + r * step));
-        v[it][r] = x;
+      for (int r = 0; r < R; ++r) v[it][r] = buf[fpad(j + r * NB)];
+      if constexpr (NS > 1) {
+        const double2 w1 = __ldg(tw + k * (L / (NS * R)));
+        v[it][1] = c_mul(v[it][1], w1);
+        if constexpr (R >= 3) {
+          const double2 w2 = c_mul(w1, w1);
+          v[it][2] = c_mul(v[it][2], w2);
+          if constexpr (R >= 4) {
+            const double2 w3 = c_mul(w2, w1);
+            v[it][3] = c_mul(v[it][3], w3);
+            if constexpr (R == 8) {
+              const double2 w4 = c_mul(w2, w2), w5 = c_mul(w4, w1), w6 = c_mul(w3, w3),
+                            w7 = c_mul(w4, w3);
+              v[it][4] = c_mul(v[it][4], w4);
+              v[it][5] = c_mul(v[it][5], w5);
+              v[it][6] = c_mul(v[it][6], w6);
+              v[it][7] = c_mul(v[it][7], w7);
+            }
+          }
+        }
       }
       if constexpr (R == 8) dft8(v[it]);
       else if constexpr (R == 4) dft4(v[it][0], v[it][1], v[it][2], v[it][3]);
@@ -86,37 +102,36 @@ __device__ __forceinline__ void fft_pass_g(double2* buf, int Ns, const double2* 
   for (int it = 0; it < ITEMS; ++it) {
     const int j = tid + it * NT;
     if (j < NB) {
-      const int k = j % Ns;
-      const int base = (j / Ns) * Ns * R + k;
+      const int k = j % NS;
+      const int base = (j / NS) * NS * R + k;
 #pragma unroll
-      for (int r = 0; r < R; ++r) buf[base + r * Ns] = v[it][r];
+      for (int r = 0; r < R; ++r) buf[fpad(base + r * NS)] = v[it][r];
     }
   }
   __syncthreads();
 }
 
-__host__ __device__ constexpr int f_n8(int L) { return L % 8 == 0 ? 1 + f_n8(L / 8) : 0; }
 __host__ __device__ constexpr int f_rem8(int L) { return L % 8 == 0 ? f_rem8(L / 8) : L; }
-__host__ __device__ constexpr int f_pow8(int n) { return n == 0 ? 1 : 8 * f_pow8(n - 1); }
 
-// Forward FFT of L = 2^a or 3 * 2^a points in buf: radix-8 passes, one
-// radix-4 or radix-2 pass, one radix-3 pass.
-template <int L, int NT>
+// Forward FFT of L = 2^a or 3 * 2^a points in buf (padded layout): radix-8
+// passes, one radix-4 or radix-2 pass, one radix-3 pass.
+template <int L, int NT, int NS = 1>
 __device__ __forceinline__ void fft_smem_g(double2* buf, const double2* __restrict__ tw, int tid) {
-  constexpr int n8 = f_n8(L);
-  constexpr int rem = f_rem8(L);  // 1, 2, 4, 3, 6 or 12
-  constexpr int r2 = rem % 4 == 0 ? 4 : (rem % 2 == 0 ? 2 : 1);
-  constexpr int r3 = rem / r2;
-  static_assert(r3 == 1 || r3 == 3, "fft_smem_g: L must be 2^a or 3 * 2^a");
-  int Ns = 1;
-#pragma unroll
-  for (int p = 0; p < n8; ++p) {
-    fft_pass_g<L, 8, NT>(buf, Ns, tw, tid);
-    Ns *= 8;
+  constexpr int rest = L / NS;  // product of the radices still to do
+  if constexpr (rest % 8 == 0) {
+    fft_pass_g<L, 8, NT, NS>(buf, tw, tid);
+    fft_smem_g<L, NT, NS * 8>(buf, tw, tid);
+  } else if constexpr (rest % 4 == 0) {
+    fft_pass_g<L, 4, NT, NS>(buf, tw, tid);
+    fft_smem_g<L, NT, NS * 4>(buf, tw, tid);
+  } else if constexpr (rest % 2 == 0) {
+    fft_pass_g<L, 2, NT, NS>(buf, tw, tid);
+    fft_smem_g<L, NT, NS * 2>(buf, tw, tid);
+  } else if constexpr (rest == 3) {
+    fft_pass_g<L, 3, NT, NS>(buf, tw, tid);
+  } else {
+    static_assert(rest == 1, "fft_smem_g: L must be 2^a or 3 * 2^a");
   }
-  if constexpr (r2 == 4) fft_pass_g<L, 4, NT>(buf, f_pow8(n8), tw, tid);
-  else if constexpr (r2 == 2) fft_pass_g<L, 2, NT>(buf, f_pow8(n8), tw, tid);
-  if constexpr (r3 == 3) fft_pass_g<L, 3, NT>(buf, f_pow8(n8) * r2, tw, tid);
 }
 
 __device__ __forceinline__ double2 c_div(double2 a, double2 b) {
@@ -141,7 +156,7 @@ __global__ void __launch_bounds__(L)
            const double* __restrict__ cosk, const double2* __restrict__ tw, const int* stop) {
   IRK_PDL_ENTER();
   if (stop && *stop) return;
-  constexpr int N = L / 2, n1 = N + 1, NT = L / 8, LS = L + 1;
+  constexpr int N = L / 2, n1 = N + 1, NT = L / 8, LS = fpad_len(L) + 1;
   constexpr int NI = N - 1;                       // interior points per line
   constexpr int NXG = (NI + kLpc - 1) / kLpc;     // x groups (strided axes)
   static_assert((AXIS == 0) == (MODE == 0 || MODE == 3), "k_dst3: axis/mode combination");
@@ -193,8 +208,8 @@ __global__ void __launch_bounds__(L)
     double2 v = make_double2(0.0, 0.0);
     if (inter) v = src[at];
     double2* b = dst3_buf + q * LS;
-    b[j] = v;
-    if (j >= 1 && j <= NI) b[L - j] = make_double2(-v.x, -v.y);
+    b[fpad(j)] = v;
+    if (j >= 1 && j <= NI) b[fpad(L - j)] = make_double2(-v.x, -v.y);
   }
   __syncthreads();
   fft_smem_g<L, NT>(buf, tw, tid);
@@ -212,15 +227,15 @@ __global__ void __launch_bounds__(L)
       Q = make_double2(0.0, 0.0);
     }
     for (int l = 1 + tid; l <= NI; l += NT) {
-      const double2 Y = buf[l];
+      const double2 Y = buf[fpad(l)];
       const double2 lam = c_fma(Q, 2.0 * cosk[l], P);
       const double2 y = c_div(make_double2(-0.5 * C.sc * Y.y, 0.5 * C.sc * Y.x), lam);
-      buf[l] = y;
-      buf[L - l] = make_double2(-y.x, -y.y);
+      buf[fpad(l)] = y;
+      buf[fpad(L - l)] = make_double2(-y.x, -y.y);
     }
     if (tid == 0) {
-      buf[0] = make_double2(0.0, 0.0);
-      buf[N] = make_double2(0.0, 0.0);
+      buf[fpad(0)] = make_double2(0.0, 0.0);
+      buf[fpad(N)] = make_double2(0.0, 0.0);
     }
     __syncthreads();
     fft_smem_g<L, NT>(buf, tw, tid);
@@ -239,7 +254,7 @@ __global__ void __launch_bounds__(L)
     const int64_t at = locate(q, j, inter);
     if (at < 0) continue;
     if (inter) {
-      const double2 Y = dst3_buf[q * LS + j];
+      const double2 Y = dst3_buf[q * LS + fpad(j)];
       dst[at] = make_double2(-0.5 * Y.y, 0.5 * Y.x);
     } else if constexpr (MODE == 3) {
       dst[at] = r[at];
@@ -249,7 +264,7 @@ __global__ void __launch_bounds__(L)
 
 template <int L>
 int prepare_l() {
-  const int smem = kLpc * (L + 1) * (int)sizeof(double2);
+  const int smem = kLpc * (fpad_len(L) + 1) * (int)sizeof(double2);
   IRK_CUDA(cudaFuncSetAttribute(k_dst3<L, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   IRK_CUDA(cudaFuncSetAttribute(k_dst3<L, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   IRK_CUDA(cudaFuncSetAttribute(k_dst3<L, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -261,7 +276,7 @@ template <int L>
 int apply_l(irk_ctx* ctx, cudaStream_t s, const Dst3Plan& P, const double2* r, double2* z,
             const int* stop) {
   constexpr int N = L / 2, n1 = N + 1, NI = N - 1, NXG = (NI + kLpc - 1) / kLpc;
-  const size_t smem = (size_t)kLpc * (L + 1) * sizeof(double2);
+  const size_t smem = (size_t)kLpc * (fpad_len(L) + 1) * sizeof(double2);
   const double2* T = P.T;
   launch(k_dst3<L, 0, 0>, (NI * NI + kLpc - 1) / kLpc, L, smem, s, r, P.T, r, P.C, P.cosk, P.tw,
          stop);
