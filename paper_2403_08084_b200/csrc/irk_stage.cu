@@ -401,7 +401,7 @@ static bool stencil_layout(const std::vector<int>& sd, StLayout& L) {
 
 // launch k_stage_apply_bulk<s, W, KT> on a persistent grid (resident CTAs
 // per SM from the occupancy API, queried once per instantiation)
-template <int S, int W, int KT>
+template <int S, int W, int KT, int NST>
 static void launch_bulk_s(irk_ctx* ctx, int64_t m, int64_t ns, int64_t ntiles,
                           const BulkLayout& BL, size_t sm, const Pattern* P, const double* mv,
                           const double* kv, const Coef2& cf, double dt, const uint8_t* mask,
@@ -409,26 +409,27 @@ static void launch_bulk_s(irk_ctx* ctx, int64_t m, int64_t ns, int64_t ntiles,
   static int occ = 0;
   static size_t occ_sm = 0;
   if (!occ || occ_sm != sm) {
-    cudaFuncSetAttribute(k_stage_apply_bulk<S, W, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_apply_bulk<S, W, KT>, KT * 32, sm);
+    cudaFuncSetAttribute(k_stage_apply_bulk<S, W, KT, NST>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_apply_bulk<S, W, KT, NST>, KT * 32,
+                                                  sm);
     occ = std::max(occ, 1);
     occ_sm = sm;
   }
   const unsigned gb = (unsigned)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * occ);
-  k_stage_apply_bulk<S, W, KT><<<gb, KT * 32, sm, ctx->stream>>>(
+  k_stage_apply_bulk<S, W, KT, NST><<<gb, KT * 32, sm, ctx->stream>>>(
       m, ns, ntiles, BL, P->sell_col, P->colhdr, mv, kv, cf, dt, mask, Y, Out);
 }
-template <int W, int KT>
+template <int W, int KT, int NST>
 static void launch_bulk(irk_ctx* ctx, int s, int64_t m, int64_t ns, int64_t ntiles,
                         const BulkLayout& BL, size_t sm, const Pattern* P, const double* mv,
                         const double* kv, const Coef2& cf, double dt, const uint8_t* mask,
                         const double* Y, double* Out) {
   switch (s) {
-    case 1: launch_bulk_s<1, W, KT>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
-    case 2: launch_bulk_s<2, W, KT>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
-    case 3: launch_bulk_s<3, W, KT>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
-    default: launch_bulk_s<4, W, KT>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
+    case 1: launch_bulk_s<1, W, KT, NST>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
+    case 2: launch_bulk_s<2, W, KT, NST>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
+    case 3: launch_bulk_s<3, W, KT, NST>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
+    default: launch_bulk_s<4, W, KT, NST>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
   }
 }
 
@@ -915,24 +916,26 @@ int irk_stage_apply(irk_ctx* ctx, int s, const double* C1_host, const double* C2
         static const bool bulk3_off = getenv("IRK_NO_BULK3") != nullptr;
         static const int bulk3_kt = getenv("IRK_BULK3_KT") ? atoi(getenv("IRK_BULK3_KT")) : 4;
         if (!bulk_off && (P->ellw == 7 || (P->ellw == 15 && !bulk3_off))) {
-          const int kT = P->ellw == 15 ? (bulk3_kt == 6 ? 6 : 4) : 8;
+          const bool d3 = P->ellw == 15;
+          const int kT = d3 ? (bulk3_kt == 6 ? 6 : 4) : 8;
+          const int nst = d3 && kT == 4 ? 3 : 2;
           BulkLayout BL;
           const int ymis = (int)(((uintptr_t)Y_dev & 15) / 8);
           if (bulk_layout(SL, P->ellw, s, kT, ymis, BL)) {
             const size_t sm =
-                2 * ((size_t)2 * kT * P->ellw * kSlice + kT * kSlice / 8 + (size_t)BL.rows_total * s) *
+                nst * ((size_t)2 * kT * P->ellw * kSlice + kT * kSlice / 8 + (size_t)BL.rows_total * s) *
                 sizeof(double);
             if (sm <= 200 * 1024) {
               const int64_t ntiles = (ns + kT - 1) / kT;
-              if (P->ellw == 7)
-                launch_bulk<7, 8>(ctx, s, m, ns, ntiles, BL, sm, P, M->val, kp.k[0], cf, dt,
-                                  rowmask_dev, Y_dev, Out_dev);
+              if (!d3)
+                launch_bulk<7, 8, 2>(ctx, s, m, ns, ntiles, BL, sm, P, M->val, kp.k[0], cf, dt,
+                                     rowmask_dev, Y_dev, Out_dev);
               else if (kT == 6)
-                launch_bulk<15, 6>(ctx, s, m, ns, ntiles, BL, sm, P, M->val, kp.k[0], cf, dt,
-                                   rowmask_dev, Y_dev, Out_dev);
+                launch_bulk<15, 6, 2>(ctx, s, m, ns, ntiles, BL, sm, P, M->val, kp.k[0], cf, dt,
+                                      rowmask_dev, Y_dev, Out_dev);
               else
-                launch_bulk<15, 4>(ctx, s, m, ns, ntiles, BL, sm, P, M->val, kp.k[0], cf, dt,
-                                   rowmask_dev, Y_dev, Out_dev);
+                launch_bulk<15, 4, 3>(ctx, s, m, ns, ntiles, BL, sm, P, M->val, kp.k[0], cf, dt,
+                                      rowmask_dev, Y_dev, Out_dev);
               IRK_CHECK_LAUNCH(ctx);
               return IRK_OK;
             }

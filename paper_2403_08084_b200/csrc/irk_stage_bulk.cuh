@@ -10,8 +10,10 @@
 //     rows [R0 + wstart_w, R0 + wstart_w + len_w + (kT-1)*32) of Y
 //     (interleaved m x S: one contiguous range of rows*S doubles),
 // so one elected thread moves the whole tile with 2 + nwin bulk copies into
-// one stage of a double buffer, and the copies of tile t + gridDim.x are in
-// flight while the warps compute tile t (warp = slice, lane = row; every
+// one stage of an NST-stage ring (2 on the 7-point 2D stencil, 3 on the
+// 15-point 3D one: enough bytes in flight per SM with one resident CTA), and
+// the copies of the next NST - 1 tiles are in flight while the warps compute
+// tile t (warp = slice, lane = row; every
 // slot's stage values come from the window buffer, values from the slabs).
 // The DRAM stream is the same as k_stage_apply_std's (values once, Y once
 // plus L2-served window overlap, Out once); what changes is that no warp
@@ -62,7 +64,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
-template <int S, int W, int KT>
+template <int S, int W, int KT, int NST>
 __global__ void __launch_bounds__(KT * 32)
     k_stage_apply_bulk(int64_t m, int64_t nslices, int64_t ntiles, const BulkLayout BL,
                        const int* __restrict__ sell_col,
@@ -72,14 +74,14 @@ __global__ void __launch_bounds__(KT * 32)
                        double* __restrict__ Out) {
   // KT warps: one per slice of the tile
   extern __shared__ __align__(128) double bsm[];
-  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t bar[NST];  // NST pipeline stages (tiles in flight + 1)
   constexpr int VAL = KT * W * kSlice;  // doubles per value slab
   constexpr int MSK = KT * kSlice / 8;  // doubles holding the tile's row-mask bytes
   const int stage_doubles = 2 * VAL + MSK + BL.rows_total * S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+#pragma unroll
+    for (int i = 0; i < NST; ++i) mbar_init(&bar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -104,15 +106,18 @@ __global__ void __launch_bounds__(KT * 32)
                (unsigned)BL.wrows[w] * S * sizeof(double), &bar[st]);
   };
   int64_t t = blockIdx.x;
-  bool pend0 = t < ntiles && interior(t);
-  bool pend1 = t + gridDim.x < ntiles && interior(t + gridDim.x);
-  unsigned ph0 = 0u, ph1 = 0u;
-  if (threadIdx.x == 0) {
-    if (pend0) issue(t, 0);
-    if (pend1) issue(t + gridDim.x, 1);
+  // bit st of pend: stage st holds (or is receiving) a tile; bit st of ph:
+  // the mbarrier phase to wait for
+  unsigned pend = 0u, ph = 0u;
+#pragma unroll
+  for (int i = 0; i < NST; ++i) {
+    const int64_t ti = t + (int64_t)i * gridDim.x;
+    if (ti < ntiles && interior(ti)) {
+      pend |= 1u << i;
+      if (threadIdx.x == 0) issue(ti, i);
+    }
   }
-  for (int i = 0; t < ntiles; t += gridDim.x, ++i) {
-    const int st = i & 1;
+  for (int st = 0; t < ntiles; t += gridDim.x, st = (st + 1 == NST ? 0 : st + 1)) {
     const int64_t sl = t * KT + warp;
     const int64_t r0 = sl * kSlice, r = r0 + lane;
     bool flagged = false;
@@ -120,10 +125,9 @@ __global__ void __launch_bounds__(KT * 32)
 #pragma unroll
     for (int q = 0; q < S; ++q) a[q] = b[q] = yc[q] = 0.0;
     bool done_row = false;
-    if (st ? pend1 : pend0) {
-      mbar_wait(&bar[st], st ? ph1 : ph0);
-      if (st) ph1 ^= 1u;
-      else ph0 ^= 1u;
+    if ((pend >> st) & 1u) {
+      mbar_wait(&bar[st], (ph >> st) & 1u);
+      ph ^= 1u << st;
       const double* base = bsm + (size_t)st * stage_doubles;
       const double* mv = base + warp * W * kSlice + lane;
       const double* kv = base + VAL + warp * W * kSlice + lane;
@@ -228,14 +232,13 @@ __global__ void __launch_bounds__(KT * 32)
     }
     // every warp is done with stage st: refill it with the tile after next
     __syncthreads();
-    const int64_t tn = t + 2 * (int64_t)gridDim.x;
+    const int64_t tn = t + NST * (int64_t)gridDim.x;
     const bool more = tn < ntiles && interior(tn);
     if (threadIdx.x == 0 && more) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       issue(tn, st);
     }
-    if (st) pend1 = more;
-    else pend0 = more;
+    pend = more ? (pend | (1u << st)) : (pend & ~(1u << st));
   }
 }
 
