@@ -19,6 +19,7 @@ Sign convention as in the reference: M u' + K u = f, K positive semidefinite.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 from enum import Enum
 from typing import Callable, Optional
@@ -30,6 +31,7 @@ from . import sparsela as la
 from ._lib import call, ctx, hptr, ptr
 from .bcs import (
     BcMethod,
+    BoundaryPrefetch,
     ConstrainedStageOperator,
     DirichletBC,
     StageUnknown,
@@ -262,6 +264,19 @@ class TimeStepper:
         self._pc_cache = {}
         self._dirk_factors = {}
         self._op_cache = {}
+        # boundary data of the next step evaluated during this step's solve
+        # (bcs.BoundaryPrefetch); False or IRK_BC_PREFETCH=0 turns it off
+        self.bc_prefetch = os.environ.get("IRK_BC_PREFETCH", "1") != "0"
+        self._bc_prefetcher = None
+
+    def _boundary_prefetch(self, problem):
+        bc = problem.dirichlet
+        if (not self.bc_prefetch or not problem.is_linear or bc is None
+                or len(bc.dofs) < BoundaryPrefetch.MIN_DOFS):
+            return None
+        if self._bc_prefetcher is None:
+            self._bc_prefetcher = BoundaryPrefetch()
+        return self._bc_prefetcher
 
     # -- state ------------------------------------------------------------
     @property
@@ -388,6 +403,8 @@ class TimeStepper:
     def step_device(self, problem: SemidiscreteProblem | None = None):
         """One step; returns (u_next as a CUDA tensor, StepReport)."""
         problem = problem if problem is not None else self.problem
+        if self._bc_prefetcher is not None:
+            self._bc_prefetcher.join()  # no user callback runs beside another
         if self.formulation is StageFormulation.DIRK:
             return _step_dirk_dev(self, problem)
         if problem.is_linear:
@@ -485,11 +502,22 @@ def _solve_constrained_dev(stepper, problem, op, rhs_il, unknown, t):
     bc = problem.dirichlet
     svals = None
     if bc is not None and len(bc.dofs):
-        svals = stage_values_dev(stage_bc_values(stepper.bc_method, stepper.tableau, bc,
-                                                 stepper._u_dev, t, stepper.dt, unknown)
-                                 ).reshape(op.s, -1)
+        tab, dt = stepper.tableau, stepper.dt
+        pf = stepper._boundary_prefetch(problem)
+        fn_values = None
+        if pf is not None:
+            fn = bc.g if stepper.bc_method is BcMethod.DAE else bc.g_dot
+            if fn is not None:
+                shape = (len(bc.dofs),)
+                fn_values = pf.take(fn, [t + ci * dt for ci in tab.c], shape)
+        svals = stage_values_dev(stage_bc_values(stepper.bc_method, tab, bc, stepper._u_dev, t,
+                                                 dt, unknown, fn_values)).reshape(op.s, -1)
         sop, srhs = constrain_stage_system_dev(op, rhs_il, bc, svals)
         A = sop._dev_op()
+        if fn_values is not None and t == stepper.t:
+            # the next step's boundary data, evaluated while the GPU solves
+            t1 = stepper._t_base + (stepper.step_index + 1) * dt
+            pf.schedule(fn, [t1 + ci * dt for ci in tab.c], shape)
     else:
         A, srhs = op._dev_op(), rhs_il
     pc = stepper._preconditioner(_SPLIT[stepper.formulation], problem)
