@@ -1063,7 +1063,32 @@ struct irk_mg : public irk::CgPrec {
                                   2 * irk::fpad_len(L) * 16));
     return IRK_OK;
   }
+  // half-length transforms (irk_dst.cuh dsth_transform): N >= 256;
+  // env IRK_DST_FULL keeps the length-2N odd-extension kernels (A/B)
+  static bool dst_half(int N) {
+    static const bool full = getenv("IRK_DST_FULL") != nullptr;
+    return !full && N >= 256;
+  }
+  template <int N>
+  static int dsth_attrs_n() {
+    const int one = irk::fpad_len(N) * 16;
+    IRK_CUDA(cudaFuncSetAttribute(irk::k_dsth_rows<N, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, one));
+    IRK_CUDA(cudaFuncSetAttribute(irk::k_dsth_rows<N, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, one));
+    IRK_CUDA(cudaFuncSetAttribute(irk::k_dsth_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  2 * one));
+    return IRK_OK;
+  }
   static int dst_attrs(int L) {
+    if (dst_half(L / 2)) {
+      switch (L / 2) {
+        case 256: return dsth_attrs_n<256>();
+        case 512: return dsth_attrs_n<512>();
+        case 1024: return dsth_attrs_n<1024>();
+        case 2048: return dsth_attrs_n<2048>();
+      }
+    }
     switch (L) {
       case 64: return dst_attrs_l<64>();
       case 128: return dst_attrs_l<128>();
@@ -1092,9 +1117,30 @@ struct irk_mg : public irk::CgPrec {
     ctx->launches += 3;
     return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
   }
+  template <int N>
+  int apply_dsth_n(irk_ctx* ctx, cudaStream_t s, const double* r, double* z, const int* stop,
+                   const irk::SkipCtl& sk, double* rz_part) {
+    using namespace irk;
+    constexpr size_t kBuf = (size_t)fpad_len(N) * 16;
+    launch(k_dsth_rows<N, false>, N / 2, N / 8, kBuf, s, r, dst_T, r, dst_cos, dst_tw, stop, sk,
+           (double*)nullptr);
+    launch(k_dsth_cols<N>, N / 4, N / 4, 2 * kBuf, s, dst_T, dstS, dst_cos, dst_tw, stop);
+    launch(k_dsth_rows<N, true>, N / 2, N / 8, kBuf, s, (const double*)dst_T, z, r, dst_cos,
+           dst_tw, stop, SkipCtl{}, rz_part);
+    ctx->launches += 3;
+    return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
+  }
   // z = B_s^-1 r (r != z)
   int apply_dst(irk_ctx* ctx, cudaStream_t s, const double* r, double* z, const int* stop,
                 const irk::SkipCtl& sk = irk::SkipCtl{}, double* rz_part = nullptr) {
+    if (dst_half(dst_N)) {
+      switch (dst_N) {
+        case 256: return apply_dsth_n<256>(ctx, s, r, z, stop, sk, rz_part);
+        case 512: return apply_dsth_n<512>(ctx, s, r, z, stop, sk, rz_part);
+        case 1024: return apply_dsth_n<1024>(ctx, s, r, z, stop, sk, rz_part);
+        case 2048: return apply_dsth_n<2048>(ctx, s, r, z, stop, sk, rz_part);
+      }
+    }
     switch (2 * dst_N) {
       case 64: return apply_dst_l<64>(ctx, s, r, z, stop, sk, rz_part);
       case 128: return apply_dst_l<128>(ctx, s, r, z, stop, sk, rz_part);
@@ -1384,7 +1430,13 @@ struct irk_mg : public irk::CgPrec {
     static const bool off = getenv("IRK_MG_NOFUSE") || getenv("IRK_CG_NOFUSE");
     // sine-transform preconditioner: one partial per CTA of the inverse row
     // kernel (row-kernel blocks of at least kBlock threads: N >= 1024)
-    if (dst_on) return (!off && 2 * dst_N / 8 >= irk::kBlock) ? dst_N / 2 : 0;
+    if (dst_on) {
+      // the row kernels' block: N / 8 threads (half-length) or N / 4
+      const int nt = dst_half(dst_N) ? dst_N / 8 : dst_N / 4;
+      const bool ok = dst_half(dst_N) ? (nt >= irk::kBlock || 2 * nt == irk::kBlock)
+                                      : nt >= irk::kBlock;
+      return (!off && ok) ? dst_N / 2 : 0;
+    }
     if (off || !s2_on || lev.size() < 2) return 0;
     const int N = (int)lev[0].g.n1 - 1;
     return N >= 512 ? ((N + irk::kBTX - 1) / irk::kBTX) * ((N + irk::kBTY - 1) / irk::kBTY)
