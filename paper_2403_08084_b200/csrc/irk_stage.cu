@@ -911,9 +911,14 @@ int irk_stage_apply(irk_ctx* ctx, int s, const double* C1_host, const double* C2
         // bulk-asynchronous tiles (k_stage_apply_bulk); env IRK_NO_BULK: the
         // per-warp window copies of k_stage_apply_std
         static const bool bulk_off = getenv("IRK_NO_BULK") != nullptr;
-        // (the 15-point 3D stencil: tiles of IRK_BULK3_KT slices, 4 or 6;
-        // IRK_NO_BULK3 keeps the per-warp copies there)
-        static const bool bulk3_off = getenv("IRK_NO_BULK3") != nullptr;
+        // The 15-point 3D stencil stays on the per-warp copies by default:
+        // a tile's value slabs and 7 windows take 60 KB per ring stage, so
+        // one 4-warp CTA per SM is resident and its compute phase, not the
+        // bytes in flight, bounds the kernel (measured at config 3, s = 4:
+        // 99 us with a 2- or 3-stage ring of 4-slice tiles, 88 us with 6-slice
+        // tiles, 77 us for k_stage_apply_std; profiles/r02/s5_ncu_full.log).
+        // IRK_BULK3=1 selects the bulk tiles there (IRK_BULK3_KT = 4 or 6).
+        static const bool bulk3_off = getenv("IRK_BULK3") == nullptr;
         static const int bulk3_kt = getenv("IRK_BULK3_KT") ? atoi(getenv("IRK_BULK3_KT")) : 4;
         if (!bulk_off && (P->ellw == 7 || (P->ellw == 15 && !bulk3_off))) {
           const bool d3 = P->ellw == 15;
