@@ -456,8 +456,9 @@ __device__ __forceinline__ void dsth_transform(double2* buf, const double2* __re
 
 // Row DSTs by the half-length transform: CTA b takes rows 1 + 2b and 2 + 2b
 // (N / 8 threads).  Arguments and fused-CG behaviour as k_dst_rows.
+// (register caps: 768 resident threads per SM, <= 85 registers)
 template <int N, bool INV>
-__global__ void __launch_bounds__(N / 8)
+__global__ void __launch_bounds__(N / 8, 768 / (N / 8))
     k_dsth_rows(const double* __restrict__ src, double* __restrict__ dst,
                 const double* __restrict__ r, const double* __restrict__ coskn,
                 const double2* __restrict__ tw, const int* stop, SkipCtl sk,
@@ -553,7 +554,7 @@ __global__ void __launch_bounds__(N / 8)
 // half-length transform: CTA b owns columns 4b .. 4b+3 (two transforms, N / 4
 // threads in two groups).
 template <int N>
-__global__ void __launch_bounds__(N / 4)
+__global__ void __launch_bounds__(N / 4, (N >= 2048 ? 1024 : 768) / (N / 4))
     k_dsth_cols(double* __restrict__ T, DstStencil S, const double* __restrict__ coskn,
                 const double2* __restrict__ tw, const int* stop) {
   IRK_PDL_ENTER();
