@@ -759,9 +759,12 @@ def _dst_prec_host(B, N, r):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,beta", [(32, 2e-2), (64, 5e-3), (256, 3e-4), (2048, 4.4e-4)])
+@pytest.mark.parametrize("n,beta", [(32, 2e-2), (64, 5e-3), (256, 3e-4), (512, 1e-3),
+                                    (1024, 2e-4), (2048, 4.4e-4)])
 def test_dst_preconditioner(cuda, irk, oracle, n, beta):
-    """Fast sine-transform preconditioner (k_dst_rows / k_dst_cols) against
+    """Fast sine-transform preconditioner (k_dst_rows / k_dst_cols below N = 256,
+    the half-length k_dsth_rows / k_dsth_cols from there: N / 8 = 32 .. 256
+    threads per transform, the fused-CG block sizes 128 and 256 included) against
     its scipy DST-I restatement, and the sine-transform-preconditioned CG
     block solve against a sparse direct solve, in a handful of iterations."""
     import scipy.sparse as sp
