@@ -181,11 +181,10 @@ template <int NT>
 __device__ __forceinline__ double dst_reduce_rr(const double* part, int G) {
   // reduce_partials' order (kBlock threads, 4 strided partials each, warp
   // trees, warps in order) on a block of NT threads: NT >= kBlock uses its
-  // first kBlock threads, a smaller NT (dividing kBlock) gives every thread
-  // kBlock / NT of the kBlock virtual threads (t + q NT: virtual warp
-  // w + q NT / 32)
-  static_assert(NT >= kBlock || (kBlock % NT == 0 && NT % 32 == 0), "dst_reduce_rr: block size");
-  constexpr int VT = NT >= kBlock ? 1 : kBlock / NT;
+  // first kBlock threads, NT = kBlock / 2 gives every thread two of the
+  // kBlock virtual threads (t and t + NT: virtual warps w and w + NT / 32)
+  static_assert(NT >= kBlock || 2 * NT == kBlock, "dst_reduce_rr: block size");
+  constexpr int VT = NT >= kBlock ? 1 : 2;
   __shared__ double pred[kBlock / 32];
   __shared__ double tot;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -462,7 +461,7 @@ __device__ __forceinline__ void dsth_transform(double2* buf, const double2* __re
 // bound, application 143 -> 124 us; at 1024^2 the latency-bound kernels lose
 // with the few spills the cap costs, 42 -> 48 us; profiles/r02/s5_regs.log).
 template <int N, bool INV>
-__global__ void __launch_bounds__(N / 8, N >= 2048 ? 768 / (N / 8) : 0)
+__global__ void __launch_bounds__(N / 8, N >= 2048 ? 768 / (N / 8) : 1)
     k_dsth_rows(const double* __restrict__ src, double* __restrict__ dst,
                 const double* __restrict__ r, const double* __restrict__ coskn,
                 const double2* __restrict__ tw, const int* stop, SkipCtl sk,
@@ -558,7 +557,7 @@ __global__ void __launch_bounds__(N / 8, N >= 2048 ? 768 / (N / 8) : 0)
 // half-length transform: CTA b owns columns 4b .. 4b+3 (two transforms, N / 4
 // threads in two groups).
 template <int N>
-__global__ void __launch_bounds__(N / 4, N >= 2048 ? 1024 / (N / 4) : 0)
+__global__ void __launch_bounds__(N / 4, N >= 2048 ? 1024 / (N / 4) : 1)
     k_dsth_cols(double* __restrict__ T, DstStencil S, const double* __restrict__ coskn,
                 const double2* __restrict__ tw, const int* stop) {
   IRK_PDL_ENTER();
@@ -595,293 +594,6 @@ __global__ void __launch_bounds__(N / 4, N >= 2048 ? 1024 / (N / 4) : 0)
   for (int t = threadIdx.x; t < 4 * (N - 1); t += 2 * NT) {
     const int l = 1 + (t >> 2), c = t & 3;
     const double2 Y = dst_buf[(c >> 1) * LP + fpad(l)];
-    T[(size_t)l * N + k0 + c] = (c & 1) ? Y.y : Y.x;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Warp-per-transform kernels (N = 1024).  At 1024^2 the kernels above are one
-// wave of CTAs whose lifetime is ~14 block-wide barriers and four shared-
-// memory passes of one butterfly per thread: latency, not throughput.  Here
-// ONE WARP owns the half-length transform of a row pair: 1024 = 32 x 32, two
-// radix-32 passes with 32 points per lane in registers (DFT-32 = 8 x 4
-// Cooley-Tukey, constant twiddles), one shared-memory transpose between them,
-// __syncwarp only.  The 1024-point buffer of a warp is padded by one element
-// per 32 (wpad): lane-strided and unit-strided accesses of both passes are
-// conflict-free.
-
-// e^{-2 pi i p / 32}
-__host__ __device__ constexpr double w32_cos(int p) {
-  constexpr double c[9] = {1.0,
-                           0.98078528040323044913,
-                           0.92387953251128675613,
-                           0.83146961230254523708,
-                           0.70710678118654752440,
-                           0.55557023301960222474,
-                           0.38268343236508977173,
-                           0.19509032201612826785,
-                           0.0};
-  p &= 31;
-  if (p > 16) p = 32 - p;
-  return p <= 8 ? c[p] : -c[16 - p];
-}
-__host__ __device__ constexpr double w32_sin(int p) { return w32_cos(p - 8); }
-
-// forward DFT of 32 points in registers: in natural order, out X[k1 + 8 k2]
-// in x[4 k1 + k2]
-__device__ __forceinline__ void dft32(double2 (&x)[32]) {
-#pragma unroll
-  for (int n2 = 0; n2 < 4; ++n2) {
-    double2 t[8];
-#pragma unroll
-    for (int n1 = 0; n1 < 8; ++n1) t[n1] = x[4 * n1 + n2];
-    dft8(t);
-#pragma unroll
-    for (int k1 = 0; k1 < 8; ++k1) {
-      const int e = n2 * k1;
-      x[4 * k1 + n2] = e == 0 ? t[k1] : c_mul(t[k1], make_double2(w32_cos(e), -w32_sin(e)));
-    }
-  }
-#pragma unroll
-  for (int k1 = 0; k1 < 8; ++k1) dft4(x[4 * k1], x[4 * k1 + 1], x[4 * k1 + 2], x[4 * k1 + 3]);
-}
-
-constexpr int kWN = 1024;                 // transform length of the warp kernels
-constexpr int kWLen = kWN + kWN / 32;     // padded buffer of one warp
-__host__ __device__ constexpr int wpad(int i) { return i + (i >> 5); }
-
-// In: buf[wpad(j)] = v_j (the pre-processed sequence of dsth_transform).
-// Out: buf[wpad(k)] = S_k, k = 1..N-1, buf[wpad(0)] = 0.  One warp.
-__device__ __forceinline__ void dstw_core(double2* buf, const double2* __restrict__ tw, int lane) {
-  constexpr int N = kWN;
-  double2 x[32];
-  // pass 1 (Ns = 1): points lane + 32 r
-#pragma unroll
-  for (int r = 0; r < 32; ++r) x[r] = buf[wpad(lane + 32 * r)];
-  dft32(x);
-  __syncwarp();
-#pragma unroll
-  for (int k1 = 0; k1 < 8; ++k1)
-#pragma unroll
-    for (int k2 = 0; k2 < 4; ++k2) buf[wpad(lane * 32 + k1 + 8 * k2)] = x[4 * k1 + k2];
-  __syncwarp();
-  // pass 2 (Ns = 32): twiddles w^r, w = e^{-2 pi i lane / 1024}, by powers
-  {
-    const double2 w1 = __ldg(tw + 2 * lane);  // table of length 2N
-    const double2 w2 = c_mul(w1, w1), w3 = c_mul(w2, w1), w4 = c_mul(w2, w2);
-    double2 b = make_double2(1.0, 0.0);       // w^{4 g}
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      double2 v0 = buf[wpad(lane + 32 * (4 * g))];
-      double2 v1 = buf[wpad(lane + 32 * (4 * g + 1))];
-      double2 v2 = buf[wpad(lane + 32 * (4 * g + 2))];
-      double2 v3 = buf[wpad(lane + 32 * (4 * g + 3))];
-      x[4 * g] = g == 0 ? v0 : c_mul(v0, b);
-      x[4 * g + 1] = c_mul(v1, g == 0 ? w1 : c_mul(b, w1));
-      x[4 * g + 2] = c_mul(v2, g == 0 ? w2 : c_mul(b, w2));
-      x[4 * g + 3] = c_mul(v3, g == 0 ? w3 : c_mul(b, w3));
-      b = g == 0 ? w4 : c_mul(b, w4);
-    }
-  }
-  dft32(x);
-  __syncwarp();
-#pragma unroll
-  for (int k1 = 0; k1 < 8; ++k1)
-#pragma unroll
-    for (int k2 = 0; k2 < 4; ++k2) buf[wpad(lane + 32 * (k1 + 8 * k2))] = x[4 * k1 + k2];
-  __syncwarp();
-  // post-processing (see dsth_transform): lane owns k = 16 lane .. 16 lane + 15
-  double2 R[16], I[16];
-#pragma unroll
-  for (int e = 0; e < 16; ++e) {
-    const int k = 16 * lane + e;
-    const double2 Vk = buf[wpad(k)], Vn = buf[wpad((N - k) & (N - 1))];
-    R[e] = make_double2(0.5 * (Vk.x + Vn.x), 0.5 * (Vk.y + Vn.y));
-    I[e] = make_double2(0.5 * (Vn.y - Vk.y), 0.5 * (Vk.x - Vn.x));
-  }
-  if (lane == 0) R[0] = make_double2(0.5 * R[0].x, 0.5 * R[0].y);
-#pragma unroll
-  for (int e = 1; e < 16; ++e) R[e] = c_add(R[e], R[e - 1]);
-  double2 inc = R[15];
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double a = __shfl_up_sync(0xffffffffu, inc.x, o);
-    const double c = __shfl_up_sync(0xffffffffu, inc.y, o);
-    if (lane >= o) inc = make_double2(inc.x + a, inc.y + c);
-  }
-  double2 off;
-  off.x = __shfl_up_sync(0xffffffffu, inc.x, 1);
-  off.y = __shfl_up_sync(0xffffffffu, inc.y, 1);
-  if (lane == 0) off = make_double2(0.0, 0.0);
-  __syncwarp();  // every V read is done
-#pragma unroll
-  for (int e = 0; e < 16; ++e) {
-    const int k = 16 * lane + e;
-    buf[wpad(2 * k)] = k == 0 ? make_double2(0.0, 0.0) : I[e];
-    buf[wpad(2 * k + 1)] = c_add(off, R[e]);
-  }
-  __syncwarp();
-}
-
-// Row DSTs, one warp per row pair, WPC warps per CTA (grid N / 2 / WPC).
-// Arguments and fused-CG behaviour as k_dst_rows.
-template <bool INV, int WPC>
-__global__ void __launch_bounds__(32 * WPC)
-    k_dstw_rows(const double* __restrict__ src, double* __restrict__ dst,
-                const double* __restrict__ r, const double* __restrict__ coskn,
-                const double2* __restrict__ tw, const int* stop, SkipCtl sk,
-                double* __restrict__ rz_part) {
-  IRK_PDL_ENTER();
-  constexpr int N = kWN, n1 = N + 1, NTH = 32 * WPC;
-  if constexpr (!INV) {
-    if (sk.st) {
-      const double rr = dst_reduce_rr<NTH>(sk.rr, sk.G);
-      const bool skip = cg_skip_pred<double>(sk.st, rr, sk.maxit);
-      if (blockIdx.x == 0 && threadIdx.x == 0) sk.st->skip = skip ? 1 : 0;
-      if (skip) return;
-      stop = nullptr;
-    }
-  }
-  if (stop && *stop) return;
-  extern __shared__ double2 dst_buf[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double2* buf = dst_buf + warp * kWLen;
-  const int pair = blockIdx.x * WPC + warp;  // < N / 2
-  const int ra = 1 + 2 * pair, rb = ra + 1;
-  const bool hb = rb <= N - 1;
-  constexpr int sstride = INV ? N : n1;
-  const double* sa = src + (size_t)ra * sstride;
-  const double* sb = src + (size_t)(hb ? rb : ra) * sstride;
-  // load and pre-process: pairs (j, N - j), j = 1 + lane + 32 i <= N / 2
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int j = 1 + lane + 32 * i;
-    const double aj = sa[j], an = sa[N - j];
-    const double bj = hb ? sb[j] : 0.0, bn = hb ? sb[N - j] : 0.0;
-    const double sj = __ldg(coskn + (N / 2 - j));  // sin(pi j / N)
-    const double sma = aj + an, dfa = aj - an, smb = bj + bn, dfb = bj - bn;
-    buf[wpad(j)] = make_double2(fma(sj, sma, 0.5 * dfa), fma(sj, smb, 0.5 * dfb));
-    if (j != N / 2)
-      buf[wpad(N - j)] = make_double2(fma(sj, sma, -0.5 * dfa), fma(sj, smb, -0.5 * dfb));
-  }
-  if (lane == 0) buf[wpad(0)] = make_double2(0.0, 0.0);
-  __syncwarp();
-  dstw_core(buf, tw, lane);
-  constexpr int dstride = INV ? n1 : N;
-  double* da = dst + (size_t)ra * dstride;
-  double* db = dst + (size_t)rb * dstride;
-  double rz = 0.0;
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const int k = lane + 32 * i;
-    if (k >= 1) {
-      const double2 S = buf[wpad(k)];
-      da[k] = S.x;
-      if (hb) db[k] = S.y;
-      if constexpr (INV) {
-        if (rz_part) rz += r[(size_t)ra * n1 + k] * S.x + (hb ? r[(size_t)rb * n1 + k] * S.y : 0.0);
-      }
-    } else if constexpr (INV) {
-      const double va = r[(size_t)ra * n1], vb = hb ? r[(size_t)rb * n1] : 0.0;
-      da[0] = va;  // boundary column x = 0: identity rows
-      if (hb) db[0] = vb;
-      rz += va * va + vb * vb;
-    } else {
-      da[0] = 0.0;
-      if (hb) db[0] = 0.0;
-    }
-  }
-  if constexpr (INV) {
-    if (lane == 0) {  // boundary column x = N
-      const double va = r[(size_t)ra * n1 + N], vb = hb ? r[(size_t)rb * n1 + N] : 0.0;
-      da[N] = va;
-      if (hb) db[N] = vb;
-      rz += va * va + vb * vb;
-    }
-    // boundary rows y = 0 (first CTA) and y = N (last CTA): identity rows
-    if (blockIdx.x == 0)
-      for (int k = threadIdx.x; k <= N; k += NTH) {
-        const double v = r[k];
-        dst[k] = v;
-        rz += v * v;
-      }
-    if (blockIdx.x == gridDim.x - 1)
-      for (int k = threadIdx.x; k <= N; k += NTH) {
-        const double v = r[(size_t)N * n1 + k];
-        dst[(size_t)N * n1 + k] = v;
-        rz += v * v;
-      }
-    if (rz_part) {
-      __shared__ double wred[WPC];
-      rz = warp_sum(rz);
-      if (lane == 0) wred[warp] = rz;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < WPC; ++w) t += wred[w];
-        rz_part[blockIdx.x] = t;
-      }
-    }
-  }
-}
-
-// Column DSTs, spectral scaling and inverse column DSTs on T in place: CTA b
-// owns columns 4b .. 4b+3, two warps (one transform each).
-__global__ void __launch_bounds__(64)
-    k_dstw_cols(double* __restrict__ T, DstStencil S, const double* __restrict__ coskn,
-                const double2* __restrict__ tw, const int* stop) {
-  IRK_PDL_ENTER();
-  if (stop && *stop) return;
-  constexpr int N = kWN;
-  extern __shared__ double2 dst_buf[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double2* buf = dst_buf + warp * kWLen;
-  const int k0 = 4 * blockIdx.x;
-#pragma unroll 8
-  for (int t = threadIdx.x; t < 4 * (N - 1); t += 64) {
-    const int l = 1 + (t >> 2), c = t & 3;
-    const double v = T[(size_t)l * N + k0 + c];
-    double2* b = dst_buf + (c >> 1) * kWLen;
-    if (c & 1) b[wpad(l)].y = v;
-    else b[wpad(l)].x = v;
-  }
-  __syncthreads();
-  const int ka = k0 + 2 * warp, kb = ka + 1;
-  const double cka = coskn[ka], ckb = coskn[kb];
-  const double sc = 4.0 / ((double)N * (double)N);
-#pragma unroll 1
-  for (int pass = 0; pass < 2; ++pass) {
-    // pre-processing in place: pairs (j, N - j)
-#pragma unroll 4
-    for (int i = 0; i < 16; ++i) {
-      const int j = 1 + lane + 32 * i;
-      const double sj = __ldg(coskn + (N / 2 - j));
-      double2 zj = buf[wpad(j)], zn = buf[wpad(N - j)];
-      if (pass == 1) {
-        // spectral scaling of the forward transform's output (row
-        // frequencies j and N - j of columns ka, kb); column 0 is the zero
-        // column (any nonzero lambda)
-        const double cj = coskn[j], cn = coskn[N - j];
-        const double pa = S.s00 + 2.0 * S.s10 * cka, qa = 2.0 * S.s01 + 4.0 * S.s11 * cka;
-        const double pb = S.s00 + 2.0 * S.s10 * ckb, qb = 2.0 * S.s01 + 4.0 * S.s11 * ckb;
-        const double laj = ka == 0 ? 1.0 : pa + cj * qa, lan = ka == 0 ? 1.0 : pa + cn * qa;
-        zj = make_double2(zj.x * sc / laj, zj.y * sc / (pb + cj * qb));
-        zn = make_double2(zn.x * sc / lan, zn.y * sc / (pb + cn * qb));
-      }
-      const double2 sm = c_add(zj, zn), df = c_sub(zj, zn);
-      buf[wpad(j)] = make_double2(fma(sj, sm.x, 0.5 * df.x), fma(sj, sm.y, 0.5 * df.y));
-      if (j != N / 2)
-        buf[wpad(N - j)] = make_double2(fma(sj, sm.x, -0.5 * df.x), fma(sj, sm.y, -0.5 * df.y));
-    }
-    if (lane == 0) buf[wpad(0)] = make_double2(0.0, 0.0);
-    __syncwarp();
-    dstw_core(buf, tw, lane);
-  }
-  __syncthreads();
-#pragma unroll 8
-  for (int t = threadIdx.x; t < 4 * (N - 1); t += 64) {
-    const int l = 1 + (t >> 2), c = t & 3;
-    const double2 Y = dst_buf[(c >> 1) * kWLen + wpad(l)];
     T[(size_t)l * N + k0 + c] = (c & 1) ? Y.y : Y.x;
   }
 }

@@ -1130,30 +1130,9 @@ struct irk_mg : public irk::CgPrec {
     ctx->launches += 3;
     return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
   }
-  // warp-per-transform kernels (irk_dst.cuh k_dstw_*): N = 1024 only; env
-  // IRK_DST_NOWARP keeps the block-per-transform half-length kernels (A/B)
-  static constexpr int kDstWpc = 2;  // warps (row pairs) per CTA of the row kernels
-  static bool dst_warp(int N) {
-    static const bool off = getenv("IRK_DST_NOWARP") != nullptr;
-    return !off && N == irk::kWN && dst_half(N);
-  }
-  int apply_dstw(irk_ctx* ctx, cudaStream_t s, const double* r, double* z, const int* stop,
-                 const irk::SkipCtl& sk, double* rz_part) {
-    using namespace irk;
-    constexpr int N = kWN;
-    constexpr size_t kBuf = (size_t)kWLen * 16;  // one warp's padded buffer
-    launch(k_dstw_rows<false, kDstWpc>, N / 2 / kDstWpc, 32 * kDstWpc, kDstWpc * kBuf, s, r, dst_T,
-           r, dst_cos, dst_tw, stop, sk, (double*)nullptr);
-    launch(k_dstw_cols, N / 4, 64, 2 * kBuf, s, dst_T, dstS, dst_cos, dst_tw, stop);
-    launch(k_dstw_rows<true, kDstWpc>, N / 2 / kDstWpc, 32 * kDstWpc, kDstWpc * kBuf, s,
-           (const double*)dst_T, z, r, dst_cos, dst_tw, stop, SkipCtl{}, rz_part);
-    ctx->launches += 3;
-    return cudaPeekAtLastError() == cudaSuccess ? IRK_OK : IRK_ECUDA;
-  }
   // z = B_s^-1 r (r != z)
   int apply_dst(irk_ctx* ctx, cudaStream_t s, const double* r, double* z, const int* stop,
                 const irk::SkipCtl& sk = irk::SkipCtl{}, double* rz_part = nullptr) {
-    if (dst_warp(dst_N)) return apply_dstw(ctx, s, r, z, stop, sk, rz_part);
     if (dst_half(dst_N)) {
       switch (dst_N) {
         case 256: return apply_dsth_n<256>(ctx, s, r, z, stop, sk, rz_part);
@@ -1451,7 +1430,6 @@ struct irk_mg : public irk::CgPrec {
     static const bool off = getenv("IRK_MG_NOFUSE") || getenv("IRK_CG_NOFUSE");
     // sine-transform preconditioner: one partial per CTA of the inverse row
     // kernel (row-kernel blocks of at least kBlock threads: N >= 1024)
-    if (dst_on && dst_warp(dst_N)) return off ? 0 : dst_N / 2 / kDstWpc;
     if (dst_on) {
       // the row kernels' block: N / 8 threads (half-length) or N / 4
       const int nt = dst_half(dst_N) ? dst_N / 8 : dst_N / 4;
