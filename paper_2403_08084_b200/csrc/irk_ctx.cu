@@ -102,7 +102,10 @@ int irk_ctx_destroy(irk_ctx* ctx) {
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
-  for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
+  for (auto& g : ctx->graphs) {
+    cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+  }
   for (irk_ctx* a : ctx->aux) irk_ctx_destroy(a);
   if (ctx->solve_log) cudaFree(ctx->solve_log);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);

@@ -1187,8 +1187,20 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   // arguments and replays as one cached graph.
   double* red = ctx->red;
   static const bool graph_off = getenv("IRK_NO_GRAPH") != nullptr;
+  // One graph per deferred solve (external preconditioner, graph-resident
+  // loop): the init kernel, the solve and the closing log / store kernels are
+  // captured together; the three kernels whose arguments change from solve to
+  // solve (rhs, log slot, output) are updated in the instantiated graph
+  // before every replay, so no eager kernel sits between consecutive solve
+  // graphs (each eager <-> graph boundary costs ~9 us of GPU idle).  Env
+  // IRK_NO_ONEGRAPH: eager init / log / store around the graph.
+  static const bool onegraph_off = getenv("IRK_NO_ONEGRAPH") != nullptr;
+  static const bool while_off_ = getenv("IRK_NO_WHILE") != nullptr;
+  static const bool split_while_ = getenv("IRK_SPLIT_WHILE") != nullptr;
+  const bool onegraph = kExtOk && prec != nullptr && !onegraph_off && !graph_off && !while_off_ &&
+                        !split_while_ && maxit > 0 && !its_host && !relres_host && ctx->log_on;
   if constexpr (kExtOk) {
-    if (prec) {
+    if (prec && !onegraph) {
       // external preconditioner: the eager init reads the strided rhs itself
       launch(k_cg_init_ext<T>, G, kBlock, 0, s, m, rhs, ld_rhs, w.x, w.r, w.p0, rtol * rtol,
              atol * atol, st1, red + 2 * cg_part_doubles<T, NB>(G), cnt);
@@ -1366,7 +1378,52 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
     kc.add(mask).add(w).add(red).add(cnt).add(rtol).add(atol);
     kc.add(prec ? prec->uid : (uint64_t)0).add(prefix).add(stencil).add(maxit).add(n_ext);
     kc.k += key.k;
-    kc.add(2).add(body_its).add(settle);
+    kc.add(2).add(body_its).add(settle).add(onegraph);
+    if constexpr (kExtOk) {
+      if (onegraph) {
+        IRK_TRY(log_reserve(ctx));
+        cudaGraphNode_t un[3] = {nullptr, nullptr, nullptr};
+        const int gs = grid_for(ctx, m);
+        IRK_TRY(graph_launch_prefix_while(
+            ctx, kc.k,
+            [&](cudaStream_t cs, cudaGraphConditionalHandle h) -> int {
+              launch(k_cg_init_ext<T>, G, kBlock, 0, cs, m, rhs, ld_rhs, w.x, w.r, w.p0,
+                     rtol * rtol, atol * atol, st1, red + 2 * cg_part_doubles<T, NB>(G), cnt);
+              IRK_CHECK_LAUNCH(ctx);
+              un[0] = capture_tail(cs);
+              IRK_TRY(init_body(cs));
+              IRK_TRY(chunk_body(cs, 0, prefix));
+              if (settle && prefix > 0) return launch_cond(cs, h);
+              return IRK_OK;
+            },
+            while_body, &body_kernels,
+            [&](cudaStream_t cs) -> int {
+              // after the WHILE node (not a kernel: no programmatic edge)
+              launch_plain(k_cg_log<T>, 1, 32, 0, cs, st0, st1, NB, (int)body_kernels, prefix,
+                           (int)settle, ctx->solve_log + 4 * ctx->log_n);
+              IRK_CHECK_LAUNCH(ctx);
+              un[1] = capture_tail(cs);
+              launch(k_cg_store<T, NB>, gs, kBlock, 0, cs, m, w.x, xout, ld_x);
+              IRK_CHECK_LAUNCH(ctx);
+              un[2] = capture_tail(cs);
+              return IRK_OK;
+            },
+            un, 3,
+            [&](cudaGraphExec_t ex, const cudaGraphNode_t* nd) -> int {
+              IRK_CUDA(exec_set_kernel_args(ex, nd[0], k_cg_init_ext<T>, dim3(G), dim3(kBlock), m,
+                                            rhs, ld_rhs, w.x, w.r, w.p0, rtol * rtol, atol * atol,
+                                            st1, red + 2 * cg_part_doubles<T, NB>(G), cnt));
+              IRK_CUDA(exec_set_kernel_args(ex, nd[1], k_cg_log<T>, dim3(1), dim3(32), st0, st1, NB,
+                                            (int)body_kernels, prefix, (int)settle,
+                                            ctx->solve_log + 4 * ctx->log_n));
+              IRK_CUDA(exec_set_kernel_args(ex, nd[2], k_cg_store<T, NB>, dim3(gs), dim3(kBlock), m,
+                                            w.x, xout, ld_x));
+              return IRK_OK;
+            }));
+        ctx->log_n++;
+        return IRK_OK;
+      }
+    }
     IRK_TRY(graph_launch_prefix_while(
         ctx, kc.k,
         [&](cudaStream_t cs, cudaGraphConditionalHandle h) -> int {

@@ -9,6 +9,8 @@
 #include <cstdlib>
 #include <cstdio>
 #include <string>
+#include <tuple>
+#include <utility>
 #include <utility>
 #include <vector>
 
@@ -88,6 +90,12 @@ struct irk_ctx {
     cudaGraphExec_t exec;
     int64_t kernels;          // per launch (straight-line part)
     int64_t body_kernels = 0;  // per pass of a conditional WHILE body
+    // kernel nodes whose arguments change from launch to launch (updated
+    // with cudaGraphExecKernelNodeSetParams before every replay); their
+    // handles belong to `graph`, which is kept alive for them
+    cudaGraph_t graph = nullptr;
+    cudaGraphNode_t unode[4] = {};
+    int n_unode = 0;
   };
   std::vector<GraphEntry> graphs;
   cudaStream_t cap_stream = nullptr;
@@ -249,6 +257,7 @@ int graph_launch(irk_ctx* ctx, const std::string& key, F&& body) {
   IRK_CUDA(ei);
   if (ctx->graphs.size() >= 64) {
     cudaGraphExecDestroy(ctx->graphs.front().exec);
+    if (ctx->graphs.front().graph) cudaGraphDestroy(ctx->graphs.front().graph);
     ctx->graphs.erase(ctx->graphs.begin());
   }
   ctx->graphs.push_back({key, exec, ctx->launches - l0});
@@ -310,6 +319,7 @@ int graph_launch_while(irk_ctx* ctx, const std::string& key, F&& body,
   IRK_CUDA(e);
   if (ctx->graphs.size() >= 64) {
     cudaGraphExecDestroy(ctx->graphs.front().exec);
+    if (ctx->graphs.front().graph) cudaGraphDestroy(ctx->graphs.front().graph);
     ctx->graphs.erase(ctx->graphs.begin());
   }
   ctx->graphs.push_back({key, exec, ctx->launches - l0});
@@ -327,11 +337,36 @@ int graph_launch_while(irk_ctx* ctx, const std::string& key, F&& body,
 // graph_launch; the prefix kernels are counted per launch, *body_kernels
 // receives the kernel count of one body pass.  `pre(stream, handle)` may
 // launch a kernel that sets the loop condition (default 1 at every launch).
-template <class F, class B>
+// The kernel node a capturing stream ends in (the kernel just captured).
+inline cudaGraphNode_t capture_tail(cudaStream_t s) {
+  cudaStreamCaptureStatus st;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t n = 0;
+  if (cudaStreamGetCaptureInfo(s, &st, nullptr, nullptr, &deps, &n) != cudaSuccess || n != 1)
+    return nullptr;
+  return deps[0];
+}
+
+struct NoPost {
+  int operator()(cudaStream_t) const { return IRK_OK; }
+};
+struct NoUpdate {
+  int operator()(cudaGraphExec_t, const cudaGraphNode_t*) const { return IRK_OK; }
+};
+
+// `post(stream)` (optional) is captured after the WHILE node.  `unodes`
+// (optional, n_unodes <= 4 handles recorded by pre / post with
+// capture_tail) are kernel nodes whose arguments differ between launches:
+// `update(exec, nodes)` sets them before every replay of the cached graph
+// (the first launch runs with the captured arguments).
+template <class F, class B, class Pst = NoPost, class U = NoUpdate>
 int graph_launch_prefix_while(irk_ctx* ctx, const std::string& key, F&& pre, B&& body,
-                              int64_t* body_kernels) {
+                              int64_t* body_kernels, Pst&& post = NoPost{},
+                              const cudaGraphNode_t* unodes = nullptr, int n_unodes = 0,
+                              U&& update = NoUpdate{}) {
   for (auto& g : ctx->graphs) {
     if (g.key == key) {
+      if (g.n_unode) IRK_TRY(update(g.exec, g.unode));
       IRK_CUDA(cudaGraphLaunch(g.exec, ctx->stream));
       ctx->launches += g.kernels;
       *body_kernels = g.body_kernels;
@@ -373,6 +408,7 @@ int graph_launch_prefix_while(irk_ctx* ctx, const std::string& key, F&& pre, B&&
       e = cudaStreamUpdateCaptureDependencies(ctx->cap_stream, &node, 1,
                                               cudaStreamSetCaptureDependencies);
     }
+    if (e == cudaSuccess) rc = post(ctx->cap_stream);
   }
   cudaGraph_t got = nullptr;
   const cudaError_t ee = cudaStreamEndCapture(ctx->cap_stream, &got);
@@ -398,13 +434,33 @@ int graph_launch_prefix_while(irk_ctx* ctx, const std::string& key, F&& pre, B&&
   const int64_t bk = ctx->launches - l0 - pre_kernels;
   cudaGraphExec_t exec = nullptr;
   e = cudaGraphInstantiate(&exec, graph, 0);
-  cudaGraphDestroy(graph);
+  bool keep = n_unodes > 0 && n_unodes <= 4 && e == cudaSuccess;
+  for (int i = 0; keep && i < n_unodes; ++i) keep = unodes[i] != nullptr;
+  if (n_unodes > 0 && !keep && e == cudaSuccess) {
+    // the caller's arguments cannot be updated in this graph: not cacheable
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    set_error("graph_launch_prefix_while: updatable kernel nodes not recorded");
+    return IRK_ECUDA;
+  }
+  if (!keep) cudaGraphDestroy(graph);
   IRK_CUDA(e);
   if (ctx->graphs.size() >= 64) {
     cudaGraphExecDestroy(ctx->graphs.front().exec);
+    if (ctx->graphs.front().graph) cudaGraphDestroy(ctx->graphs.front().graph);
     ctx->graphs.erase(ctx->graphs.begin());
   }
   ctx->graphs.push_back({key, exec, pre_kernels, bk});
+  ctx->launches = l0 + pre_kernels;  // body passes are counted by the caller
+  *body_kernels = bk;
+  if (keep) {
+    auto& ge = ctx->graphs.back();
+    ge.graph = graph;
+    ge.n_unode = n_unodes;
+    for (int i = 0; i < n_unodes; ++i) ge.unode[i] = unodes[i];
+    // arguments that were not known at capture time (the body's kernel count)
+    IRK_TRY(update(ge.exec, ge.unode));
+  }
   ctx->launches = l0 + pre_kernels;  // body passes are counted by the caller
   *body_kernels = bk;
   IRK_CUDA(cudaGraphLaunch(exec, ctx->stream));
@@ -443,6 +499,42 @@ inline cudaError_t launch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cuda
   cfg.attrs = at;
   cfg.numAttrs = pdl_on() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
+// Launch without the programmatic-serialisation attribute (a kernel whose
+// predecessor in a captured graph is not a kernel node).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_plain(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s,
+                                Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
+// New arguments for a kernel node of an instantiated graph (same kernel,
+// grid and block as captured; arguments converted to the kernel's types).
+template <typename Tup, size_t... I>
+inline void tuple_ptrs(Tup& t, void** out, std::index_sequence<I...>) {
+  ((out[I] = (void*)&std::get<I>(t)), ...);
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t exec_set_kernel_args(cudaGraphExec_t exec, cudaGraphNode_t node,
+                                        void (*k)(KArgs...), dim3 g, dim3 b, Args&&... args) {
+  static_assert(sizeof...(KArgs) == sizeof...(Args), "exec_set_kernel_args: argument count");
+  std::tuple<std::remove_cv_t<KArgs>...> vals(std::forward<Args>(args)...);
+  void* ptrs[sizeof...(KArgs)];
+  tuple_ptrs(vals, ptrs, std::index_sequence_for<KArgs...>{});
+  cudaKernelNodeParams kp = {};
+  kp.func = (void*)k;
+  kp.gridDim = g;
+  kp.blockDim = b;
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = ptrs;
+  kp.extra = nullptr;
+  return cudaGraphExecKernelNodeSetParams(exec, node, &kp);
 }
 
 inline int grid_for(const irk_ctx* ctx, int64_t work_items, int per_block = kBlock,
