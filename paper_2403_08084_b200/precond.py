@@ -261,12 +261,13 @@ class StagePreconditioner:
                 C_ = Md if self.form is Splitting.IA else (Ks[0] if len(Ks) == 1 else Ks[i])
                 call("irk_stage_couple", ctx(), s, i, hptr(coef), C_.handle,
                      ptr(self.mask()), ptr(R), ptr(X), ptr(tmp), 1)
-            else:
-                call("irk_stage_get", ctx(), m, s, i, ptr(R), ptr(tmp))
             fac = self.block_factors[i]
             xi = X[i:]
+            # a block without coupling terms reads its stage column of R in
+            # place (stride s): no staging copy
+            rhs_i, ld_i = (tmp, 1) if coef is not None else (R[i:], s)
             # deferred (no host round trip) when the caller collects the log
-            st = fac.dev_solve(tmp, xi, ld_rhs=1, ld_x=s, settings=self.settings,
+            st = fac.dev_solve(rhs_i, xi, ld_rhs=ld_i, ld_x=s, settings=self.settings,
                                defer=self.defer_solves)
             self.inner_iterations.append([st])
         self._last_apply = self.inner_iterations[n0:]
