@@ -461,7 +461,7 @@ __device__ __forceinline__ void dsth_transform(double2* buf, const double2* __re
 // bound, application 143 -> 124 us; at 1024^2 the latency-bound kernels lose
 // with the few spills the cap costs, 42 -> 48 us; profiles/r02/s5_regs.log).
 template <int N, bool INV>
-__global__ void __launch_bounds__(N / 8, N >= 2048 ? 768 / (N / 8) : 1)
+__global__ void __launch_bounds__(N / 8, N >= 2048 ? 768 / (N / 8) : 0)
     k_dsth_rows(const double* __restrict__ src, double* __restrict__ dst,
                 const double* __restrict__ r, const double* __restrict__ coskn,
                 const double2* __restrict__ tw, const int* stop, SkipCtl sk,
@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(N / 8, N >= 2048 ? 768 / (N / 8) : 1)
 // half-length transform: CTA b owns columns 4b .. 4b+3 (two transforms, N / 4
 // threads in two groups).
 template <int N>
-__global__ void __launch_bounds__(N / 4, N >= 2048 ? 1024 / (N / 4) : 1)
+__global__ void __launch_bounds__(N / 4, N >= 2048 ? 1024 / (N / 4) : 0)
     k_dsth_cols(double* __restrict__ T, DstStencil S, const double* __restrict__ coskn,
                 const double2* __restrict__ tw, const int* stop) {
   IRK_PDL_ENTER();
