@@ -401,7 +401,7 @@ static bool stencil_layout(const std::vector<int>& sd, StLayout& L) {
 
 // launch k_stage_apply_bulk<s, W, KT> on a persistent grid (resident CTAs
 // per SM from the occupancy API, queried once per instantiation)
-template <int S, int W, int KT, int NST>
+template <int S, int W, int KT, int NST, bool VD = false>
 static void launch_bulk_s(irk_ctx* ctx, int64_t m, int64_t ns, int64_t ntiles,
                           const BulkLayout& BL, size_t sm, const Pattern* P, const double* mv,
                           const double* kv, const Coef2& cf, double dt, const uint8_t* mask,
@@ -409,27 +409,27 @@ static void launch_bulk_s(irk_ctx* ctx, int64_t m, int64_t ns, int64_t ntiles,
   static int occ = 0;
   static size_t occ_sm = 0;
   if (!occ || occ_sm != sm) {
-    cudaFuncSetAttribute(k_stage_apply_bulk<S, W, KT, NST>,
+    cudaFuncSetAttribute(k_stage_apply_bulk<S, W, KT, NST, VD>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_apply_bulk<S, W, KT, NST>, KT * 32,
-                                                  sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_apply_bulk<S, W, KT, NST, VD>,
+                                                  KT * 32, sm);
     occ = std::max(occ, 1);
     occ_sm = sm;
   }
   const unsigned gb = (unsigned)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * occ);
-  k_stage_apply_bulk<S, W, KT, NST><<<gb, KT * 32, sm, ctx->stream>>>(
+  k_stage_apply_bulk<S, W, KT, NST, VD><<<gb, KT * 32, sm, ctx->stream>>>(
       m, ns, ntiles, BL, P->sell_col, P->colhdr, mv, kv, cf, dt, mask, Y, Out);
 }
-template <int W, int KT, int NST>
+template <int W, int KT, int NST, bool VD = false>
 static void launch_bulk(irk_ctx* ctx, int s, int64_t m, int64_t ns, int64_t ntiles,
                         const BulkLayout& BL, size_t sm, const Pattern* P, const double* mv,
                         const double* kv, const Coef2& cf, double dt, const uint8_t* mask,
                         const double* Y, double* Out) {
   switch (s) {
-    case 1: launch_bulk_s<1, W, KT, NST>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
-    case 2: launch_bulk_s<2, W, KT, NST>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
-    case 3: launch_bulk_s<3, W, KT, NST>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
-    default: launch_bulk_s<4, W, KT, NST>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
+    case 1: launch_bulk_s<1, W, KT, NST, VD>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
+    case 2: launch_bulk_s<2, W, KT, NST, VD>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
+    case 3: launch_bulk_s<3, W, KT, NST, VD>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
+    default: launch_bulk_s<4, W, KT, NST, VD>(ctx, m, ns, ntiles, BL, sm, P, mv, kv, cf, dt, mask, Y, Out); break;
   }
 }
 
@@ -911,28 +911,47 @@ int irk_stage_apply(irk_ctx* ctx, int s, const double* C1_host, const double* C2
         // bulk-asynchronous tiles (k_stage_apply_bulk); env IRK_NO_BULK: the
         // per-warp window copies of k_stage_apply_std
         static const bool bulk_off = getenv("IRK_NO_BULK") != nullptr;
-        // The 15-point 3D stencil stays on the per-warp copies by default:
-        // a tile's value slabs and 7 windows take 60 KB per ring stage, so
-        // one 4-warp CTA per SM is resident and its compute phase, not the
-        // bytes in flight, bounds the kernel (measured at config 3, s = 4:
-        // 99 us with a 2- or 3-stage ring of 4-slice tiles, 88 us with 6-slice
-        // tiles, 77 us for k_stage_apply_std; profiles/r02/s5_ncu_full.log).
-        // IRK_BULK3=1 selects the bulk tiles there (IRK_BULK3_KT = 4 or 6).
-        static const bool bulk3_off = getenv("IRK_BULK3") == nullptr;
+        // The 15-point 3D stencil: values direct (VD: only the row mask and
+        // the 7 Y windows ride the bulk copies, the value slabs go straight
+        // to registers), 4-slice tiles, 2-stage ring: 29 KB per stage, three
+        // CTAs per SM.  With the value slabs staged too a stage takes 60 KB,
+        // one 4-warp CTA per SM is resident and its compute phase bounds the
+        // kernel.  Measured at config 3, s = 4 (profiles/r02/s5_k2vd.log,
+        // s5_ncu_full.log): VD 52.4 us (0.97 of the copy peak in algorithmic
+        // bytes), VD with 8-slice tiles 66.5, staged values 99 (4-slice, 2- or
+        // 3-stage ring) / 88 (6-slice), per-warp copies (k_stage_apply_std)
+        // 77.4 us.  IRK_BULK3 = std | staged | vd8 selects the others
+        // (IRK_BULK3_KT = 4 or 6 for staged); IRK_BULK2=vd: VD on the 2D
+        // stencil too.
+        static const char* b3 = getenv("IRK_BULK3");
+        static const bool bulk3_off = b3 && !strcmp(b3, "std");
         static const int bulk3_kt = getenv("IRK_BULK3_KT") ? atoi(getenv("IRK_BULK3_KT")) : 4;
+        static const int bulk3_vd = !b3 ? 4 : !strcmp(b3, "vd8") ? 8 : !strcmp(b3, "staged") ? 0 : 4;
+        static const bool bulk2_vd = getenv("IRK_BULK2") && !strcmp(getenv("IRK_BULK2"), "vd");
         if (!bulk_off && (P->ellw == 7 || (P->ellw == 15 && !bulk3_off))) {
           const bool d3 = P->ellw == 15;
-          const int kT = d3 ? (bulk3_kt == 6 ? 6 : 4) : 8;
-          const int nst = d3 && kT == 4 ? 3 : 2;
+          const bool vd = d3 ? bulk3_vd != 0 : bulk2_vd;
+          const int kT = !d3 ? 8 : vd ? bulk3_vd : (bulk3_kt == 6 ? 6 : 4);
+          const int nst = vd ? 2 : (d3 && kT == 4 ? 3 : 2);
           BulkLayout BL;
           const int ymis = (int)(((uintptr_t)Y_dev & 15) / 8);
           if (bulk_layout(SL, P->ellw, s, kT, ymis, BL)) {
             const size_t sm =
-                nst * ((size_t)2 * kT * P->ellw * kSlice + kT * kSlice / 8 + (size_t)BL.rows_total * s) *
+                nst * ((vd ? (size_t)0 : (size_t)2 * kT * P->ellw * kSlice) + kT * kSlice / 8 +
+                       (size_t)BL.rows_total * s) *
                 sizeof(double);
             if (sm <= 200 * 1024) {
               const int64_t ntiles = (ns + kT - 1) / kT;
-              if (!d3)
+              if (!d3 && bulk2_vd)
+                launch_bulk<7, 8, 2, true>(ctx, s, m, ns, ntiles, BL, sm, P, M->val, kp.k[0], cf, dt,
+                                           rowmask_dev, Y_dev, Out_dev);
+              else if (vd && kT == 8)
+                launch_bulk<15, 8, 2, true>(ctx, s, m, ns, ntiles, BL, sm, P, M->val, kp.k[0], cf,
+                                            dt, rowmask_dev, Y_dev, Out_dev);
+              else if (vd)
+                launch_bulk<15, 4, 2, true>(ctx, s, m, ns, ntiles, BL, sm, P, M->val, kp.k[0], cf,
+                                            dt, rowmask_dev, Y_dev, Out_dev);
+              else if (!d3)
                 launch_bulk<7, 8, 2>(ctx, s, m, ns, ntiles, BL, sm, P, M->val, kp.k[0], cf, dt,
                                      rowmask_dev, Y_dev, Out_dev);
               else if (kT == 6)
