@@ -921,13 +921,17 @@ int irk_stage_apply(irk_ctx* ctx, int s, const double* C1_host, const double* C2
         // bytes), VD with 8-slice tiles 66.5, staged values 99 (4-slice, 2- or
         // 3-stage ring) / 88 (6-slice), per-warp copies (k_stage_apply_std)
         // 77.4 us.  IRK_BULK3 = std | staged | vd8 selects the others
-        // (IRK_BULK3_KT = 4 or 6 for staged); IRK_BULK2=vd: VD on the 2D
-        // stencil too.
+        // (IRK_BULK3_KT = 4 or 6 for staged).
         static const char* b3 = getenv("IRK_BULK3");
         static const bool bulk3_off = b3 && !strcmp(b3, "std");
         static const int bulk3_kt = getenv("IRK_BULK3_KT") ? atoi(getenv("IRK_BULK3_KT")) : 4;
         static const int bulk3_vd = !b3 ? 4 : !strcmp(b3, "vd8") ? 8 : !strcmp(b3, "staged") ? 0 : 4;
-        static const bool bulk2_vd = getenv("IRK_BULK2") && !strcmp(getenv("IRK_BULK2"), "vd");
+        // 2D stencil: values direct for s >= 2 (config 2, s = 3: 30.3 -> 28.0 us;
+        // neutral at 2048^2; s = 1 keeps the staged slabs, measured 0.80 of the
+        // peak there; profiles/r02/s5_k2final.log).  IRK_BULK2 = vd | staged
+        // forces one variant.
+        static const char* b2 = getenv("IRK_BULK2");
+        const bool bulk2_vd = b2 ? !strcmp(b2, "vd") : s >= 2;
         if (!bulk_off && (P->ellw == 7 || (P->ellw == 15 && !bulk3_off))) {
           const bool d3 = P->ellw == 15;
           const bool vd = d3 ? bulk3_vd != 0 : bulk2_vd;
