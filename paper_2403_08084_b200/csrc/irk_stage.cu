@@ -1091,45 +1091,6 @@ int irk_stage_couple(irk_ctx* ctx, int s, int i, const double* coef_host, const 
     if (coef_host[j] != 0.0) jm |= 1u << j;
   const Pattern* P = C->pat;
   unsigned g = (unsigned)((m + kBlock - 1) / kBlock);
-  // 7-point 2D stencil patterns, odd s: bulk-asynchronous tiles
-  // (k_stage_couple_bulk); env IRK_NO_CPLBULK keeps the per-row gathers
-  static const bool cplbulk_off = getenv("IRK_NO_CPLBULK") != nullptr;
-  if (!cplbulk_off && P->ellw == 7 && (int)P->stencil.size() == 7 && (s == 1 || s == 3)) {
-    StLayout SL;
-    if (stencil_layout(P->stencil, SL) && SL.nwin <= 3) {
-      constexpr int kT = 8;
-      BulkLayout BL;
-      const int ymis = (int)(((uintptr_t)X_dev & 15) / 8);
-      if (bulk_layout(SL, 7, s, kT, ymis, BL)) {
-        const size_t sm = 2 * ((size_t)kT * kSlice / 8 + (size_t)BL.rows_total * s) * sizeof(double);
-        const int64_t ns = P->nslices, ntiles = (ns + kT - 1) / kT;
-        static int occ1 = 0, occ3 = 0;
-        int& occ = s == 1 ? occ1 : occ3;
-        if (!occ) {
-          if (s == 1)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_couple_bulk<1, 7, kT>,
-                                                          kT * 32, sm);
-          else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_couple_bulk<3, 7, kT>,
-                                                          kT * 32, sm);
-          occ = std::max(occ, 1);
-        }
-        const unsigned gb = (unsigned)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * occ);
-        if (sm <= 48 * 1024) {
-          if (s == 1)
-            k_stage_couple_bulk<1, 7, kT><<<gb, kT * 32, sm, ctx->stream>>>(
-                m, ns, ntiles, BL, P->sell_col, P->colhdr, C->val, cf, jm, rowmask_dev, i, R_dev,
-                X_dev, out_dev, ld_out);
-          else
-            k_stage_couple_bulk<3, 7, kT><<<gb, kT * 32, sm, ctx->stream>>>(
-                m, ns, ntiles, BL, P->sell_col, P->colhdr, C->val, cf, jm, rowmask_dev, i, R_dev,
-                X_dev, out_dev, ld_out);
-          IRK_CHECK_LAUNCH(ctx);
-          return IRK_OK;
-        }
-      }
-    }
-  }
 #define IRK_CPL(WW)                                                                          \
   IRK_STAGE_SWITCH(s, (k_stage_couple<SS, WW><<<g, kBlock, 0, ctx->stream>>>(                   \
                           m, i, P->slice_ptr, P->ellw, P->colhdr, P->sell_col, C->uval, C->val, \

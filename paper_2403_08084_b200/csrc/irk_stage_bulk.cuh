@@ -261,120 +261,6 @@ __global__ void __launch_bounds__(KT * 32)
   }
 }
 
-// Gauss-Seidel coupling (k_stage_couple) on stencil-aligned ELL patterns by
-// the same bulk-asynchronous tiles:
-//   out[r * ld] = R[r*S + i] - sum_k C[r,k] sum_{j in J} coef[j] X[c_k*S + j]
-// (masked rows: out = R).  The X windows of a tile ride the bulk copies into a
-// 2-stage ring, the values of C go straight to registers; odd S only (an
-// even-S row of the window buffer would need the rotated reads above).  The
-// per-row gather kernel it replaces is bound by its 7 dependent gathers:
-// 0.40 of the copy peak in DRAM bytes at config 2.
-template <int S, int W, int KT>
-__global__ void __launch_bounds__(KT * 32)
-    k_stage_couple_bulk(int64_t m, int64_t nslices, int64_t ntiles, const BulkLayout BL,
-                        const int* __restrict__ sell_col, const int* __restrict__ colhdr,
-                        const double* __restrict__ cval, const Mat8 coef, unsigned jmask,
-                        const uint8_t* __restrict__ mask, int i, const double* __restrict__ R,
-                        const double* __restrict__ X, double* __restrict__ out, int64_t ld_out) {
-  static_assert(S % 2 == 1, "k_stage_couple_bulk: odd S");
-  constexpr int NST = 2;
-  extern __shared__ __align__(128) double bsm[];
-  __shared__ __align__(8) uint64_t bar[NST];
-  constexpr int MSK = KT * kSlice / 8;
-  const int stage_doubles = MSK + BL.rows_total * S;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int q = 0; q < NST; ++q) mbar_init(&bar[q], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  auto interior = [&](int64_t t) {
-    const int64_t R0 = t * KT * kSlice;
-    return R0 + BL.lo >= 0 && R0 + BL.hi <= m && (t + 1) * KT <= nslices;
-  };
-  auto issue = [&](int64_t t, int st) {
-    double* base = bsm + (size_t)st * stage_doubles;
-    const int64_t R0 = t * KT * kSlice;
-    unsigned bytes = mask ? MSK * (unsigned)sizeof(double) : 0u;
-    for (int w = 0; w < BL.nwin; ++w) bytes += (unsigned)BL.wrows[w] * S * (unsigned)sizeof(double);
-    mbar_expect_tx(&bar[st], bytes);
-    if (mask) bulk_g2s(base, mask + R0, MSK * sizeof(double), &bar[st]);
-    double* yb = base + MSK;
-    for (int w = 0; w < BL.nwin; ++w)
-      bulk_g2s(yb + (size_t)BL.wbuf[w] * S, X + (R0 + BL.wsrc[w]) * S,
-               (unsigned)BL.wrows[w] * S * sizeof(double), &bar[st]);
-  };
-  int64_t t = blockIdx.x;
-  unsigned pend = 0u, ph = 0u;
-#pragma unroll
-  for (int q = 0; q < NST; ++q) {
-    const int64_t tq = t + (int64_t)q * gridDim.x;
-    if (tq < ntiles && interior(tq)) {
-      pend |= 1u << q;
-      if (threadIdx.x == 0) issue(tq, q);
-    }
-  }
-  for (int st = 0; t < ntiles; t += gridDim.x, st ^= 1) {
-    const int64_t sl = t * KT + warp;
-    const int64_t r = sl * kSlice + lane;
-    const bool live = sl < nslices && r < m;
-    bool flagged = false;
-    double acc = 0.0;
-    // this lane's R entry and values of C: issued before the barrier wait
-    const double rv = live ? R[r * S + i] : 0.0;
-    double cv[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k)
-      cv[k] = live ? __ldg(cval + (size_t)sl * W * kSlice + k * kSlice + lane) : 0.0;
-    bool windowed = false;
-    if ((pend >> st) & 1u) {
-      mbar_wait(&bar[st], (ph >> st) & 1u);
-      ph ^= 1u << st;
-      const double* base = bsm + (size_t)st * stage_doubles;
-      const double* yb = base + MSK + (size_t)(warp * kSlice + lane) * S;
-      if (mask) flagged = reinterpret_cast<const uint8_t*>(base)[warp * kSlice + lane] != 0;
-      const int d = lane < W ? __ldg(colhdr + sl * W + lane) : 0;
-      windowed = __all_sync(0xffffffffu, lane >= W || d == BL.sd[lane < W ? lane : 0]);
-      if (windowed) {
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-          const double* yr = yb + (size_t)BL.krow[k] * S;
-          double w = 0.0;
-#pragma unroll
-          for (int j = 0; j < S; ++j)
-            if (jmask & (1u << j)) w += coef.q[j] * yr[j];
-          acc += cv[k] * w;
-        }
-      }
-    } else if (live) {
-      flagged = mask && mask[r];
-    }
-    if (!windowed && live && !flagged) {
-      // boundary tile or a slice off the stencil: per-entry gathers
-#pragma unroll
-      for (int k = 0; k < W; ++k) {
-        const int c = sell_col_at(colhdr, sell_col, (int)(sl * W + k),
-                                  (int)(sl * kSlice * W + k * kSlice + lane), r);
-        double w = 0.0;
-#pragma unroll
-        for (int j = 0; j < S; ++j)
-          if (jmask & (1u << j)) w += coef.q[j] * __ldg(X + (int64_t)c * S + j);
-        acc += cv[k] * w;
-      }
-    }
-    if (live) out[r * ld_out] = flagged ? rv : rv - acc;
-    __syncthreads();
-    const int64_t tn = t + NST * (int64_t)gridDim.x;
-    const bool more = tn < ntiles && interior(tn);
-    if (threadIdx.x == 0 && more) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      issue(tn, st);
-    }
-    pend = more ? (pend | (1u << st)) : (pend & ~(1u << st));
-  }
-}
-
 // host: bulk layout of a stencil (its StLayout windows) for tiles of kT
 // slices.  ymis = (Y address mod 16) / 8: the global source of every bulk
 // copy must be 16-byte aligned (Krylov basis vectors of odd length start
