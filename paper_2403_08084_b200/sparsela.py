@@ -1332,18 +1332,6 @@ def _fgmres_graph(A, P, n, st, rebuild=False):
     return g
 
 
-_ONE_DEV: dict = {}
-
-
-def _one_dev():
-    """The device scalar 1.0 (numerator of irk_scale_dev), one per device."""
-    dev = str(device())
-    t = _ONE_DEV.get(dev)
-    if t is None:
-        t = _ONE_DEV[dev] = _torch().ones(1, dtype=_torch().float64, device=device())
-    return t
-
-
 def fgmres_device(A: _DevOp, b, P: _DevOp | None = None, settings: KrylovSettings | None = None,
                   x0=None) -> FgmresResult:
     """Restarted flexible GMRES on device vectors (control flow of
@@ -1410,7 +1398,6 @@ def fgmres_device(A: _DevOp, b, P: _DevOp | None = None, settings: KrylovSetting
             r = residual_of(x)
     hbuf = dev_empty(128)
     tmp = dev_empty(n) if left else None
-    one_dev = _one_dev()
     while True:
         cycle = min(st.restart, st.maxit - iterations)
         if cycle <= 0:
@@ -1448,14 +1435,11 @@ def fgmres_device(A: _DevOp, b, P: _DevOp | None = None, settings: KrylovSetting
                  1 if st.reorth else 0)
             if _GAPS is not None:
                 _GAPS.append(_ev_rec())  # GPU work of the iteration ends here
-            # v_{j+1} = w / ||w|| from the device scalar (the same 1.0 / h times
-            # w the host would form), enqueued BEFORE the host reads h: the GPU
-            # normalises while the host does the read-back and the Givens
-            # update.  After a lucky breakdown w is not used again.
-            call("irk_scale_dev", ctx(), n, ptr(one_dev), ptr(hbuf[j + 1:]), ptr(w), ptr(w))
             hcol = hbuf[: j + 2].cpu().numpy()
             H[: j + 2, j] = hcol
             lucky = H[j + 1, j] < breakdown_tol
+            if not lucky:
+                call("irk_axpby", ctx(), n, 1.0 / H[j + 1, j], ptr(w), 0.0, ptr(w))
             for i in range(j):
                 t_ = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
                 H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
