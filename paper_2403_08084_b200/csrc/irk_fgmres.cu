@@ -256,6 +256,7 @@ struct irk_fgraph {
   int* st = nullptr;
   double* red = nullptr;  // the context scratch the graph was built with
   cudaGraphExec_t exec = nullptr;
+  int64_t pass_kernels = 0;  // kernels one pass of the WHILE body launches
 };
 
 extern "C" {
@@ -346,6 +347,22 @@ int irk_fgmres_graph_create(irk_ctx* ctx, void* step_graph, int64_t n, int cycle
     set_error("irk_fgmres_graph_create: instantiate: %s", cudaGetErrorString(e));
     return IRK_ECUDA;
   }
+  // launch accounting of a replay: the kernel nodes of the captured
+  // application plus the Arnoldi kernels above, per pass
+  {
+    size_t nn = 0;
+    if (cudaGraphGetNodes((cudaGraph_t)step_graph, nullptr, &nn) == cudaSuccess && nn > 0) {
+      std::vector<cudaGraphNode_t> nodes(nn);
+      if (cudaGraphGetNodes((cudaGraph_t)step_graph, nodes.data(), &nn) == cudaSuccess) {
+        for (size_t i = 0; i < nn; ++i) {
+          cudaGraphNodeType ty;
+          if (cudaGraphNodeGetType(nodes[i], &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel)
+            fg->pass_kernels++;
+        }
+      }
+    }
+    fg->pass_kernels += reorth ? 7 : 5;
+  }
   *out = fg;
   return IRK_OK;
 }
@@ -381,6 +398,7 @@ int irk_fgmres_graph_run(irk_ctx* ctx, irk_fgraph* fg, int cap, const double* r,
   IRK_CUDA(cudaStreamSynchronize(s));
   *k_host = hs[kFgK];
   *conv_host = hs[kFgConv];
+  ctx->launches += (int64_t)hs[kFgK] * fg->pass_kernels;
   for (int i = 0; i <= hs[kFgK]; ++i) hist_host[i] = hh[i];
   return IRK_OK;
 }

@@ -1197,8 +1197,23 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   static const bool onegraph_off = getenv("IRK_NO_ONEGRAPH") != nullptr;
   static const bool while_off_ = getenv("IRK_NO_WHILE") != nullptr;
   static const bool split_while_ = getenv("IRK_SPLIT_WHILE") != nullptr;
+  // A solve issued while ctx->stream is being captured (the preconditioner
+  // application of a device-resident FGMRES cycle, irk_fgmres.cu) becomes a
+  // straight-line kernel sequence of the caller's graph: init, exactly
+  // `maxit` iterations (kernels of a finished solve do nothing), store.  No
+  // graph launch, no WHILE node (conditional nodes cannot sit in a child
+  // graph), no log entry: the caller passes the fixed iteration count.
+  cudaStreamCaptureStatus capst = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &capst) != cudaSuccess) capst = cudaStreamCaptureStatusNone;
+  const bool captured = capst == cudaStreamCaptureStatusActive;
+  if (captured) {
+    IRK_REQUIRE(kExtOk && prec != nullptr && !its_host && !relres_host && maxit > 0 && maxit <= 8,
+                "run_cg: only a deferred externally preconditioned solve of at most 8 fixed "
+                "iterations can be captured");
+  }
   const bool onegraph = kExtOk && prec != nullptr && !onegraph_off && !graph_off && !while_off_ &&
-                        !split_while_ && maxit > 0 && !its_host && !relres_host && ctx->log_on;
+                        !split_while_ && maxit > 0 && !its_host && !relres_host && ctx->log_on &&
+                        !captured;
   if constexpr (kExtOk) {
     if (prec && !onegraph) {
       // external preconditioner: the eager init reads the strided rhs itself
@@ -1340,6 +1355,13 @@ int run_cg(irk_ctx* ctx, int64_t m, const MatView& A, const SysParams<T>& P, con
   const int prefix = (prec && maxit > 0 && !graph_off && !while_off)
                          ? (prefix_hint >= 0 ? (prefix_hint & ~1) : prefix_env)
                          : 0;
+  if (captured) {
+    IRK_TRY(init_body(s));
+    IRK_TRY(chunk_body(s, 0, maxit));
+    launch(k_cg_store<T, NB>, grid_for(ctx, m), kBlock, 0, s, m, w.x, xout, ld_x);
+    IRK_CHECK_LAUNCH(ctx);
+    return IRK_OK;
+  }
   // The key holds every launch argument of the loop kernels.
   GraphKey key;
   key.add((const void*)&k_cg_spmv<T, NB, HASB, MAXW>).add((const void*)&k_cg_update<T, NB>);

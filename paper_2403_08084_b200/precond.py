@@ -241,7 +241,7 @@ class StagePreconditioner:
         # it, so X needs no zeroing
         order, coefs = self._sweep_plan()
         n0 = len(self.inner_iterations)
-        if self._concurrent_blocks(coefs):
+        if self._concurrent_blocks(coefs) and not la._torch().cuda.is_current_stream_capturing():
             # block Jacobi on multigrid blocks, deferred: the s independent
             # solves read their stage columns of R in place and run
             # concurrently (one auxiliary stream per block after the first)
@@ -276,7 +276,8 @@ class StagePreconditioner:
     def _graph_key(self):
         """Identity of a capturable application (graph-replayed inside the
         device FGMRES cycles): the sequential sweep over blocks solved by a
-        fixed kernel sequence (direct inverses, fixed-sweep Chebyshev)."""
+        fixed kernel sequence (direct inverses, fixed-sweep Chebyshev, a fixed
+        number of sine-transform-preconditioned CG iterations)."""
         if self.kind is PreconditionerKind.SCHUR or self._shift is not None:
             return None
         if not self._mg_blocks():
@@ -411,6 +412,10 @@ class StagePreconditioner:
 
             def account(self, applications):
                 pc.inner_iterations.extend(list(pc._last_apply) * applications)
+
+            def fixed_solves(self):
+                return all(f._fixed_iterations(pc.settings) is not None
+                           for f in pc.block_factors)
 
         return _Op()
 

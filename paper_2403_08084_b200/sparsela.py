@@ -495,6 +495,11 @@ class _DevOp:
         """Book-keeping of ``applications`` replays of a captured
         application (the inner iteration counts a direct call records)."""
 
+    def fixed_solves(self) -> bool:
+        """True when the application is a sweep of fixed-iteration
+        sine-transform block solves (large systems keep device cycles)."""
+        return False
+
 
 class _SpmvOp(_DevOp):
     def __init__(self, A: SparseMatrix):
@@ -618,6 +623,7 @@ class BlockSolveSettings:
 
 
 _DST_OFF = bool(os.environ.get("IRK_NO_DST"))  # A/B: multigrid V-cycle under "auto"
+_DEVFG_DST_OFF = bool(os.environ.get("IRK_NO_DEVFG_DST"))  # A/B: no captured fixed solves
 
 
 class _MgHierarchy:
@@ -859,6 +865,7 @@ class BlockFactorization:
         self._mg = None
         self._inv = None
         self._cheb = None
+        self._fixed = {}  # (rtol, atol, maxit) -> captured iteration count or None
         meth = self.settings.method
         # direct: the inverse is formed on the first solve, so factors that are
         # built but never solved with (regularity checks of per-Newton blocks
@@ -979,6 +986,14 @@ class BlockFactorization:
                  hptr(lo), hptr(hi), ptr(rhs), int(ld_rhs), ptr(x), int(ld_x), int(k))
             self.last_iterations, self.last_relres = k, float("nan")
             return k  # fixed sweep count: nothing to log or check
+        if self._fixed and _torch().cuda.is_current_stream_capturing():
+            k = self._fixed_iterations(st)
+            if k is None:
+                raise RuntimeError("block solve is not capturable with these settings")
+            call("irk_mg_pcg", ctx(), self._mg.handle, ptr(rhs), int(ld_rhs), ptr(x), int(ld_x),
+                 float(st.rtol), float(st.atol), int(k), None, None)
+            self.last_iterations, self.last_relres = k, float("nan")
+            return k  # fixed straight-line iterations: nothing logged
         its = np.zeros(8, dtype=np.int32)
         rel = np.zeros(8, dtype=np.float64)
         one = np.ones(8)
@@ -1030,8 +1045,35 @@ class BlockFactorization:
     def graph_safe(self, settings: BlockSolveSettings | None = None) -> bool:
         """dev_solve is a fixed kernel sequence without host synchronisation
         (direct inverse or fixed-sweep Chebyshev): capturable in a graph."""
-        meth = (settings or self.settings).method
-        return (self.direct and meth in ("auto", "direct")) or meth == "chebyshev"
+        st = settings or self.settings
+        meth = st.method
+        if (self.direct and meth in ("auto", "direct")) or meth == "chebyshev":
+            return True
+        return self._fixed_iterations(st) is not None
+
+    def _fixed_iterations(self, st) -> int | None:
+        """Iteration count of a capturable sine-transform-preconditioned CG
+        solve, or None.  The preconditioner is the exact inverse of the
+        symmetrised stencil, so CG converges in a problem-independent handful
+        of iterations: a probe solve (random right-hand side, once per factor
+        and tolerance) measures the count, and a captured solve issues exactly
+        that many straight-line iterations (run_cg's captured branch).  Only
+        for preconditioner use (raise_on_maxit False: FGMRES is flexible, an
+        iterate short of rtol costs outer iterations, not correctness)."""
+        if _DEVFG_DST_OFF or st.raise_on_maxit or self._mg is None or self.direct:
+            return None
+        if st.method not in ("auto", "mg", "dst") or not self._mg.dst:
+            return None
+        key = (float(st.rtol), float(st.atol), int(st.maxit))
+        if key not in self._fixed:
+            torch = _torch()
+            g = torch.Generator(device="cuda").manual_seed(7)
+            b = torch.rand(self.n, dtype=torch.float64, device="cuda", generator=g)
+            x = dev_empty(self.n)
+            k = self.dev_solve(b, x, settings=st)
+            ok = self.last_relres <= st.rtol or st.atol > 0
+            self._fixed[key] = int(k) if (ok and 1 <= int(k) <= 4) else None
+        return self._fixed[key]
 
     def _dev_op(self):
         fac = self
@@ -1228,6 +1270,13 @@ def _ev_rec():
 # small share of their iteration).  Env IRK_NO_DEVFGMRES: always the host loop.
 DEVFG_MAX_N = 1 << 16
 _DEVFG_OFF = bool(os.environ.get("IRK_NO_DEVFGMRES"))
+# Above DEVFG_MAX_N the cycles still run on the device when the preconditioner
+# is a sweep over sine-transform-preconditioned blocks (fixed straight-line
+# solves, BlockFactorization._fixed_iterations): there the host round trip per
+# Arnoldi step and the eager <-> graph boundaries around every block solve are
+# ~15 % of a step.  The basis (restart + 1 vectors) and Z stay allocated with
+# the cached graph, so the size is bounded.  Env IRK_NO_DEVFG_DST: host loop.
+DEVFG_DST_MAX_N = 1 << 23
 _FG_CACHE: "OrderedDict[tuple, _FgmresGraph]" = OrderedDict()
 _FG_SEEN: dict = {}
 
@@ -1302,7 +1351,9 @@ class _FgmresGraph:
 def _fgmres_graph(A, P, n, st, rebuild=False):
     """The cached cycle graph for (A, P), or None (not capturable, too large,
     or a key seen for the first time: one-off operators are not captured)."""
-    if _DEVFG_OFF or n > DEVFG_MAX_N or st.restart >= 64 or not st.right_pc:
+    if _DEVFG_OFF or st.restart >= 64 or not st.right_pc:
+        return None
+    if n > DEVFG_MAX_N and (P is None or n > DEVFG_DST_MAX_N or not P.fixed_solves()):
         return None
     ka = A.graph_key()
     kp = P.graph_key() if P is not None else ()

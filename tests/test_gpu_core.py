@@ -1042,3 +1042,55 @@ def test_stage_apply_bulk_tiles_vs_oracle(cuda, irk, oracle, s, shift):
 
 def _to_il(v, m, s):
     return np.ascontiguousarray(np.asarray(v).reshape(s, m).T).reshape(-1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,n", [("gs-lower", 256), ("jacobi", 128)])
+def test_fgmres_device_cycle_with_captured_dst_blocks(cuda, irk, kind, n):
+    """Sweeps over sine-transform-preconditioned blocks are capturable: a
+    captured block solve is a straight-line sequence of a fixed number of CG
+    iterations (run_cg's captured branch; the count comes from a probe
+    solve), so the device-resident FGMRES cycle holds the whole
+    preconditioner application.  It reproduces the host loop (whose block
+    solves stop on their tolerance) to the outer tolerance, in the same
+    number of outer iterations (+-1).  dt / h^2 as in config 2 (there the
+    probe finds 2 iterations); n = 256 is above DEVFG_MAX_N unknowns."""
+    from paper_2403_08084_b200 import bcs
+    from paper_2403_08084_b200 import sparsela as la
+
+    M, K, bd = irk.assemble_p1(irk.StructuredGrid(2, n))
+    tab = irk.radau_iia(3)
+    dt = 1000.0 / n ** 2
+    s = tab.s
+    Ainv = np.linalg.inv(tab.A)
+    op = bcs.ConstrainedStageOperator(irk.KroneckerStageOperator(Ainv, np.eye(s), M, [K], dt),
+                                      bd)
+    pc = irk.build_preconditioner(irk.PreconditionerKind(kind), tab, M, K, dt, irk.Splitting.IA, bd,
+                                  la.BlockSolveSettings(rtol=1e-6))
+    fac = pc.block_factors[0]
+    assert fac._mg is not None and fac._mg.dst and not fac.direct
+    ks = [f._fixed_iterations(pc.settings) for f in pc.block_factors]
+    assert all(k is not None and 1 <= k <= 4 for k in ks), ks
+    assert fac.graph_safe(pc.settings) and pc._graph_key() is not None
+    # strict settings are never captured (a capped solve must raise)
+    assert fac._fixed_iterations(la.BlockSolveSettings(rtol=1e-6, raise_on_maxit=True)) is None
+    A, P = op._dev_op(), pc._dev_op()
+    assert P.fixed_solves()
+    b = la.to_dev(np.random.default_rng(n).standard_normal(op.n))
+    st = la.KrylovSettings(rtol=1e-12, maxit=200)
+    la._FG_CACHE.clear()
+    la._FG_SEEN.clear()
+    host = la.fgmres_device(A, b, P, st)
+    assert not la._FG_CACHE
+    n0 = len(pc.inner_iterations)
+    dev = la.fgmres_device(A, b, P, st)
+    assert len(la._FG_CACHE) == 1
+    assert abs(dev.iterations - host.iterations) <= 1
+    assert dev.residuals[-1] <= 1e-12 * dev.residuals[0]
+    x_h, x_d = host.x.cpu().numpy(), dev.x.cpu().numpy()
+    assert np.linalg.norm(x_d - x_h) <= 1e-9 * np.linalg.norm(x_h)
+    # the book-keeping records the fixed count per block solve and application
+    rec = pc.inner_iterations[n0:]
+    assert rec == [[k] for k in ks] * dev.iterations
+    again = la.fgmres_device(A, b, P, st)
+    assert np.array_equal(again.x.cpu().numpy(), x_d)  # deterministic replay
