@@ -413,6 +413,11 @@ class StagePreconditioner:
             def account(self, applications):
                 pc.inner_iterations.extend(list(pc._last_apply) * applications)
 
+            def discard(self, applications):
+                k = len(pc._last_apply) * applications
+                if k:
+                    del pc.inner_iterations[-k:]
+
             def fixed_solves(self):
                 return all(f._fixed_iterations(pc.settings) is not None
                            for f in pc.block_factors)

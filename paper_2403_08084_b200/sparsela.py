@@ -495,6 +495,10 @@ class _DevOp:
         """Book-keeping of ``applications`` replays of a captured
         application (the inner iteration counts a direct call records)."""
 
+    def discard(self, applications: int) -> None:
+        """Drop the book-keeping of the last ``applications`` direct calls
+        (the warm-up and capture calls of a cycle graph are not solves)."""
+
     def fixed_solves(self) -> bool:
         """True when the application is a sweep of fixed-iteration
         sine-transform block solves (large systems keep device cycles)."""
@@ -1314,6 +1318,8 @@ class _FgmresGraph:
         finally:
             if was:
                 gc.enable()
+        if P is not None:
+            P.discard(2)  # the warm-up and the captured application
         h = C.c_void_p()
         call("irk_fgmres_graph_create", ctx(), C.c_void_p(self.tg.raw_cuda_graph()), n, cycle,
              1 if reorth else 0, ptr(self.V), n, ptr(self.Z), n, ptr(self.vj), ptr(self.zj),
